@@ -1,0 +1,92 @@
+/*
+ * relief_gpu.h -- additive B200 entry points of librelief_b200.so.
+ *
+ * Nothing here exists in the reference; relief.h alone is the drop-in ABI.
+ * These calls expose what the GPU build adds on top of it:
+ *   - device selection and device-resident input (no host round trip),
+ *   - per-phase device timings under the reference's Table-I labels
+ *     (reference integration.hpp:119-126),
+ *   - the post-processing chain of the reference (postprocess.cpp:40-197)
+ *     run on the device map,
+ *   - the synthetic scan generator used by tests and bench.py (an independent
+ *     implementation of the reference simulator, sim.cpp:29-262).
+ * All calls follow relief.h's conventions: relief_status return values and a
+ * thread-local message behind relief_last_error().
+ */
+#ifndef RELIEF_GPU_H
+#define RELIEF_GPU_H
+
+#include "relief.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Number of CUDA devices visible to this process (0 when none). */
+RELIEF_API int relief_gpu_device_count(void);
+
+/* relief_map_create on an explicit CUDA device ordinal. */
+RELIEF_API relief_map* relief_gpu_map_create_on(int device, double resolution, int width,
+                                                int height, double center_x, double center_y);
+RELIEF_API int relief_gpu_map_device(const relief_map* map);
+
+/* relief_map_integrate with the point stream already in device memory of the
+ * map's device (d_xyz: 3*n doubles, x y z packed). Synchronous like the
+ * reference call: stats are final on return. */
+RELIEF_API relief_status relief_gpu_map_integrate_device(relief_map* map,
+                                                         const relief_config* config,
+                                                         const double* d_xyz, size_t n_points,
+                                                         const double pose[12], double stamp,
+                                                         relief_scan_stats* stats_out);
+
+/* Device time (seconds) of the last integrate call per phase, in the
+ * reference's Table-I order: point transform & z error count, drift
+ * compensation, height update & ray casting, overlap clearance,
+ * traversability, normal calculation, total. Phases fused into one kernel
+ * report their combined time under the first label and 0 for the others. */
+RELIEF_API relief_status relief_gpu_map_phase_seconds(const relief_map* map, double out[7]);
+
+/* Finer device-time breakdown of the last integrate call (seconds): host->device
+ * upload (+ recenter shift), ingest, drift, cell sort, gated fusion, ray
+ * casting, cell phases, total excluding the upload. */
+RELIEF_API relief_status relief_gpu_map_kernel_seconds(const relief_map* map, double out[8]);
+
+/* Kernel launches issued by the last integrate call (evidence for bench.py). */
+RELIEF_API int64_t relief_gpu_map_last_launches(const relief_map* map);
+
+/* Copies one masked layer (same semantics as relief_map_layer) into device
+ * memory of the map's device. */
+RELIEF_API relief_status relief_gpu_map_layer_device(const relief_map* map, const char* layer,
+                                                     double* d_out, size_t capacity);
+
+/* Post-processing chain (reference postprocess.hpp:28-44, postprocess.cpp:
+ * 40-197) on one masked layer of the map, computed on the device. kinds[s]:
+ * 0 gaussian, 1 box, 2 median, 3 min_inpaint; radii/sigmas as FilterStep.
+ * The map itself is not modified. values_out/valid_out are host buffers of
+ * width*height entries. */
+RELIEF_API relief_status relief_gpu_map_smooth_chain(const relief_map* map, const char* layer,
+                                                     const int* kinds, const int* radii,
+                                                     const double* sigmas, int n_steps,
+                                                     double* values_out, uint8_t* valid_out);
+
+/* Same chain on caller-supplied host data (values + 0/1 validity). */
+RELIEF_API relief_status relief_gpu_smooth_chain(const double* values, const uint8_t* valid,
+                                                 int width, int height, const int* kinds,
+                                                 const int* radii, const double* sigmas,
+                                                 int n_steps, double* values_out,
+                                                 uint8_t* valid_out);
+
+/* Synthetic scan: scene + sensor of a reliefmap config file, rendered from
+ * pose (row-major [R|t]) at `time` with splitmix64 stream (seed, scan_index)
+ * per ray. Returns the point count (only min(count, capacity) points are
+ * written), or -1 on error. Host code; matches the reference simulator
+ * bit for bit (tests/test_sim_parity.py). */
+RELIEF_API int64_t relief_gpu_sim_render(const char* config_path, const double pose[12],
+                                         double time, uint64_t seed, uint64_t scan_index,
+                                         double* xyz, int64_t capacity);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RELIEF_GPU_H */

@@ -1,0 +1,353 @@
+"""B200-native elevation-map update path of arXiv 2204.12876 (reliefmap drop-in).
+
+The product is ``lib/librelief_b200.so``: the reference's C ABI (``include/relief.h``)
+implemented as host C++ over hand-written sm_100a CUDA kernels, plus the additive
+``include/relief_gpu.h`` entry points. This module is a thin ctypes mirror of that ABI
+for Python callers (tests, bench.py); it mirrors the reference C API names, argument
+meaning and error behaviour (reference proj/include/relief/relief.h:37-129):
+
+    lib = load_library()
+    m = ReliefMap.create(lib, resolution=0.04, width=500, height=500)
+    stats = m.integrate(xyz, pose34, stamp, config=None)   # relief_map_integrate
+    elev = m.layer("elevation")                            # relief_map_layer
+
+There is no CPU fallback: loading fails loudly when the shared library is missing,
+and map creation fails when no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+PKG_DIR = Path(__file__).resolve().parent
+DEFAULT_LIB = PKG_DIR / "lib" / "librelief_b200.so"
+
+LAYER_NAMES = (
+    "elevation", "variance", "last_update", "upper_bound", "upper_bound_valid",
+    "traversability", "normal_x", "normal_y", "normal_z", "valid",
+)
+
+STATUS_NAMES = {
+    0: "OK", 1: "USAGE", 2: "DATA", 3: "OUT_OF_MAP", 4: "INVALID_POSE", 5: "INVALID_VARIANCE",
+    6: "INVALID_MODEL", 7: "DEGENERATE_PLANE", 8: "NOTHING_TO_INPAINT", 9: "OUT_OF_TRAJECTORY",
+    10: "PARSE", 11: "IO",
+}
+
+# Post-processing chain step kinds (relief_gpu.h).
+GAUSSIAN, BOX, MEDIAN, MIN_INPAINT = 0, 1, 2, 3
+
+
+class ScanStats(ctypes.Structure):
+    """relief_scan_stats (reference relief.h:89-102), ABI-fixed layout."""
+
+    _fields_ = [
+        ("points_in", ctypes.c_int64),
+        ("points_excluded", ctypes.c_int64),
+        ("points_out_of_range", ctypes.c_int64),
+        ("points_out_of_map", ctypes.c_int64),
+        ("points_rejected_outlier", ctypes.c_int64),
+        ("points_ignored_low", ctypes.c_int64),
+        ("points_fused", ctypes.c_int64),
+        ("cells_updated", ctypes.c_int64),
+        ("cells_removed_by_cleanup", ctypes.c_int64),
+        ("cells_cleared_by_overlap", ctypes.c_int64),
+        ("drift_offset_applied", ctypes.c_double),
+        ("total_seconds", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class ReliefError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_DP = ctypes.POINTER(ctypes.c_double)
+_I = ctypes.c_int
+_SZ = ctypes.c_size_t
+_CS = ctypes.c_char_p
+
+# Symbols of relief.h (the drop-in ABI) and their ctypes signatures.
+RELIEF_H_SIGNATURES = {
+    "relief_last_error": (_CS, []),
+    "relief_version": (_CS, []),
+    "relief_config_default": (_P, []),
+    "relief_config_load": (_P, [_CS]),
+    "relief_config_free": (None, [_P]),
+    "relief_config_set_mode": (_I, [_P, _CS]),
+    "relief_config_set_seed": (_I, [_P, ctypes.c_uint64]),
+    "relief_map_create": (_P, [_D, _I, _I, _D, _D]),
+    "relief_map_load": (_P, [_CS]),
+    "relief_map_save": (_I, [_P, _CS]),
+    "relief_map_free": (None, [_P]),
+    "relief_map_width": (_I, [_P]),
+    "relief_map_height": (_I, [_P]),
+    "relief_map_resolution": (_D, [_P]),
+    "relief_map_center": (_I, [_P, _DP, _DP]),
+    "relief_map_layer": (_I, [_P, _CS, _DP, _SZ]),
+    "relief_map_integrate": (_I, [_P, _P, _DP, _SZ, _DP, _D, ctypes.POINTER(ScanStats)]),
+    "relief_run_simulate": (_I, [_CS, _CS, ctypes.c_uint64, _I, _CS]),
+    "relief_run_replay": (_I, [_CS, ctypes.POINTER(_CS), _SZ, _CS, _CS, _CS]),
+    "relief_run_bench": (_I, [_CS, ctypes.POINTER(_SZ), _SZ, _I, _CS, _CS]),
+    "relief_run_export": (_I, [_CS, _CS, _CS, _CS]),
+    "relief_run_segment": (_I, [_CS, _CS, _CS, ctypes.POINTER(_SZ)]),
+}
+
+# Additive relief_gpu.h symbols.
+RELIEF_GPU_H_SIGNATURES = {
+    "relief_gpu_device_count": (_I, []),
+    "relief_gpu_map_create_on": (_P, [_I, _D, _I, _I, _D, _D]),
+    "relief_gpu_map_device": (_I, [_P]),
+    "relief_gpu_map_integrate_device": (_I, [_P, _P, ctypes.c_void_p, _SZ, _DP, _D, ctypes.POINTER(ScanStats)]),
+    "relief_gpu_map_phase_seconds": (_I, [_P, _DP]),
+    "relief_gpu_map_kernel_seconds": (_I, [_P, _DP]),
+    "relief_gpu_map_last_launches": (ctypes.c_int64, [_P]),
+    "relief_gpu_map_layer_device": (_I, [_P, _CS, ctypes.c_void_p, _SZ]),
+    "relief_gpu_map_smooth_chain": (_I, [_P, _CS, ctypes.POINTER(_I), ctypes.POINTER(_I), _DP, _I, _DP,
+                                         ctypes.POINTER(ctypes.c_uint8)]),
+    "relief_gpu_smooth_chain": (_I, [_DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, ctypes.POINTER(_I),
+                                     ctypes.POINTER(_I), _DP, _I, _DP, ctypes.POINTER(ctypes.c_uint8)]),
+    "relief_gpu_sim_render": (ctypes.c_int64, [_CS, _DP, _D, ctypes.c_uint64, ctypes.c_uint64, _DP,
+                                               ctypes.c_int64]),
+}
+
+
+def _bind(lib: ctypes.CDLL, table: dict) -> None:
+    for name, (res, args) in table.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def load_library(path: Optional[os.PathLike] = None, gpu_api: Optional[bool] = None) -> ctypes.CDLL:
+    """Loads a library exporting relief.h (this repo's product by default).
+
+    ``gpu_api`` binds relief_gpu.h too; it defaults to True for the product library.
+    Raises FileNotFoundError when the library is missing -- there is no fallback.
+    """
+    p = Path(path) if path is not None else DEFAULT_LIB
+    if not p.exists():
+        raise FileNotFoundError(
+            f"{p} not found: build it with `python -m paper_2204_12876_b200.build` "
+            "(the B200 path has no CPU fallback)")
+    lib = ctypes.CDLL(str(p), mode=ctypes.RTLD_LOCAL)
+    _bind(lib, RELIEF_H_SIGNATURES)
+    if gpu_api if gpu_api is not None else path is None:
+        _bind(lib, RELIEF_GPU_H_SIGNATURES)
+    lib._relief_path = str(p)
+    return lib
+
+
+def _check(lib, status: int) -> None:
+    if status != 0:
+        raise ReliefError(status, lib.relief_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+def pose34(R=None, t=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """Row-major 3x4 [R | t] as relief_map_integrate expects."""
+    R = np.eye(3) if R is None else np.asarray(R, dtype=np.float64)
+    out = np.zeros((3, 4), dtype=np.float64)
+    out[:, :3] = R
+    out[:, 3] = t
+    return np.ascontiguousarray(out.reshape(12))
+
+
+class Config:
+    """relief_config handle (reference relief.h:61-66)."""
+
+    def __init__(self, lib, handle):
+        self.lib = lib
+        self.handle = handle
+
+    @classmethod
+    def default(cls, lib) -> "Config":
+        h = lib.relief_config_default()
+        if not h:
+            raise ReliefError(2, lib.relief_last_error().decode())
+        return cls(lib, h)
+
+    @classmethod
+    def load(cls, lib, path) -> "Config":
+        h = lib.relief_config_load(str(path).encode())
+        if not h:
+            raise ReliefError(10, lib.relief_last_error().decode())
+        return cls(lib, h)
+
+    @classmethod
+    def from_text(cls, lib, text: str, path) -> "Config":
+        Path(path).write_text(text)
+        return cls.load(lib, path)
+
+    def set_mode(self, mode: str) -> None:
+        _check(self.lib, self.lib.relief_config_set_mode(self.handle, mode.encode()))
+
+    def set_seed(self, seed: int) -> None:
+        _check(self.lib, self.lib.relief_config_set_seed(self.handle, seed))
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.relief_config_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ReliefMap:
+    """relief_map handle: the device-resident elevation map."""
+
+    def __init__(self, lib, handle):
+        self.lib = lib
+        self.handle = handle
+
+    @classmethod
+    def create(cls, lib, resolution=0.04, width=250, height=250, center_x=0.0, center_y=0.0,
+               device: Optional[int] = None) -> "ReliefMap":
+        if device is None:
+            h = lib.relief_map_create(resolution, width, height, center_x, center_y)
+        else:
+            h = lib.relief_gpu_map_create_on(device, resolution, width, height, center_x, center_y)
+        if not h:
+            raise ReliefError(1, lib.relief_last_error().decode())
+        return cls(lib, h)
+
+    @classmethod
+    def load(cls, lib, path) -> "ReliefMap":
+        h = lib.relief_map_load(str(path).encode())
+        if not h:
+            raise ReliefError(10, lib.relief_last_error().decode())
+        return cls(lib, h)
+
+    def save(self, path) -> None:
+        _check(self.lib, self.lib.relief_map_save(self.handle, str(path).encode()))
+
+    @property
+    def width(self) -> int:
+        return self.lib.relief_map_width(self.handle)
+
+    @property
+    def height(self) -> int:
+        return self.lib.relief_map_height(self.handle)
+
+    @property
+    def resolution(self) -> float:
+        return self.lib.relief_map_resolution(self.handle)
+
+    def center(self):
+        x, y = ctypes.c_double(), ctypes.c_double()
+        _check(self.lib, self.lib.relief_map_center(self.handle, ctypes.byref(x), ctypes.byref(y)))
+        return x.value, y.value
+
+    def layer(self, name: str) -> np.ndarray:
+        out = np.empty(self.width * self.height, dtype=np.float64)
+        _check(self.lib, self.lib.relief_map_layer(self.handle, name.encode(), _dptr(out), out.size))
+        return out.reshape(self.height, self.width)
+
+    def layers(self) -> dict:
+        return {n: self.layer(n) for n in LAYER_NAMES}
+
+    def integrate(self, xyz, pose, stamp: float, config: Optional[Config] = None) -> ScanStats:
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1)
+        pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+        st = ScanStats()
+        status = self.lib.relief_map_integrate(
+            self.handle, config.handle if config is not None else None,
+            _dptr(xyz) if xyz.size else None, xyz.size // 3, _dptr(pose), stamp, ctypes.byref(st))
+        _check(self.lib, status)
+        return st
+
+    def integrate_device(self, d_xyz_ptr: int, n: int, pose, stamp: float,
+                         config: Optional[Config] = None) -> ScanStats:
+        """relief_gpu_map_integrate_device: points already in device memory."""
+        pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+        st = ScanStats()
+        status = self.lib.relief_gpu_map_integrate_device(
+            self.handle, config.handle if config is not None else None, ctypes.c_void_p(d_xyz_ptr), n,
+            _dptr(pose), stamp, ctypes.byref(st))
+        _check(self.lib, status)
+        return st
+
+    def phase_seconds(self) -> np.ndarray:
+        out = np.zeros(7, dtype=np.float64)
+        _check(self.lib, self.lib.relief_gpu_map_phase_seconds(self.handle, _dptr(out)))
+        return out
+
+    def kernel_seconds(self) -> np.ndarray:
+        """[upload, ingest, drift, sort, fusion, rays, cell phases, total excl. upload]."""
+        out = np.zeros(8, dtype=np.float64)
+        _check(self.lib, self.lib.relief_gpu_map_kernel_seconds(self.handle, _dptr(out)))
+        return out
+
+    def last_launches(self) -> int:
+        return int(self.lib.relief_gpu_map_last_launches(self.handle))
+
+    def smooth_chain(self, layer: str, steps: Sequence[tuple]):
+        """steps: (kind, radius, sigma) tuples; returns (values, valid)."""
+        n = self.width * self.height
+        kinds = (ctypes.c_int * len(steps))(*[s[0] for s in steps])
+        radii = (ctypes.c_int * len(steps))(*[s[1] for s in steps])
+        sig = (ctypes.c_double * len(steps))(*[float(s[2]) for s in steps])
+        vals = np.empty(n, dtype=np.float64)
+        ok = np.empty(n, dtype=np.uint8)
+        _check(self.lib, self.lib.relief_gpu_map_smooth_chain(
+            self.handle, layer.encode(), kinds, radii, sig, len(steps), _dptr(vals),
+            ok.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+        return vals.reshape(self.height, self.width), ok.reshape(self.height, self.width)
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.relief_map_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def smooth_chain(lib, values: np.ndarray, valid: np.ndarray, steps: Sequence[tuple]):
+    """relief_gpu_smooth_chain on host arrays; returns (values, valid)."""
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    valid = np.ascontiguousarray(valid, dtype=np.uint8)
+    H, W = values.shape
+    kinds = (ctypes.c_int * len(steps))(*[s[0] for s in steps])
+    radii = (ctypes.c_int * len(steps))(*[s[1] for s in steps])
+    sig = (ctypes.c_double * len(steps))(*[float(s[2]) for s in steps])
+    vo = np.empty_like(values)
+    ko = np.empty_like(valid)
+    u8 = ctypes.POINTER(ctypes.c_uint8)
+    _check(lib, lib.relief_gpu_smooth_chain(_dptr(values), valid.ctypes.data_as(u8), W, H, kinds, radii,
+                                            sig, len(steps), _dptr(vo), ko.ctypes.data_as(u8)))
+    return vo, ko
+
+
+def sim_render(lib, config_path, pose, time: float, seed: int, scan_index: int,
+               capacity: int = 1 << 22) -> np.ndarray:
+    """Synthetic scan from a reliefmap config (relief_gpu_sim_render); (n, 3) float64."""
+    pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+    buf = np.empty(capacity * 3, dtype=np.float64)
+    n = lib.relief_gpu_sim_render(str(config_path).encode(), _dptr(pose), time, seed, scan_index,
+                                  _dptr(buf), capacity)
+    if n < 0:
+        raise ReliefError(2, lib.relief_last_error().decode())
+    if n > capacity:
+        return sim_render(lib, config_path, pose, time, seed, scan_index, capacity=int(n))
+    return buf[: 3 * n].reshape(n, 3).copy()

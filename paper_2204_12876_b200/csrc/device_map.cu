@@ -1,0 +1,230 @@
+// Device map lifecycle: allocation, fresh fill, layer export, snapshot
+// upload/download.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "device_map.hpp"
+
+namespace rb200 {
+
+void checkCuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(Err::kDevice, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+GridArgs gridArgs(const Grid& g) {
+  GridArgs a;
+  a.W = g.width;
+  a.H = g.height;
+  a.res = g.resolution;
+  a.ox = g.originX();
+  a.oy = g.originY();
+  a.xmax = a.ox + g.width * g.resolution;
+  a.ymax = a.oy + g.height * g.resolution;
+  return a;
+}
+
+namespace {
+
+constexpr std::size_t kAlign = 256;
+inline std::size_t alignUp(std::size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+// Carves typed arrays out of one allocation.
+struct Carver {
+  char* base;
+  std::size_t off = 0;
+  template <typename T>
+  T* take(std::size_t n) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off = alignUp(off + n * sizeof(T));
+    return p;
+  }
+};
+
+std::size_t layerBytes(std::size_t n) { return 8 * alignUp(n * 8) + 2 * alignUp(n); }
+
+void carveLayers(Carver& c, Layers& L, std::size_t n) {
+  L.elev = c.take<double>(n);
+  L.var = c.take<double>(n);
+  L.last = c.take<double>(n);
+  L.ub = c.take<double>(n);
+  L.trav = c.take<double>(n);
+  L.nx = c.take<double>(n);
+  L.ny = c.take<double>(n);
+  L.nz = c.take<double>(n);
+  L.valid = c.take<uint8_t>(n);
+  L.ubv = c.take<uint8_t>(n);
+}
+
+__global__ void k_fill_fresh(Layers L, std::size_t n, int32_t* kstar) {
+  const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  L.elev[i] = nan;
+  L.var[i] = nan;
+  L.last[i] = 0.0;
+  L.ub[i] = __longlong_as_double(0x7ff0000000000000LL);
+  L.trav[i] = 0.0;
+  L.nx[i] = 0.0;
+  L.ny[i] = 0.0;
+  L.nz[i] = 0.0;
+  L.valid[i] = 0;
+  L.ubv[i] = 0;
+  kstar[i] = INT_MAX;
+}
+
+// Layer ids for the masked export; order = reference snapshot.cpp:43-48.
+enum LayerId { kElev, kVar, kLast, kUb, kUbv, kTrav, kNx, kNy, kNz, kValid };
+
+__global__ void k_export(Layers L, std::size_t n, int which, double* out) {
+  const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  const bool v = L.valid[i] != 0;
+  double r;
+  switch (which) {
+    case kElev: r = v ? L.elev[i] : nan; break;
+    case kVar: r = v ? L.var[i] : nan; break;
+    case kLast: r = v ? L.last[i] : nan; break;
+    case kUb: r = L.ubv[i] ? L.ub[i] : nan; break;
+    case kUbv: r = L.ubv[i] ? 1.0 : 0.0; break;
+    case kTrav: r = v ? L.trav[i] : nan; break;
+    case kNx: r = v ? L.nx[i] : nan; break;
+    case kNy: r = v ? L.ny[i] : nan; break;
+    case kNz: r = v ? L.nz[i] : nan; break;
+    default: r = v ? 1.0 : 0.0; break;
+  }
+  out[i] = r;
+}
+
+int layerId(const char* name) {
+  static const char* names[] = {"elevation",      "variance", "last_update", "upper_bound",
+                                "upper_bound_valid", "traversability", "normal_x", "normal_y",
+                                "normal_z",       "valid"};
+  for (int k = 0; k < 10; ++k)
+    if (std::strcmp(name, names[k]) == 0) return k;
+  return -1;
+}
+
+}  // namespace
+
+DeviceMap* createDeviceMap(int device, const Grid& grid) {
+  grid.validate();
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(Err::kDevice, "no CUDA device available: librelief_b200 has no CPU fallback");
+  }
+  if (device < 0 || device >= count) fail(Err::kUsage, "CUDA device ordinal out of range");
+  checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  auto* m = new DeviceMap();
+  m->device = device;
+  m->grid = grid;
+  try {
+    checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
+    for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
+    const std::size_t n = grid.cells();
+    const std::size_t bytes = 2 * layerBytes(n) + 2 * alignUp(n * 4) + alignUp((n + 1) * 4) +
+                              alignUp(n) + 4 * kAlign;
+    checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
+    Carver c{static_cast<char*>(m->slab)};
+    carveLayers(c, m->cur, n);
+    carveLayers(c, m->alt, n);
+    m->count = c.take<int32_t>(n);
+    m->kstar = c.take<int32_t>(n);
+    m->start = c.take<uint32_t>(n + 1);
+    m->cls = c.take<uint8_t>(n);
+    checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
+    checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
+    checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
+    fillFresh(*m);
+    checkCuda(cudaStreamSynchronize(m->stream), "map init");
+  } catch (...) {
+    destroyDeviceMap(m);
+    throw;
+  }
+  return m;
+}
+
+void destroyDeviceMap(DeviceMap* m) {
+  if (m == nullptr) return;
+  cudaSetDevice(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  cudaFree(m->slab);
+  cudaFree(m->pslab);
+  cudaFree(m->rslab);
+  cudaFree(m->export_buf);
+  cudaFree(m->hist);
+  cudaFree(m->stats);
+  cudaFree(m->drift_offset);
+  if (m->h_stats) cudaFreeHost(m->h_stats);
+  for (auto& e : m->ev)
+    if (e) cudaEventDestroy(e);
+  if (m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+}
+
+void fillFresh(DeviceMap& m) {
+  const std::size_t n = m.grid.cells();
+  k_fill_fresh<<<static_cast<unsigned>((n + 255) / 256), 256, 0, m.stream>>>(m.cur, n, m.kstar);
+  checkCuda(cudaGetLastError(), "fill launch");
+}
+
+void ensurePointCapacity(DeviceMap& m, std::size_t n) {
+  if (n <= m.cap && m.pslab != nullptr) return;
+  std::size_t cap = 1 << 16;
+  while (cap < n) cap <<= 1;
+  cudaFree(m.pslab);
+  m.pslab = nullptr;
+  const std::size_t bytes = alignUp(cap * 24) + 4 * alignUp(cap * 8) + 5 * alignUp(cap * 4) +
+                            alignUp(cap) + 8 * kAlign;
+  checkCuda(cudaMalloc(&m.pslab, bytes), "point scratch allocation");
+  Carver c{static_cast<char*>(m.pslab)};
+  m.xyz_in = c.take<double>(cap * 3);
+  m.px = c.take<double>(cap);
+  m.py = c.take<double>(cap);
+  m.pz = c.take<double>(cap);
+  m.pvar = c.take<double>(cap);
+  m.key0 = c.take<uint32_t>(cap);
+  m.key1 = c.take<uint32_t>(cap);
+  m.val0 = c.take<uint32_t>(cap);
+  m.val1 = c.take<uint32_t>(cap);
+  m.raylist = c.take<uint32_t>(cap);
+  m.kept = c.take<uint8_t>(cap);
+  m.cap = cap;
+}
+
+bool exportLayerDevice(DeviceMap& m, const char* name, double* d_out) {
+  const int id = layerId(name);
+  if (id < 0) return false;
+  const std::size_t n = m.grid.cells();
+  k_export<<<static_cast<unsigned>((n + 255) / 256), 256, 0, m.stream>>>(m.cur, n, id, d_out);
+  checkCuda(cudaGetLastError(), "export launch");
+  return true;
+}
+
+void uploadLayers(DeviceMap& m, const double* const host[8], const uint8_t* valid,
+                  const uint8_t* ubv) {
+  const std::size_t n = m.grid.cells();
+  double* dst[8] = {m.cur.elev, m.cur.var, m.cur.last, m.cur.ub,
+                    m.cur.trav, m.cur.nx,  m.cur.ny,   m.cur.nz};
+  for (int k = 0; k < 8; ++k)
+    checkCuda(cudaMemcpyAsync(dst[k], host[k], n * 8, cudaMemcpyHostToDevice, m.stream), "upload");
+  checkCuda(cudaMemcpyAsync(m.cur.valid, valid, n, cudaMemcpyHostToDevice, m.stream), "upload");
+  checkCuda(cudaMemcpyAsync(m.cur.ubv, ubv, n, cudaMemcpyHostToDevice, m.stream), "upload");
+  checkCuda(cudaStreamSynchronize(m.stream), "upload sync");
+}
+
+void downloadLayers(const DeviceMap& m, double* const host[8], uint8_t* valid, uint8_t* ubv) {
+  const std::size_t n = m.grid.cells();
+  const double* src[8] = {m.cur.elev, m.cur.var, m.cur.last, m.cur.ub,
+                          m.cur.trav, m.cur.nx,  m.cur.ny,   m.cur.nz};
+  for (int k = 0; k < 8; ++k)
+    checkCuda(cudaMemcpyAsync(host[k], src[k], n * 8, cudaMemcpyDeviceToHost, m.stream), "download");
+  checkCuda(cudaMemcpyAsync(valid, m.cur.valid, n, cudaMemcpyDeviceToHost, m.stream), "download");
+  checkCuda(cudaMemcpyAsync(ubv, m.cur.ubv, n, cudaMemcpyDeviceToHost, m.stream), "download");
+  checkCuda(cudaStreamSynchronize(m.stream), "download sync");
+}
+
+}  // namespace rb200

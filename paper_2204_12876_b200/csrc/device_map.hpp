@@ -1,0 +1,150 @@
+// Device-resident elevation map and the per-scan launch plan.
+//
+// HBM layout: structure of arrays, one contiguous
+// 256-byte aligned array per layer, row-major r*W + c, exactly the layer set
+// of the reference map (reference grid.hpp:90-101):
+//   f64  elevation, variance, last_update, upper_bound, traversability,
+//        normal_x, normal_y, normal_z
+//   u8   valid, upper_bound_valid
+// = 66 B/cell persistent. The persistent layers are double buffered so a
+// robot-centric recenter is one streaming copy (cur -> alt, then swap).
+// Per-scan scratch: i32 point count + segment start, u8 ray class, i32 k*.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "relief_internal.hpp"
+
+namespace rb200 {
+
+struct Layers {
+  double* elev = nullptr;
+  double* var = nullptr;
+  double* last = nullptr;
+  double* ub = nullptr;
+  double* trav = nullptr;
+  double* nx = nullptr;
+  double* ny = nullptr;
+  double* nz = nullptr;
+  uint8_t* valid = nullptr;
+  uint8_t* ubv = nullptr;
+};
+
+// Counters written by the kernels; copied to the host once per scan.
+struct DevStats {
+  unsigned long long out_of_range;
+  unsigned long long excluded;
+  unsigned long long out_of_map;
+  unsigned long long outlier;
+  unsigned long long ignored_low;
+  unsigned long long fused;
+  unsigned long long cells_updated;
+  unsigned long long removed;
+  unsigned long long overlap_cleared;
+  unsigned long long candidate_rays;  // rays queued for the k* pass
+  double drift_offset;                // applied offset (0 when not applied)
+  int drift_n;
+  int drift_clamped;
+  int error_code;                     // 0 ok, 1 non-positive variance
+  int pad;
+};
+
+// Geometry + parameters passed by value to kernels.
+struct GridArgs {
+  int W, H;
+  double res;
+  double ox, oy;      // origin = center - extent/2
+  double xmax, ymax;  // ox + W*res, oy + H*res
+};
+
+struct DeviceMap {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Grid grid;
+  Layers cur, alt;
+  void* slab = nullptr;  // backing allocation of both layer sets + cell scratch
+  // per-cell scratch
+  int32_t* count = nullptr;
+  uint32_t* start = nullptr;
+  uint8_t* cls = nullptr;
+  int32_t* kstar = nullptr;
+  // per-point scratch (grown on demand)
+  std::size_t cap = 0;
+  void* pslab = nullptr;
+  double* xyz_in = nullptr;  // device copy of the caller's points
+  double* px = nullptr;
+  double* py = nullptr;
+  double* pz = nullptr;
+  double* pvar = nullptr;
+  uint32_t* key0 = nullptr;
+  uint32_t* key1 = nullptr;
+  uint32_t* val0 = nullptr;
+  uint32_t* val1 = nullptr;
+  uint32_t* raylist = nullptr;
+  uint8_t* kept = nullptr;
+  // reduction scratch
+  void* rslab = nullptr;
+  std::size_t rcap = 0;
+  double* drift_sum_part = nullptr;
+  int* drift_n_part = nullptr;
+  uint32_t* hist = nullptr;
+  uint32_t* scan_part = nullptr;
+  std::size_t hist_cap = 0;
+  DevStats* stats = nullptr;     // device
+  DevStats* h_stats = nullptr;   // pinned host mirror
+  double* drift_offset = nullptr;  // device scalar
+  // host-side bookkeeping
+  double last_stamp = 0.0;
+  bool has_last = false;
+  double* export_buf = nullptr;  // masked-layer staging for get_layer
+  cudaEvent_t ev[8] = {};
+  double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
+  double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
+  long long last_launches = 0;
+};
+
+GridArgs gridArgs(const Grid& g);
+
+// Lifecycle (device_map.cu).
+DeviceMap* createDeviceMap(int device, const Grid& grid);
+void destroyDeviceMap(DeviceMap* m);
+void ensurePointCapacity(DeviceMap& m, std::size_t n);
+void fillFresh(DeviceMap& m);  // reference grid.cpp:24-39 fill values
+void checkCuda(cudaError_t e, const char* what);
+
+// Masked export of one named layer into device memory (reference
+// snapshot.cpp:50-77). Returns false for an unknown layer name.
+bool exportLayerDevice(DeviceMap& m, const char* name, double* d_out);
+// Raw (unmasked) upload / download of the ten persistent layers, used by
+// snapshot load / save. host arrays are W*H each in the order of kLayerNames.
+void uploadLayers(DeviceMap& m, const double* const host[8], const uint8_t* valid,
+                  const uint8_t* ubv);
+void downloadLayers(const DeviceMap& m, double* const host[8], uint8_t* valid, uint8_t* ubv);
+
+// Whole per-scan pipeline (pipeline.cu).
+struct ScanResult {
+  std::int64_t points_in = 0, excluded = 0, out_of_range = 0, out_of_map = 0, outlier = 0,
+               ignored_low = 0, fused = 0, cells_updated = 0, removed = 0, overlap_cleared = 0;
+  double drift_offset = 0.0;
+  bool drift_clamped = false;
+  int drift_points = 0;
+  double seconds = 0.0;
+};
+ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& params, const double* xyz,
+                               std::size_t n, bool xyz_on_device, const Pose& pose,
+                               double stamp, double dt);
+
+// Post-processing chain on a masked layer held in device memory (postchain.cu).
+struct ChainStep {
+  int kind;  // 0 gaussian, 1 box, 2 median, 3 min_inpaint
+  int radius;
+  double sigma;
+};
+void smoothChainDevice(int device, cudaStream_t stream, const double* d_values,
+                       const uint8_t* d_valid, int W, int H, const ChainStep* steps, int n_steps,
+                       double* d_values_out, uint8_t* d_valid_out);
+
+}  // namespace rb200

@@ -1,0 +1,1095 @@
+// The per-scan update path on the device: input_pointcloud / move_to /
+// update_variance of the paper, reproducing the reference's deterministic
+// integrateScan (reference integration.cpp:70-260) bit for bit.
+//
+// Launch plan per scan:
+//   K4a k_shift          recenter: streaming copy of the 10 persistent layers
+//   K1  k_ingest         range / exclusion / transform / sigma_p^2 / cell /
+//                        drift vote / per-cell count      (one thread per point)
+//       k_drift_finalize fixed-order reduction of the drift vote (1 block)
+//   K4b k_apply_offset   drift offset on valid heights and finite bounds
+//   K2  radix sort       stable LSD sort of (cell, point) -> per-cell segments
+//                        in scan order; exclusive scan count -> segment start
+//   K3  k_fuse           gated Kalman fold, one thread per occupied cell
+//       k_classify       per-cell ray class (nothing / bound / removal candidate)
+//   K5  k_rays_pass1     exact 2-D DDA per kept point: bounds of invalid cells,
+//                        k* = first removing ray per candidate cell
+//       k_remove         invalidate cells with k* < inf
+//   K6  k_rays_pass2     bounds of removed cells from rays k >= k*
+//   K7  k_cells          overlap clearance + normals + traversability + time
+//                        variance, one shared-memory tile with a halo
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "device_map.hpp"
+#include "fp_exact.cuh"
+
+namespace rb200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr double kInf = __builtin_huge_val();
+
+__device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+template <typename T>
+__device__ __forceinline__ T warpSum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Invalidate one cell (reference grid.cpp:126-137).
+__device__ __forceinline__ void invalidateCell(const Layers& L, size_t i) {
+  L.valid[i] = 0;
+  L.elev[i] = dnan();
+  L.var[i] = dnan();
+  L.last[i] = 0.0;
+  L.trav[i] = 0.0;
+  L.nx[i] = 0.0;
+  L.ny[i] = 0.0;
+  L.nz[i] = 0.0;
+  L.ub[i] = dinf();
+  L.ubv[i] = 0;
+}
+
+// ------------------------------------------------------------- K4a shift
+// out[r][c] = in[r+dr][c+dc], exposed cells get the fresh fill
+// (reference grid.cpp:70-111).
+__global__ void __launch_bounds__(kThreads) k_shift(Layers in, Layers out, int W, int H, int dc,
+                                                    int dr) {
+  const size_t n = static_cast<size_t>(W) * H;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / W);
+    const int c = static_cast<int>(i - static_cast<size_t>(r) * W);
+    const int sr = r + dr, sc = c + dc;
+    if (sr >= 0 && sr < H && sc >= 0 && sc < W) {
+      const size_t j = static_cast<size_t>(sr) * W + sc;
+      out.elev[i] = in.elev[j];
+      out.var[i] = in.var[j];
+      out.last[i] = in.last[j];
+      out.ub[i] = in.ub[j];
+      out.trav[i] = in.trav[j];
+      out.nx[i] = in.nx[j];
+      out.ny[i] = in.ny[j];
+      out.nz[i] = in.nz[j];
+      out.valid[i] = in.valid[j];
+      out.ubv[i] = in.ubv[j];
+    } else {
+      out.elev[i] = dnan();
+      out.var[i] = dnan();
+      out.last[i] = 0.0;
+      out.ub[i] = dinf();
+      out.trav[i] = 0.0;
+      out.nx[i] = 0.0;
+      out.ny[i] = 0.0;
+      out.nz[i] = 0.0;
+      out.valid[i] = 0;
+      out.ubv[i] = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------- K1 ingest
+struct IngestArgs {
+  GridArgs g;
+  double R[9];
+  double t[3];
+  double max_range2;
+  int excl_enabled;
+  double excl_b, excl_c, excl_dmax, excl_tan;
+  double alpha_d, sigma_p_min2;
+  int drift_enabled;
+  double drift_thr;
+};
+
+// Per point (reference integration.cpp:85-113,134-140; sensing.cpp:32-41;
+// drift.cpp:24-42; grid.cpp:41-47): fate, map-frame point, sigma_p^2, cell,
+// drift vote against the pre-fusion map, per-cell point count.
+__global__ void __launch_bounds__(kThreads)
+    k_ingest(const double* __restrict__ xyz, uint32_t n, IngestArgs a, Layers L,
+             int32_t* __restrict__ count, double* __restrict__ px, double* __restrict__ py,
+             double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
+             uint8_t* __restrict__ kept, double* __restrict__ drift_part,
+             int* __restrict__ drift_npart, DevStats* st) {
+  const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  int oor = 0, exc = 0, oom = 0, dn = 0;
+  double ds = 0.0;
+  uint32_t cell = WH;
+  if (k < n) {
+    const double x = xyz[3 * static_cast<size_t>(k)];
+    const double y = xyz[3 * static_cast<size_t>(k) + 1];
+    const double z = xyz[3 * static_cast<size_t>(k) + 2];
+    const double sq = (x * x + y * y) + z * z;
+    bool keep = false;
+    if (sq > a.max_range2) {
+      oor = 1;
+    } else if (a.excl_enabled &&
+               z > smin(a.excl_dmax,
+                        a.excl_b + smax(0.0, libm_hypot(x, y) - a.excl_c) * a.excl_tan)) {
+      exc = 1;
+    } else {
+      keep = true;
+    }
+    if (keep) {
+      const double mx = ((a.R[0] * x + a.R[1] * y) + a.R[2] * z) + a.t[0];
+      const double my = ((a.R[3] * x + a.R[4] * y) + a.R[5] * z) + a.t[1];
+      const double mz = ((a.R[6] * x + a.R[7] * y) + a.R[8] * z) + a.t[2];
+      const double d = sqrt(sq);
+      px[k] = mx;
+      py[k] = my;
+      pz[k] = mz;
+      pvar[k] = smax(a.alpha_d * d * d, a.sigma_p_min2);
+      const int col = x86_to_int(floor((mx - a.g.ox) / a.g.res));
+      const int row = x86_to_int(floor((my - a.g.oy) / a.g.res));
+      if (col >= 0 && col < a.g.W && row >= 0 && row < a.g.H) {
+        cell = static_cast<uint32_t>(row) * a.g.W + col;
+        if (a.drift_enabled && L.valid[cell] && !(L.trav[cell] <= a.drift_thr)) {
+          ds = mz - L.elev[cell];
+          dn = 1;
+        }
+      } else {
+        oom = 1;
+      }
+    }
+    key[k] = cell;
+    kept[k] = keep ? 1 : 0;
+  }
+  // Per-cell point count, one atomic per run of equal cells in the warp.
+  const unsigned peers = __match_any_sync(0xffffffffu, cell);
+  if (cell < WH && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
+
+  // Fixed-shape block reduction: deterministic drift partial per block.
+  __shared__ double s_sum[kThreads / 32];
+  __shared__ int s_cnt[4][kThreads / 32];
+  ds = warpSum(ds);
+  dn = warpSum(dn);
+  oor = warpSum(oor);
+  exc = warpSum(exc);
+  oom = warpSum(oom);
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_sum[warp] = ds;
+    s_cnt[0][warp] = dn;
+    s_cnt[1][warp] = oor;
+    s_cnt[2][warp] = exc;
+    s_cnt[3][warp] = oom;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bs = s_sum[0];
+    int c0 = s_cnt[0][0], c1 = s_cnt[1][0], c2 = s_cnt[2][0], c3 = s_cnt[3][0];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      bs += s_sum[w];
+      c0 += s_cnt[0][w];
+      c1 += s_cnt[1][w];
+      c2 += s_cnt[2][w];
+      c3 += s_cnt[3][w];
+    }
+    drift_part[blockIdx.x] = bs;
+    drift_npart[blockIdx.x] = c0;
+    if (c1) atomicAdd(&st->out_of_range, static_cast<unsigned long long>(c1));
+    if (c2) atomicAdd(&st->excluded, static_cast<unsigned long long>(c2));
+    if (c3) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c3));
+  }
+}
+
+// ------------------------------------------------------ drift (one block)
+// Mean error over the votes and the clamped offset (reference drift.cpp:24-55,
+// integration.cpp:119-128). Sums run in a fixed tree, so the result is
+// run-to-run deterministic; it differs from the sequential sum only in the
+// last bits.
+__global__ void __launch_bounds__(1024)
+    k_drift_finalize(const double* part, const int* npart, int nblocks, int min_points,
+                     double max_off, double* offset_out, DevStats* st) {
+  __shared__ double s_sum[32];
+  __shared__ long long s_cnt[32];
+  double s = 0.0;
+  long long c = 0;
+  for (int b = threadIdx.x; b < nblocks; b += 1024) {
+    s += part[b];
+    c += npart[b];
+  }
+  s = warpSum(s);
+  c = warpSum(c);
+  if ((threadIdx.x & 31) == 0) {
+    s_sum[threadIdx.x >> 5] = s;
+    s_cnt[threadIdx.x >> 5] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = s_sum[0];
+    long long cnt = s_cnt[0];
+    for (int w = 1; w < 32; ++w) {
+      total += s_sum[w];
+      cnt += s_cnt[w];
+    }
+    const int nvote = static_cast<int>(cnt);
+    double off = 0.0;
+    if (nvote >= min_points) {
+      const double mean = total / nvote;
+      off = sclamp(mean, -max_off, max_off);
+      st->drift_offset = off;
+      st->drift_clamped = off != mean;
+      st->drift_n = nvote;
+    }
+    *offset_out = off;
+  }
+}
+
+// Reference drift.cpp:44-55.
+__global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, const double* off_p) {
+  const double off = *off_p;
+  if (off == 0.0) return;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (L.valid[i]) L.elev[i] += off;
+    if (L.ubv[i]) L.ub[i] += off;
+  }
+}
+
+// ------------------------------------------------ K2 stable radix sort
+// LSD radix sort of 32-bit cell keys carrying the point index. Tiles of
+// 4096 keys; per pass: tile digit histograms -> exclusive scan (digit-major,
+// tile-minor) -> stable scatter, ranking inside the tile with per-warp
+// counters and __match_any_sync. Stability across passes keeps scan order
+// within each cell, which is what the gated fold needs.
+constexpr int kSortItems = 16;
+constexpr int kTile = kThreads * kSortItems;
+
+__global__ void __launch_bounds__(kThreads)
+    k_radix_hist(const uint32_t* __restrict__ keys, uint32_t n, int shift, int bits,
+                 uint32_t* __restrict__ hist, uint32_t ntiles) {
+  extern __shared__ uint32_t sh[];
+  const int buckets = 1 << bits;
+  const uint32_t mask = buckets - 1;
+  for (int i = threadIdx.x; i < buckets; i += kThreads) sh[i] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kTile;
+#pragma unroll 4
+  for (int j = 0; j < kSortItems; ++j) {
+    const uint32_t idx = base + j * kThreads + threadIdx.x;
+    const uint32_t d = idx < n ? (keys[idx] >> shift) & mask : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[d], __popc(peers));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < buckets; i += kThreads) hist[static_cast<size_t>(i) * ntiles + blockIdx.x] = sh[i];
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                    uint32_t n, int shift, int bits, const uint32_t* __restrict__ offsets,
+                    uint32_t ntiles, uint32_t* __restrict__ keys_out,
+                    uint32_t* __restrict__ vals_out, int first_pass, int write_keys) {
+  extern __shared__ uint16_t wcnt[];  // [8 warps][buckets]
+  const int buckets = 1 << bits;
+  const uint32_t mask = buckets - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 8 * buckets; i += kThreads) wcnt[i] = 0;
+  __syncthreads();
+  uint16_t* my = wcnt + warp * buckets;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t wbase = blockIdx.x * kTile + warp * (kTile / 8);
+  uint32_t key[kSortItems], val[kSortItems];
+  uint16_t rank[kSortItems];
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    const uint32_t idx = wbase + r * 32 + lane;
+    const bool ok = idx < n;
+    key[r] = ok ? keys_in[idx] : 0xffffffffu;
+    val[r] = ok ? (first_pass ? idx : vals_in[idx]) : 0u;
+    const uint32_t d = ok ? (key[r] >> shift) & mask : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    uint16_t before = 0;
+    if (ok) before = my[d];
+    __syncwarp();
+    rank[r] = before + __popc(peers & lt);
+    if (ok && lane == __ffs(peers) - 1) my[d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // Exclusive prefix over warps per digit.
+  for (int d = threadIdx.x; d < buckets; d += kThreads) {
+    uint16_t run = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint16_t t = wcnt[w * buckets + d];
+      wcnt[w * buckets + d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    if (key[r] == 0xffffffffu && wbase + r * 32 + lane >= n) continue;
+    const uint32_t d = (key[r] >> shift) & mask;
+    const uint32_t pos = offsets[static_cast<size_t>(d) * ntiles + blockIdx.x] + my[d] + rank[r];
+    if (write_keys) keys_out[pos] = key[r];
+    vals_out[pos] = val[r];
+  }
+}
+
+// Exclusive scan of u32 (three kernels: tile sums, scan of tile sums, tile
+// rescans). Used for radix offsets and for cell segment starts.
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t s_warp[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) wpre += s_warp[w];
+    tot += s_warp[w];
+  }
+  __syncthreads();
+  *total = tot;
+  return wpre + incl - v;
+}
+
+__global__ void __launch_bounds__(kThreads) k_scan_reduce(const uint32_t* __restrict__ in, size_t n,
+                                                          uint32_t* __restrict__ part) {
+  const size_t base = blockIdx.x * static_cast<size_t>(kScanTile);
+  uint32_t s = 0;
+  for (int j = 0; j < kScanItems; ++j) {
+    const size_t idx = base + j * kThreads + threadIdx.x;
+    if (idx < n) s += in[idx];
+  }
+  s = warpSum(s);
+  __shared__ uint32_t sw[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += sw[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_scan_top(uint32_t* part, int nparts) {
+  uint32_t carry = 0;
+  for (int base = 0; base < nparts; base += kThreads) {
+    const int i = base + threadIdx.x;
+    const uint32_t v = i < nparts ? part[i] : 0;
+    uint32_t total;
+    const uint32_t ex = blockExclusiveScan(v, &total);
+    if (i < nparts) part[i] = carry + ex;
+    carry += total;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_scan_down(const uint32_t* __restrict__ in, size_t n, const uint32_t* __restrict__ part,
+                uint32_t* __restrict__ out, uint32_t* __restrict__ total_out) {
+  __shared__ uint32_t tile[kScanTile];
+  const size_t base = blockIdx.x * static_cast<size_t>(kScanTile);
+  for (int j = 0; j < kScanItems; ++j) {
+    const size_t idx = base + j * kThreads + threadIdx.x;
+    tile[j * kThreads + threadIdx.x] = idx < n ? in[idx] : 0u;
+  }
+  __syncthreads();
+  uint32_t loc[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    loc[j] = s;
+    s += tile[threadIdx.x * kScanItems + j];
+  }
+  uint32_t block_total;
+  const uint32_t ex = blockExclusiveScan(s, &block_total) + part[blockIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) tile[threadIdx.x * kScanItems + j] = ex + loc[j];
+  __syncthreads();
+  for (int j = 0; j < kScanItems; ++j) {
+    const size_t idx = base + j * kThreads + threadIdx.x;
+    if (idx < n) out[idx] = tile[j * kThreads + threadIdx.x];
+  }
+  if (total_out != nullptr && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
+    *total_out = part[blockIdx.x] + block_total;
+}
+
+// ------------------------------------------------------------- K3 fusion
+struct FuseArgs {
+  double now;
+  double sigma_init2, sigma_outlier2, sigma_max2, maha;
+  int wall;
+};
+
+// Gated Kalman fold (reference integration.cpp:40-55,142-203, grid.cpp:139-147):
+// one thread per occupied cell walks that cell's points in scan order.
+__global__ void __launch_bounds__(kThreads)
+    k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
+           const uint32_t* __restrict__ start, const uint32_t* __restrict__ order,
+           const double* __restrict__ pz, const double* __restrict__ pvar, FuseArgs a,
+           DevStats* st) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const int cnt = i < ncell ? count[i] : 0;
+  unsigned long long nf = 0, no = 0, ni = 0, upd = 0;
+  if (cnt > 0) {
+    bool valid = L.valid[i] != 0;
+    double h = L.elev[i], v = L.var[i];
+    bool fused_any = false, var_changed = false;
+    const uint32_t s0 = start[i];
+    for (int j = 0; j < cnt; ++j) {
+      const uint32_t k = order[s0 + j];
+      const double z = pz[k];
+      const double sp = pvar[k];
+      const double ch = valid ? h : z;
+      const double cv = valid ? v : a.sigma_init2;
+      if (cv <= 0.0 || sp <= 0.0) {
+        atomicExch(&st->error_code, 1);
+        break;
+      }
+      if (cnt > a.wall && z < ch) {
+        ++ni;
+        continue;
+      }
+      if (fabs(z - ch) / sqrt(cv) > a.maha) {
+        ++no;
+        if (valid) {
+          v = smin(cv + a.sigma_outlier2, a.sigma_max2);
+          var_changed = true;
+        }
+        continue;
+      }
+      const double denom = cv + sp;
+      h = (sp * ch + cv * z) / denom;
+      v = cv * sp / denom;
+      valid = true;
+      fused_any = true;
+      ++nf;
+    }
+    if (fused_any) {
+      L.elev[i] = h;
+      L.var[i] = v;
+      L.last[i] = a.now;
+      L.valid[i] = 1;
+      L.ub[i] = h;
+      L.ubv[i] = 1;
+      upd = 1;
+    } else if (var_changed) {
+      L.var[i] = v;
+    }
+  }
+  nf = warpSum(nf);
+  no = warpSum(no);
+  ni = warpSum(ni);
+  upd = warpSum(upd);
+  if ((threadIdx.x & 31) == 0 && (nf | no | ni | upd)) {
+    if (nf) atomicAdd(&st->fused, nf);
+    if (no) atomicAdd(&st->outlier, no);
+    if (ni) atomicAdd(&st->ignored_low, ni);
+    if (upd) atomicAdd(&st->cells_updated, upd);
+  }
+}
+
+// ------------------------------------------------------------- K5/K6 rays
+enum : uint8_t { kClsNone = 0, kClsBound = 1, kClsCandidate = 2 };
+
+struct RayArgs {
+  GridArgs g;
+  double o[3];  // sensor origin = pose translation
+  double now, t_free, alpha_n;
+  int cleanup, bound;
+};
+
+// Post-fusion ray class per cell; also resets k* (reference raycast.cpp:
+// 132-183 gates that do not depend on the ray).
+__global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayArgs a, uint8_t* cls,
+                                                       int32_t* kstar) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    uint8_t c = kClsNone;
+    if (!L.valid[i]) {
+      c = a.bound ? kClsBound : kClsNone;
+    } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
+               (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
+      c = kClsCandidate;
+    }
+    cls[i] = c;
+    kstar[i] = INT_MAX;
+  }
+}
+
+// Liang-Barsky slab clip (reference raycast.cpp:30-42).
+__device__ __forceinline__ bool clipAxis(double p, double q, double& t0, double& t1) {
+  if (p == 0.0) return q >= 0.0;
+  const double r = q / p;
+  if (p < 0.0) {
+    if (r > t1) return false;
+    t0 = smax(t0, r);
+  } else {
+    if (r < t0) return false;
+    t1 = smin(t1, r);
+  }
+  return t0 <= t1;
+}
+
+__device__ __forceinline__ int clampCell(int v, int n) { return v < 0 ? 0 : (v > n - 1 ? n - 1 : v); }
+
+// Exact 2-D DDA from o to p (reference raycast.cpp:48-130). Calls
+// visit(cell, t_enter, t_next, vertical) for every emitted cell; the ray
+// height there is o.z + (0.5*(t_enter+t_next))*dz, or o.z + 0.5*dz for a
+// vertical ray. Returns nothing; the operation sequence is the reference's.
+template <typename Visit>
+__device__ __forceinline__ void walkRay(const GridArgs& g, const double o[3], double px, double py,
+                                        Visit&& visit) {
+  const double dx = px - o[0];
+  const double dy = py - o[1];
+  const double res = g.res;
+  if (libm_hypot(dx, dy) < 1e-12) {
+    if (o[0] >= g.ox && o[0] < g.xmax && o[1] >= g.oy && o[1] < g.ymax) {
+      const int row = clampCell(x86_to_int(floor((o[1] - g.oy) / res)), g.H);
+      const int col = clampCell(x86_to_int(floor((o[0] - g.ox) / res)), g.W);
+      visit(static_cast<uint32_t>(row) * g.W + col, 0.0, 0.0, true);
+    }
+    return;
+  }
+  double t0 = 0.0, t1 = 1.0;
+  if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return;
+  if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return;
+  if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return;
+  if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
+  if (t0 >= t1) return;
+
+  const bool end_in = px >= g.ox && px < g.xmax && py >= g.oy && py < g.ymax;
+  int end_row = -1, end_col = -1;
+  if (end_in) {
+    end_row = clampCell(x86_to_int(floor((py - g.oy) / res)), g.H);
+    end_col = clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
+  }
+  const double sx = o[0] + t0 * dx;
+  const double sy = o[1] + t0 * dy;
+  int col = clampCell(x86_to_int(floor((sx - g.ox) / res)), g.W);
+  int row = clampCell(x86_to_int(floor((sy - g.oy) / res)), g.H);
+  const int step_col = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+  const int step_row = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+  double tmx = kInf, tmy = kInf, tdx = kInf, tdy = kInf;
+  if (step_col != 0) {
+    const double boundary = g.ox + (col + (step_col > 0 ? 1 : 0)) * res;
+    tmx = (boundary - o[0]) / dx;
+    tdx = res / fabs(dx);
+  }
+  if (step_row != 0) {
+    const double boundary = g.oy + (row + (step_row > 0 ? 1 : 0)) * res;
+    tmy = (boundary - o[1]) / dy;
+    tdy = res / fabs(dy);
+  }
+  double t_enter = t0;
+  while (true) {
+    const double t_next = smin3(tmx, tmy, t1);
+    const bool is_end = end_in && row == end_row && col == end_col;
+    if (!is_end && t_next > t_enter)
+      visit(static_cast<uint32_t>(row) * g.W + col, t_enter, t_next, false);
+    if (t_next >= t1) break;
+    if (tmx < tmy) {
+      col += step_col;
+      tmx += tdx;
+      if (col < 0 || col >= g.W) break;
+    } else {
+      row += step_row;
+      tmy += tdy;
+      if (row < 0 || row >= g.H) break;
+    }
+    t_enter = t_next;
+  }
+}
+
+__device__ __forceinline__ double rayHeight(double oz, double dz, double te, double tn, bool vertical) {
+  return vertical ? oz + 0.5 * dz : oz + (0.5 * (te + tn)) * dz;
+}
+
+// Running min of the upper bound with the reference's comparison (raycast.cpp:
+// 167-183): CAS while ray_h < current.
+__device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) {
+  unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.ub + c);
+  double cur = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(addr)));
+  while (h < cur) {
+    const unsigned long long want = static_cast<unsigned long long>(__double_as_longlong(cur));
+    const unsigned long long got =
+        atomicCAS(addr, want, static_cast<unsigned long long>(__double_as_longlong(h)));
+    if (got == want) {
+      L.ubv[c] = 1;
+      break;
+    }
+    cur = __longlong_as_double(static_cast<long long>(got));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
+                 const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
+                 Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
+                 DevStats* st) {
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  if (k >= n || !kept[k]) return;
+  const double ex = px[k], ey = py[k], ez = pz[k];
+  const double dz = ez - a.o[2];
+  bool touched = false;
+  bool dir_ready = false;
+  double ux = 0.0, uy = 0.0, uz = 0.0;
+  walkRay(a.g, a.o, ex, ey, [&](uint32_t c, double te, double tn, bool vertical) {
+    const uint8_t cl = cls[c];
+    if (cl == kClsNone) return;
+    const double h = rayHeight(a.o[2], dz, te, tn, vertical);
+    if (cl == kClsBound) {
+      boundMin(L, c, h);
+      return;
+    }
+    touched = true;
+    // Removal gates (reference raycast.cpp:138-150), literal comparison forms.
+    if (h >= L.elev[c] - sqrt(L.var[c])) return;
+    if (!dir_ready) {
+      const double vx = ex - a.o[0], vy = ey - a.o[1], vz = dz;
+      const double n2 = (vx * vx + vy * vy) + vz * vz;
+      ux = vx;
+      uy = vy;
+      uz = vz;
+      if (n2 > 0.0) {
+        const double nrm = sqrt(n2);
+        ux = vx / nrm;
+        uy = vy / nrm;
+        uz = vz / nrm;
+      }
+      dir_ready = true;
+    }
+    const double align = fabs((ux * L.nx[c] + uy * L.ny[c]) + uz * L.nz[c]);
+    if (align <= a.alpha_n) return;
+    if (static_cast<int32_t>(k) < kstar[c]) atomicMin(kstar + c, static_cast<int32_t>(k));
+  });
+  if (touched && a.bound) {
+    const unsigned slot = static_cast<unsigned>(atomicAdd(&st->candidate_rays, 1ull));
+    raylist[slot] = k;
+  }
+}
+
+// Invalidate every cell some ray removed (set is order independent).
+__global__ void __launch_bounds__(kThreads) k_remove(Layers L, size_t n, const int32_t* kstar,
+                                                     DevStats* st) {
+  unsigned long long cnt = 0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (kstar[i] != INT_MAX) {
+      invalidateCell(L, i);
+      ++cnt;
+    }
+  }
+  cnt = warpSum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&st->removed, cnt);
+}
+
+// Bounds of removed cells: only rays at or after the first removing ray saw
+// them invalid (reference integration.cpp:212-222 ordering).
+__global__ void __launch_bounds__(kThreads)
+    k_rays_pass2(const uint32_t* __restrict__ raylist, const DevStats* st_in,
+                 const double* __restrict__ px, const double* __restrict__ py,
+                 const double* __restrict__ pz, RayArgs a, Layers L,
+                 const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar) {
+  if (st_in->removed == 0) return;
+  const unsigned total = static_cast<unsigned>(st_in->candidate_rays);
+  for (unsigned q = blockIdx.x * kThreads + threadIdx.x; q < total; q += gridDim.x * kThreads) {
+    const uint32_t k = raylist[q];
+    const double dz = pz[k] - a.o[2];
+    walkRay(a.g, a.o, px[k], py[k], [&](uint32_t c, double te, double tn, bool vertical) {
+      if (cls[c] != kClsCandidate) return;
+      if (kstar[c] > static_cast<int32_t>(k)) return;
+      boundMin(L, c, rayHeight(a.o[2], dz, te, tn, vertical));
+    });
+  }
+}
+
+// ------------------------------------------------------- K7 cell phases
+struct CellArgs {
+  GridArgs g;
+  double rx, ry, rz;  // robot position = pose translation
+  int overlap;
+  double ov_r2, ov_thr;
+  int radius;  // traversability window / 2
+  double slope_max, step_max, rough_max, w_slope, w_step, w_rough;
+  int time_var;
+  double growth, sigma_max2;
+};
+
+constexpr int kTileX = 32, kTileY = 8;
+
+// Overlap clearance (analysis.cpp:296-317), normals (analysis.cpp:41-86),
+// geometric traversability (analysis.cpp:88-132) and time variance
+// (grid.cpp:113-124, integration.cpp:252-257) in one pass over a shared
+// memory tile with a (radius)-cell halo. Overlap is evaluated for halo cells
+// too, so every thread sees the post-clearance validity of its window.
+__global__ void __launch_bounds__(kTileX* kTileY)
+    k_cells(Layers L, const int32_t* __restrict__ count, CellArgs a, DevStats* st) {
+  extern __shared__ unsigned char smem[];
+  const int halo = a.radius > 1 ? a.radius : 1;
+  const int tw = kTileX + 2 * halo, th = kTileY + 2 * halo;
+  double* se = reinterpret_cast<double*>(smem);
+  uint8_t* sv = reinterpret_cast<uint8_t*>(se + tw * th);
+  const int W = a.g.W, H = a.g.H;
+  const int c0 = blockIdx.x * kTileX - halo, r0 = blockIdx.y * kTileY - halo;
+  const int tid = threadIdx.y * kTileX + threadIdx.x;
+  for (int q = tid; q < tw * th; q += kTileX * kTileY) {
+    const int rr = r0 + q / tw, cc = c0 + q % tw;
+    uint8_t v = 0;
+    double e = 0.0;
+    if (rr >= 0 && rr < H && cc >= 0 && cc < W) {
+      const size_t j = static_cast<size_t>(rr) * W + cc;
+      v = L.valid[j];
+      if (v) {
+        e = L.elev[j];
+        if (a.overlap) {
+          const double cx = a.g.ox + (cc + 0.5) * a.g.res;
+          const double cy = a.g.oy + (rr + 0.5) * a.g.res;
+          const double ddx = cx - a.rx, ddy = cy - a.ry;
+          if (!(ddx * ddx + ddy * ddy > a.ov_r2) && !(fabs(e - a.rz) <= a.ov_thr)) v = 0;
+        }
+      }
+    }
+    sv[q] = v;
+    se[q] = e;
+  }
+  __syncthreads();
+  const int r = blockIdx.y * kTileY + threadIdx.y, c = blockIdx.x * kTileX + threadIdx.x;
+  unsigned long long cleared = 0;
+  if (r < H && c < W) {
+    const size_t i = static_cast<size_t>(r) * W + c;
+    const int lr = threadIdx.y + halo, lc = threadIdx.x + halo;
+    const bool was_valid = L.valid[i] != 0;
+    const bool ok = sv[lr * tw + lc] != 0;
+    if (was_valid && !ok) {
+      invalidateCell(L, i);
+      cleared = 1;
+    } else if (ok) {
+      const double res = a.g.res;
+      const double center = se[lr * tw + lc];
+      const bool hl = c > 0 && sv[lr * tw + lc - 1], hr = c < W - 1 && sv[lr * tw + lc + 1];
+      const bool hd = r > 0 && sv[(lr - 1) * tw + lc], hu = r < H - 1 && sv[(lr + 1) * tw + lc];
+      double nx = 0.0, ny = 0.0, nz = 0.0;
+      bool has = true;
+      double dhdx = 0.0, dhdy = 0.0;
+      if (hl && hr) dhdx = (se[lr * tw + lc + 1] - se[lr * tw + lc - 1]) / (2.0 * res);
+      else if (hr) dhdx = (se[lr * tw + lc + 1] - center) / res;
+      else if (hl) dhdx = (center - se[lr * tw + lc - 1]) / res;
+      else has = false;
+      if (has) {
+        if (hd && hu) dhdy = (se[(lr + 1) * tw + lc] - se[(lr - 1) * tw + lc]) / (2.0 * res);
+        else if (hu) dhdy = (se[(lr + 1) * tw + lc] - center) / res;
+        else if (hd) dhdy = (center - se[(lr - 1) * tw + lc]) / res;
+        else has = false;
+      }
+      if (has) {
+        const double norm = sqrt((dhdx * dhdx + dhdy * dhdy) + 1.0);
+        nx = -dhdx / norm;
+        ny = -dhdy / norm;
+        nz = 1.0 / norm;
+      }
+      L.nx[i] = nx;
+      L.ny[i] = ny;
+      L.nz[i] = nz;
+      double trav = 0.0;
+      if (nx != 0.0 || ny != 0.0 || nz != 0.0) {
+        const double slope = acos(sclamp(nz, -1.0, 1.0));
+        const double s_slope = sclamp(1.0 - slope / a.slope_max, 0.0, 1.0);
+        double max_step = 0.0, sum = 0.0, sum_sq = 0.0;
+        int cntw = 0;
+        for (int dr = -a.radius; dr <= a.radius; ++dr) {
+          const int rr = r + dr;
+          if (rr < 0 || rr >= H) continue;
+          for (int dc = -a.radius; dc <= a.radius; ++dc) {
+            const int cc = c + dc;
+            if (cc < 0 || cc >= W) continue;
+            const int q = (lr + dr) * tw + (lc + dc);
+            if (!sv[q]) continue;
+            const double v = se[q];
+            max_step = smax(max_step, fabs(v - center));
+            sum += v;
+            sum_sq += v * v;
+            ++cntw;
+          }
+        }
+        const double s_step = sclamp(1.0 - max_step / a.step_max, 0.0, 1.0);
+        const double mean = sum / cntw;
+        const double var = smax(0.0, sum_sq / cntw - mean * mean);
+        const double s_rough = sclamp(1.0 - sqrt(var) / a.rough_max, 0.0, 1.0);
+        trav = a.w_slope * s_slope + a.w_step * s_step + a.w_rough * s_rough;
+      }
+      L.trav[i] = trav;
+      if (a.time_var && count[i] == 0) L.var[i] = smin(L.var[i] + a.growth, a.sigma_max2);
+    }
+  }
+  cleared = warpSum(cleared);
+  if (((threadIdx.y * kTileX + threadIdx.x) & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
+}
+
+inline unsigned gridFor(size_t n, int threads = kThreads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+inline unsigned streamGrid(size_t n) {
+  return static_cast<unsigned>(std::min<size_t>((n + kThreads - 1) / kThreads, 148 * 16));
+}
+
+int quantizedShift(double d, double res) {
+  if (std::abs(d) < res) return 0;  // one-cell hysteresis (reference grid.cpp:65-68)
+  return static_cast<int>(std::llround(d / res));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host
+ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const double* xyz,
+                               std::size_t n, bool xyz_on_device, const Pose& pose,
+                               double stamp, double dt) {
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (n >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
+  cudaStream_t s = m.stream;
+  long long launches = 0;
+  const std::size_t ncell = m.grid.cells();
+  const uint32_t N = static_cast<uint32_t>(n);
+
+  checkCuda(cudaEventRecord(m.ev[0], s), "event");
+  checkCuda(cudaMemsetAsync(m.stats, 0, sizeof(DevStats), s), "memset");
+
+  // move_to: recenter by whole cells (reference grid.cpp:87-111).
+  const int sx = quantizedShift(pose.t[0] - m.grid.center_x, m.grid.resolution);
+  const int sy = quantizedShift(pose.t[1] - m.grid.center_y, m.grid.resolution);
+  if (sx != 0 || sy != 0) {
+    m.grid.center_x += sx * m.grid.resolution;
+    m.grid.center_y += sy * m.grid.resolution;
+    k_shift<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, m.alt, m.grid.width, m.grid.height, sx, sy);
+    ++launches;
+    std::swap(m.cur, m.alt);
+  }
+  const GridArgs g = gridArgs(m.grid);
+
+  // Input stream into HBM.
+  const double* d_xyz = xyz;
+  if (n > 0) {
+    ensurePointCapacity(m, n);
+    const std::size_t nb = gridFor(n);
+    if (m.rcap < nb || m.rslab == nullptr) {
+      cudaFree(m.rslab);
+      m.rslab = nullptr;
+      m.rcap = std::max<std::size_t>(nb, 1024);
+      checkCuda(cudaMalloc(&m.rslab, m.rcap * (sizeof(double) + sizeof(int)) + 512), "reduce scratch");
+      m.drift_sum_part = static_cast<double*>(m.rslab);
+      m.drift_n_part = reinterpret_cast<int*>(m.drift_sum_part + m.rcap);
+    }
+    if (!xyz_on_device) {
+      checkCuda(cudaMemcpyAsync(m.xyz_in, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s),
+                "point upload");
+      d_xyz = m.xyz_in;
+    }
+  }
+  checkCuda(cudaMemsetAsync(m.count, 0, ncell * sizeof(int32_t), s), "memset");
+  checkCuda(cudaEventRecord(m.ev[1], s), "event");  // upload done
+
+  // K1 ingest.
+  const UpdateParams& U = P.update;
+  if (n > 0) {
+    IngestArgs ia;
+    ia.g = g;
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) ia.R[3 * r + c] = pose.R[r][c];
+      ia.t[r] = pose.t[r];
+    }
+    ia.max_range2 = U.max_range * U.max_range;
+    ia.excl_enabled = U.exclusion.enabled;
+    ia.excl_b = U.exclusion.b;
+    ia.excl_c = U.exclusion.c;
+    ia.excl_dmax = U.exclusion.d_max;
+    ia.excl_tan = std::tan(U.exclusion.theta_a);  // host libm, as the reference
+    ia.alpha_d = U.noise.alpha_d;
+    ia.sigma_p_min2 = U.noise.sigma_p_min2;
+    ia.drift_enabled = P.drift.enabled;
+    ia.drift_thr = P.drift.traversability_threshold;
+    k_ingest<<<gridFor(n), kThreads, 0, s>>>(d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz,
+                                             m.pvar, m.key0, m.kept, m.drift_sum_part,
+                                             m.drift_n_part, m.stats);
+    ++launches;
+  }
+  checkCuda(cudaEventRecord(m.ev[2], s), "event");  // ingest done
+
+  // Drift compensation.
+  if (n > 0 && P.drift.enabled) {
+    k_drift_finalize<<<1, 1024, 0, s>>>(m.drift_sum_part, m.drift_n_part,
+                                        static_cast<int>(gridFor(n)), P.drift.min_points,
+                                        P.drift.max_offset_per_scan, m.drift_offset, m.stats);
+    k_apply_offset<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, m.drift_offset);
+    launches += 2;
+  }
+  checkCuda(cudaEventRecord(m.ev[3], s), "event");  // drift done
+
+  if (n > 0) {
+    // K2: stable sort of point indices by cell, then segment starts.
+    const uint32_t WH = static_cast<uint32_t>(ncell);
+    int bits = 32 - __builtin_clz(WH);
+    const int passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
+    const int dbits = (bits + passes - 1) / passes;
+    const uint32_t ntiles = (N + kTile - 1) / kTile;
+    const std::size_t hist_n = static_cast<std::size_t>(1u << dbits) * ntiles;
+    const std::size_t need = hist_n + (hist_n / kScanTile + 2) + 2 * (ncell / kScanTile + 2) + 64;
+    if (m.hist_cap < need) {
+      cudaFree(m.hist);
+      m.hist_cap = need;
+      checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
+    }
+    uint32_t* hist = m.hist;
+    uint32_t* part = m.hist + hist_n;
+    uint32_t *kin = m.key0, *kout = m.key1, *vin = m.val0, *vout = m.val1;
+    const auto scan = [&](const uint32_t* in, std::size_t len, uint32_t* out, uint32_t* total) {
+      const unsigned nb = static_cast<unsigned>((len + kScanTile - 1) / kScanTile);
+      k_scan_reduce<<<nb, kThreads, 0, s>>>(in, len, part);
+      k_scan_top<<<1, kThreads, 0, s>>>(part, static_cast<int>(nb));
+      k_scan_down<<<nb, kThreads, 0, s>>>(in, len, part, out, total);
+      launches += 3;
+    };
+    for (int p = 0; p < passes; ++p) {
+      const int shift = p * dbits;
+      const bool last = p == passes - 1;
+      k_radix_hist<<<ntiles, kThreads, (1u << dbits) * sizeof(uint32_t), s>>>(kin, N, shift, dbits,
+                                                                              hist, ntiles);
+      ++launches;
+      scan(hist, hist_n, hist, nullptr);
+      k_radix_scatter<<<ntiles, kThreads, 8 * (1u << dbits) * sizeof(uint16_t), s>>>(
+          kin, vin, N, shift, dbits, hist, ntiles, kout, vout, p == 0, last ? 0 : 1);
+      ++launches;
+      std::swap(kin, kout);
+      std::swap(vin, vout);
+    }
+    // vin now holds point indices sorted by (cell, scan order).
+    scan(reinterpret_cast<const uint32_t*>(m.count), ncell, m.start, m.start + ncell);
+    checkCuda(cudaEventRecord(m.ev[4], s), "event");  // sort done
+
+    // K3 gated fusion.
+    FuseArgs fa;
+    fa.now = stamp;
+    fa.sigma_init2 = U.sigma_init2;
+    fa.sigma_outlier2 = U.sigma_outlier2;
+    fa.sigma_max2 = U.sigma_max2;
+    fa.maha = U.mahalanobis_threshold;
+    fa.wall = U.wall_count_threshold;
+    k_fuse<<<gridFor(ncell), kThreads, 0, s>>>(m.cur, ncell, m.count, m.start, vin, m.pz, m.pvar,
+                                               fa, m.stats);
+    ++launches;
+    checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done
+
+    // K5/K6 ray casting.
+    const bool cleanup = P.cleanup.cleanup_enabled, bound = P.cleanup.upper_bound_enabled;
+    if (cleanup || bound) {
+      RayArgs ra;
+      ra.g = g;
+      for (int i = 0; i < 3; ++i) ra.o[i] = pose.t[i];
+      ra.now = stamp;
+      ra.t_free = P.cleanup.t_free;
+      ra.alpha_n = P.cleanup.alpha_n;
+      ra.cleanup = cleanup;
+      ra.bound = bound;
+      k_classify<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, ra, m.cls, m.kstar);
+      k_rays_pass1<<<gridFor(n), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+                                                   m.kstar, m.raylist, m.stats);
+      launches += 2;
+      if (cleanup) {
+        k_remove<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, m.kstar, m.stats);
+        ++launches;
+        if (bound) {
+          k_rays_pass2<<<148 * 8, kThreads, 0, s>>>(m.raylist, m.stats, m.px, m.py, m.pz, ra,
+                                                     m.cur, m.cls, m.kstar);
+          ++launches;
+        }
+      }
+    }
+  }
+  if (n == 0) {
+    checkCuda(cudaEventRecord(m.ev[4], s), "event");
+    checkCuda(cudaEventRecord(m.ev[5], s), "event");
+  }
+  checkCuda(cudaEventRecord(m.ev[6], s), "event");  // rays done
+
+  // K7 cell phases + update_variance.
+  {
+    CellArgs ca;
+    ca.g = g;
+    ca.rx = pose.t[0];
+    ca.ry = pose.t[1];
+    ca.rz = pose.t[2];
+    ca.overlap = P.overlap.enabled;
+    ca.ov_r2 = P.overlap.radius * P.overlap.radius;
+    ca.ov_thr = P.overlap.height_threshold;
+    const TraversabilityParams& T = P.traversability;
+    ca.radius = T.window / 2;
+    ca.slope_max = T.slope_max;
+    ca.step_max = T.step_max;
+    ca.rough_max = T.roughness_max;
+    ca.w_slope = T.w_slope;
+    ca.w_step = T.w_step;
+    ca.w_rough = T.w_roughness;
+    ca.time_var = (dt != 0.0 && U.sigma_t2 != 0.0) ? 1 : 0;
+    ca.growth = U.sigma_t2 * (dt / U.nominal_update_period);
+    ca.sigma_max2 = U.sigma_max2;
+    const int halo = std::max(1, ca.radius);
+    const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
+    const dim3 grid((g.W + kTileX - 1) / kTileX, (g.H + kTileY - 1) / kTileY);
+    if (sm > 48 * 1024)
+      checkCuda(cudaFuncSetAttribute(k_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)),
+                "smem attribute");
+    k_cells<<<grid, dim3(kTileX, kTileY), sm, s>>>(m.cur, m.count, ca, m.stats);
+    ++launches;
+  }
+  checkCuda(cudaEventRecord(m.ev[7], s), "event");  // cell phases done
+  checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s), "stats");
+  checkCuda(cudaGetLastError(), "kernel launch");
+  checkCuda(cudaStreamSynchronize(s), "integrate");
+
+  const DevStats& d = *m.h_stats;
+  if (d.error_code == 1) fail(Err::kInvalidVariance, "variances must be positive");
+  ScanResult out;
+  out.points_in = static_cast<std::int64_t>(n);
+  out.excluded = static_cast<std::int64_t>(d.excluded);
+  out.out_of_range = static_cast<std::int64_t>(d.out_of_range);
+  out.out_of_map = static_cast<std::int64_t>(d.out_of_map);
+  out.outlier = static_cast<std::int64_t>(d.outlier);
+  out.ignored_low = static_cast<std::int64_t>(d.ignored_low);
+  out.fused = static_cast<std::int64_t>(d.fused);
+  out.cells_updated = static_cast<std::int64_t>(d.cells_updated);
+  out.removed = static_cast<std::int64_t>(d.removed);
+  out.overlap_cleared = static_cast<std::int64_t>(d.overlap_cleared);
+  out.drift_offset = d.drift_offset;
+  out.drift_clamped = d.drift_clamped != 0;
+  out.drift_points = d.drift_n;
+
+  float ms[7];
+  for (int k = 0; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
+  // ms: upload, ingest(+shift), drift, sort, fusion, rays, cell phases
+  for (int k = 0; k < 7; ++k) m.kernel_seconds[k] = ms[k] * 1e-3;
+  m.kernel_seconds[7] = (ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6]) * 1e-3;
+  m.phase_seconds[0] = ms[1] * 1e-3;                    // point transform & z error count
+  m.phase_seconds[1] = ms[2] * 1e-3;                    // drift compensation
+  m.phase_seconds[2] = (ms[3] + ms[4] + ms[5]) * 1e-3;  // height update & ray casting
+  m.phase_seconds[3] = ms[6] * 1e-3;                    // overlap + normals + traversability (fused)
+  m.phase_seconds[4] = 0.0;
+  m.phase_seconds[5] = 0.0;
+  m.phase_seconds[6] = m.kernel_seconds[7];
+  out.seconds = m.phase_seconds[6];
+  m.last_launches = launches;
+  return out;
+}
+
+}  // namespace rb200

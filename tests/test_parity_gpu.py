@@ -1,0 +1,212 @@
+"""GPU parity: librelief_b200.so against the reference implementation (oracle/_ref), both
+driven through the same C ABI (relief.h) with identical configs, clouds, poses and stamps.
+
+Bar: every ScanStats counter exact; elevation, variance, last_update,
+upper_bound(+valid), normals and validity bit-exact; traversability within 1e-12 (device
+acos vs libm acos). Runs with drift compensation enabled compare heights within 1e-9
+relative because the drift mean is a parallel (fixed-order) sum.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2204_12876_b200 as pk
+from paper_2204_12876_b200 import workloads as wl
+
+from conftest import assert_layers_match, assert_stats_match, ref_render
+
+pytestmark = pytest.mark.gpu
+
+
+class Pair:
+    """The same map driven through both libraries."""
+
+    def __init__(self, product, reference, tmp_path, config_text, res, W, H, cx=0.0, cy=0.0):
+        self.cfg_path = tmp_path / "run.config"
+        self.cfg_path.write_text(config_text)
+        self.libs = (product, reference)
+        self.cfgs = [pk.Config.load(lib, self.cfg_path) for lib in self.libs]
+        self.maps = [pk.ReliefMap.create(lib, res, W, H, cx, cy) for lib in self.libs]
+
+    def integrate(self, xyz, pose, stamp, drift_tol=0.0, context=""):
+        got = self.maps[0].integrate(xyz, pose, stamp, self.cfgs[0])
+        want = self.maps[1].integrate(xyz, pose, stamp, self.cfgs[1])
+        assert_stats_match(got, want, drift_tol=drift_tol, context=context)
+        return got, want
+
+    def compare(self, height_tol=0.0, context=""):
+        assert self.maps[0].center() == self.maps[1].center()
+        assert_layers_match(self.maps[0].layers(), self.maps[1].layers(), height_tol=height_tol,
+                            context=context)
+
+
+def _render(reference, pair, call):
+    return ref_render(reference, pair.cfg_path, call.pose, call.time, call.seed, call.scan_index)
+
+
+def test_c1_depth_camera_fusion_bit_exact(gpu, reference, tmp_path):
+    w = wl.c1()
+    pair = Pair(gpu, reference, tmp_path, w.config_text, w.resolution, w.width, w.height)
+    for f in range(6):
+        for call in w.calls(f):
+            xyz = _render(reference, pair, call)
+            got, _ = pair.integrate(xyz, call.pose, call.stamp, context=f"frame {f}")
+            assert got.points_fused > 0
+        pair.compare(context=f"C1 frame {f}")
+
+
+def test_lidar_recenter_every_frame_bit_exact(gpu, reference, tmp_path):
+    # C3 geometry at reduced azimuth count; defaults except drift (exact mean below).
+    text = wl._map(0.04, 300, 300) + "noise.alpha_d = 0.0002\n" + wl.lidar(512, rings=64) + wl.SCENE_S0 + \
+        "drift.enabled = false\n"
+    pair = Pair(gpu, reference, tmp_path, text, 0.04, 300, 300)
+    for f in range(8):
+        pose = wl.pose34(np.eye(3), (0.04 * f + 0.013, -0.021 * f, 1.0))
+        xyz = ref_render(reference, pair.cfg_path, pose, 0.1 * f, 3, f)
+        pair.integrate(xyz, pose, 0.15 * f, context=f"frame {f}")
+        pair.compare(context=f"lidar frame {f}")
+
+
+def test_moving_box_cleanup_removals_bit_exact(gpu, reference, tmp_path):
+    # Acceptance #4 scene (reference acceptance.cpp:275-357): the box vacates at 2.95 s and
+    # rays through its stale top remove cells -> exercises k* ordering for upper bounds.
+    text = (wl._map(0.04, 120, 120) +
+            "noise.alpha_d = 0.005\nupdate.sigma_outlier2 = 0.0001\ndrift.enabled = false\n"
+            "overlap.enabled = false\nexclusion.enabled = false\ncleanup.t_free = 1.0\n"
+            "sensor.pattern = grid\nsensor.h_fov_deg = 70\nsensor.v_fov_deg = 60\n"
+            "sensor.cols = 160\nsensor.rows = 140\nsensor.max_range = 10\n"
+            "scene.ground = 0.0\nscene.moving_box = 1.2 0.0 0.3 0.8 0.8 0.6 0 0 0 -1 2.95\n")
+    pair = Pair(gpu, reference, tmp_path, text, 0.04, 120, 120)
+    pitch = math.radians(35.0)
+    pose = wl.pose34(wl.rot_y(pitch), (0.0, 0.0, 1.2))
+    removed = 0
+    for s in range(50):
+        xyz = ref_render(reference, pair.cfg_path, pose, s * 0.1, 4, s)
+        got, _ = pair.integrate(xyz, pose, s * 0.1, context=f"scan {s}")
+        removed += got.cells_removed_by_cleanup
+        if s % 10 == 9 or got.cells_removed_by_cleanup:
+            pair.compare(context=f"moving box scan {s}")
+    assert removed > 50, removed
+
+
+def test_defaults_with_drift_tolerance(gpu, reference, tmp_path):
+    text = wl._map(0.04, 250, 250) + "noise.alpha_d = 0.0002\n" + wl.lidar(720, rings=48) + wl.SCENE_S0
+    pair = Pair(gpu, reference, tmp_path, text, 0.04, 250, 250)
+    applied = 0
+    for f in range(8):
+        pose = wl.pose34(np.eye(3), (0.02 * f, 0.0, 1.0 + 0.01 * f))
+        xyz = ref_render(reference, pair.cfg_path, pose, 0.1 * f, 7, f)
+        got, _ = pair.integrate(xyz, pose, 0.1 * f, drift_tol=1e-12, context=f"frame {f}")
+        applied += got.drift_offset_applied != 0.0
+        pair.compare(height_tol=1e-9, context=f"drift frame {f}")
+    assert applied >= 3
+
+
+def _random_cloud(rng, n, spread=2.0, zsd=0.8):
+    return np.stack([rng.normal(0, spread, n), rng.normal(0, spread, n), rng.normal(0, zsd, n)], axis=1)
+
+
+def test_random_clouds_counters_partition(gpu, reference, tmp_path):
+    # reference test_integration.cpp:216-243 with all stages on (drift off for exactness).
+    text = ("exclusion.b = 0.2\nexclusion.c = 0.1\nexclusion.theta_a_deg = 17.188733853924695\n"
+            "update.max_range = 3.0\ndrift.enabled = false\n")
+    pair = Pair(gpu, reference, tmp_path, text, 0.04, 100, 100)
+    rng = np.random.default_rng(8)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 0.5))
+    for scan in range(6):
+        xyz = _random_cloud(rng, 3000)
+        got, _ = pair.integrate(xyz, pose, scan * 0.1, context=f"scan {scan}")
+        total = (got.points_excluded + got.points_out_of_range + got.points_out_of_map +
+                 got.points_rejected_outlier + got.points_ignored_low + got.points_fused)
+        assert got.points_in == 3000 == total
+        assert got.points_excluded > 0 and got.points_out_of_range > 0
+        pair.compare(context=f"random scan {scan}")
+
+
+def test_dense_cells_wall_rule_and_outliers(gpu, reference, tmp_path):
+    # Many points per cell in scan order exercises the order-dependent gated fold.
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\nupdate.sigma_outlier2 = 0.02\n",
+                0.04, 60, 60)
+    rng = np.random.default_rng(3)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    for scan in range(5):
+        n = 40000
+        xy = rng.uniform(-0.6, 0.6, (n, 2))
+        z = -1.0 + 0.05 * rng.standard_normal(n) + (rng.random(n) < 0.1) * rng.uniform(-0.5, 0.5, n)
+        xyz = np.column_stack([xy, z])
+        got, _ = pair.integrate(xyz, pose, 0.1 * scan, context=f"scan {scan}")
+        assert got.points_ignored_low > 0 and got.points_rejected_outlier > 0
+        pair.compare(context=f"dense scan {scan}")
+
+
+def test_rotated_pose_and_far_points(gpu, reference, tmp_path):
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\n", 0.05, 80, 64, 0.3, -0.2)
+    rng = np.random.default_rng(11)
+    q = np.array([0.3, -0.5, 0.8, 0.1])
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                  [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                  [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+    for scan in range(4):
+        pose = wl.pose34(R, (0.1 * scan, -0.05 * scan, 0.7))
+        xyz = _random_cloud(rng, 5000, spread=3.0, zsd=1.0)
+        xyz[::97] *= 50.0  # far points: out of range / out of map / clipped rays
+        pair.integrate(xyz, pose, 0.3 * scan, context=f"scan {scan}")
+        pair.compare(context=f"rotated scan {scan}")
+
+
+def test_empty_cloud_only_ages(gpu, reference, tmp_path):
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\n", 0.04, 100, 100)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    pair.integrate(np.array([[0.5, 0.5, -1.0]]), pose, 0.0)
+    got, _ = pair.integrate(np.zeros((0, 3)), pose, 1.0)
+    assert got.points_in == 0 and got.points_fused == 0
+    pair.compare(context="empty cloud")
+
+
+def test_nan_and_inf_points(gpu, reference, tmp_path):
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\nexclusion.enabled = false\n",
+                0.04, 60, 60)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    rng = np.random.default_rng(5)
+    xyz = _random_cloud(rng, 2000, spread=0.8, zsd=0.1) - np.array([0, 0, 1.0])
+    xyz[7] = [np.inf, 0.0, -1.0]
+    xyz[9] = [0.2, np.nan, -1.0]
+    xyz[11] = [0.3, 0.1, np.nan]
+    xyz[13] = [-np.inf, np.nan, np.inf]
+    for s in range(3):
+        pair.integrate(xyz, pose, 2.0 * s, context=f"nan scan {s}")
+        pair.compare(context=f"nan scan {s}")
+
+
+def test_error_statuses_match(gpu, reference, tmp_path):
+    pair = Pair(gpu, reference, tmp_path, "update.sigma_init2 = 0\n", 0.1, 10, 10)
+    bad = wl.pose34(np.diag([5.0, 1.0, 1.0]), (0, 0, 0))
+    for m, c in zip(pair.maps, pair.cfgs):
+        with pytest.raises(pk.ReliefError) as e:
+            m.integrate(np.zeros((1, 3)), bad, 0.0, c)
+        assert e.value.status == 4
+        with pytest.raises(pk.ReliefError) as e:
+            m.integrate(np.array([[0.1, 0.1, -1.0]]), wl.pose34(np.eye(3), (0, 0, 1)), 0.0, c)
+        assert e.value.status == 5
+        with pytest.raises(pk.ReliefError) as e:
+            m.layer("bogus")
+        assert e.value.status == 1 and "elevation" in e.value.message
+
+
+def test_snapshot_cross_compatible(gpu, reference, tmp_path):
+    w = wl.c1()
+    pair = Pair(gpu, reference, tmp_path, w.config_text, w.resolution, w.width, w.height)
+    for f in range(3):
+        for call in w.calls(f):
+            pair.integrate(_render(reference, pair, call), call.pose, call.stamp)
+    pm, rm = pair.maps
+    pm.save(tmp_path / "p.relief")
+    rm.save(tmp_path / "r.relief")
+    assert (tmp_path / "p.relief").read_bytes() == (tmp_path / "r.relief").read_bytes()
+    loaded = pk.ReliefMap.load(gpu, tmp_path / "r.relief")
+    assert_layers_match(loaded.layers(), rm.layers(), tol_trav=0.0, context="loaded snapshot")
