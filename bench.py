@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 point-cloud -> elevation-map update path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl b200|reference]
+
+A step is one map update (relief_map_integrate semantics) with one synthetic frame of the
+workload (default C4: 128-ring LiDAR, 1,000,064 points, into a 1000x1000 @0.04 m map with the
+default pipeline incl. ray-cast cleanup, drift compensation, overlap clearance, normals and
+geometric traversability). Frames are rendered by the library's scene simulator (bit-identical
+to the reference simulator); the map evolves across steps as in a real mission.
+
+Legs of the b200 arm (one JSON line from rank 0):
+  value      points/s with the frame already resident in HBM (relief_gpu_map_integrate_device),
+             device time from CUDA events recorded on the library's own stream, L2 flushed
+             (256 MiB write) before every step, summed over exactly K steps, max over ranks.
+  e2e        the same metric through the drop-in C ABI relief_map_integrate with the frame in
+             pinned host memory: host->device copy of the points and the device->host read of
+             the scan statistics inside the timed region (host clock around the synchronous call).
+  roofline   the dominant kernel's algorithmic bytes / its event-timed duration vs measured HBM
+             copy bandwidth (MEASURED_PEAKS.json); traffic from the committed ncu capture.
+  cpu_baseline  the reference (oracle/_ref, reliefmap compiled in place) timed on this host's
+             cores in its parallel mode on a bounded sample of the same workload (rank 0, N=1).
+N>1 (torchrun): every rank owns an independent map and frame stream on its own GPU (replicas,
+weak scaling); NCCL only carries the barrier and the max-over-ranks reduction of the timing.
+
+--impl reference: rank 0 alone times the reference's CPU implementation (oracle/_ref, parallel
+mode, all host threads up to its 16-thread cap) through its own C API on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "points/sec integrated and per-frame map-update ms (1/2/4/8 B200) vs CPU ref"
+REF_LIB = ROOT / "oracle" / "_ref" / "librelief_ref.so"
+L2_FLUSH_BYTES = 256 << 20
+DEVSTATS_BYTES = 104  # DevStats read back per scan (device_map.hpp)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- workloads
+def render_frames(lib, w, cfg_path, n_frames, ref=None):
+    """Distinct frames (cycled if more steps are needed). ref: use the reference's renderer."""
+    import paper_2204_12876_b200 as pk
+    frames = []
+    for f in range(n_frames):
+        calls = []
+        for c in w.calls(f):
+            if ref is None:
+                xyz = pk.sim_render(lib, cfg_path, c.pose, c.time, c.seed, c.scan_index)
+            else:
+                xyz = ref_render(ref, cfg_path, c.pose, c.time, c.seed, c.scan_index)
+            calls.append((np.ascontiguousarray(xyz), c))
+        frames.append(calls)
+    return frames
+
+
+def ref_render(ref, cfg_path, pose, t, seed, idx, cap=1 << 21):
+    DP = ctypes.POINTER(ctypes.c_double)
+    ref.ref_render_scan.restype = ctypes.c_int64
+    ref.ref_render_scan.argtypes = [ctypes.c_char_p, DP, ctypes.c_double, ctypes.c_uint64,
+                                    ctypes.c_uint64, DP, ctypes.c_int64]
+    pose = np.ascontiguousarray(pose, dtype=np.float64)
+    buf = np.empty(cap * 3)
+    n = ref.ref_render_scan(str(cfg_path).encode(), pose.ctypes.data_as(DP), t, seed, idx,
+                            buf.ctypes.data_as(DP), cap)
+    if n > cap:
+        return ref_render(ref, cfg_path, pose, t, seed, idx, cap=int(n))
+    return buf[: 3 * n].reshape(n, 3).copy()
+
+
+# -------------------------------------------------------- reference (CPU)
+def time_reference(w, cfg_text, steps, warmup, mode="par"):
+    """Times oracle/_ref (the reference compiled in place) through its own C API."""
+    import paper_2204_12876_b200 as pk
+    ref = pk.load_library(REF_LIB, gpu_api=False)
+    d = Path(tempfile.mkdtemp())
+    cfgp = d / "ref.config"
+    cfgp.write_text(cfg_text)
+    cfg = pk.Config.load(ref, cfgp)
+    cfg.set_mode(mode)
+    m = pk.ReliefMap.create(ref, w.resolution, w.width, w.height)
+    frames = render_frames(None, w, cfgp, min(steps + warmup, 4), ref=ref)
+    times, pts = [], 0
+    for s in range(warmup + steps):
+        calls = frames[s % len(frames)]
+        t0 = time.perf_counter()
+        for xyz, c in calls:
+            m.integrate(xyz, c.pose, 0.1 * s, cfg)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+            pts += sum(len(x) for x, _ in calls)
+    return pts / sum(times), times
+
+
+def cpu_threads_used(mode):
+    return 1 if mode == "det" else min(os.cpu_count() or 1, 16)
+
+
+# ------------------------------------------------------------- b200 arm
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import paper_2204_12876_b200 as pk
+    from paper_2204_12876_b200 import workloads as wl
+
+    lib = pk.load_library()
+    if lib.relief_gpu_device_count() <= local_rank:
+        raise RuntimeError(f"rank {rank}: CUDA device {local_rank} not visible (no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    w = wl.ALL[args.workload]()
+    tmp = Path(tempfile.mkdtemp())
+    cfgp = tmp / "w.config"
+    cfgp.write_text(w.config_text)
+    cfg = pk.Config.load(lib, cfgp)
+    n_frames = min(args.steps + args.warmup, 8)
+    t0 = time.time()
+    frames = render_frames(lib, w, cfgp, n_frames)
+    pts_per_frame = sum(len(x) for x, _ in frames[0])
+    log(f"[rank {rank}] rendered {n_frames} frames of {pts_per_frame} pts in {time.time() - t0:.1f}s")
+
+    # device-resident copies for `value`, pinned host copies for `e2e`
+    dev_frames = [[(torch.from_numpy(x).to(f"cuda:{local_rank}").contiguous(), c) for x, c in fr]
+                  for fr in frames]
+    pin_frames = []
+    for fr in frames:
+        calls = []
+        for x, c in fr:
+            t = torch.from_numpy(x).pin_memory()
+            calls.append((t.numpy(), c))
+        pin_frames.append(calls)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{local_rank}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- value leg: inputs resident in HBM
+    m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
+    for s in range(args.warmup):
+        for t, c in dev_frames[s % n_frames]:
+            m.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
+    barrier()
+    dev_t, wall_t, launches, phase_sum, ksum = [], [], 0, np.zeros(7), np.zeros(8)
+    with ClockSampler(local_rank) as clocks:
+        for s in range(args.warmup, args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            step_dev = 0.0
+            t0 = time.perf_counter()
+            for t, c in dev_frames[s % n_frames]:
+                m.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
+                ks = m.kernel_seconds()
+                step_dev += ks[7]
+                ksum += ks
+                phase_sum += m.phase_seconds()
+                launches += m.last_launches()
+            wall_t.append(time.perf_counter() - t0)
+            dev_t.append(step_dev)
+    barrier()
+    clock_info = clocks.summary()
+    dev_total = max_over_ranks(sum(dev_t))
+    value = world * pts_per_frame * args.steps / dev_total
+    ms_per_step = dev_total / args.steps * 1e3
+
+    # Dominant kernel group + roofline
+    kmean = ksum / args.steps
+    names = ["ingest", "drift", "sort", "fusion", "rays", "cells"]
+    shares = dict(zip(names, kmean[1:7]))
+    dom = max(shares, key=shares.get)
+    roof = roofline(dom, kmean, m, w, pts_per_frame, frames)
+
+    # post-processing chain (C5) on the final map
+    chain_t = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        m.smooth_chain("elevation", wl.C5_CHAIN)
+        chain_t.append(time.perf_counter() - t0)
+    chain_ms = statistics.median(chain_t) * 1e3
+
+    # ---------------- e2e leg: drop-in C ABI, pinned host input
+    m2 = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
+    for s in range(args.warmup):
+        for x, c in pin_frames[s % n_frames]:
+            m2.integrate(x, c.pose, 0.1 * s, cfg)
+    barrier()
+    e2e_t = []
+    for s in range(args.warmup, args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for x, c in pin_frames[s % n_frames]:
+            m2.integrate(x, c.pose, 0.1 * s, cfg)  # H2D + kernels + stats D2H, synchronous
+        e2e_t.append(time.perf_counter() - t0)
+    barrier()
+    e2e_total = max_over_ranks(sum(e2e_t))
+    e2e_value = world * pts_per_frame * args.steps / e2e_total
+
+    result = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline and REF_LIB.exists():
+            cpu_steps = args.cpu_frames
+            v, times = time_reference(w, w.config_text, cpu_steps, 1, mode="par")
+            cpu = {"value": v, "unit": "points/s", "cores": cpu_threads_used("par"),
+                   "kind": "reference",
+                   "sample": f"{cpu_steps} frames of {args.workload} ({pts_per_frame} pts each) after 1 "
+                             f"warm-up frame, reliefmap reference (oracle/_ref) par mode via its C API",
+                   "ms_per_frame": statistics.median(times) * 1e3,
+                   "host_cpus": os.cpu_count()}
+        result = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (library scene simulator, bit-identical to the reference renderer)",
+            "config": {"workload": f"{w.name}: {w.description}", "points_per_frame": pts_per_frame,
+                       "map": f"{w.width}x{w.height}@{w.resolution}m",
+                       "calls_per_frame": len(frames[0]), "distinct_frames": n_frames,
+                       "parallelism": f"replicas x{world} (independent map per GPU)",
+                       "l2": "flushed before every timed step (256 MiB write)"},
+            "frame_ms_with_post": ms_per_step + chain_ms,
+            "post_chain_ms": chain_ms,
+            "wall_ms_per_step": statistics.mean(wall_t) * 1e3,
+            "phase_ms": {lbl: float(v) * 1e3 / args.steps for lbl, v in zip(
+                ["point transform & z error count", "drift compensation", "height update & ray casting",
+                 "overlap clearance+normals+traversability (fused)", "traversability", "normal calculation",
+                 "total"], phase_sum)},
+            "kernel_ms": {n: float(v) * 1e3 for n, v in zip(names, kmean[1:7])},
+            "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": 24 * pts_per_frame,
+                    "d2h_bytes_per_step": DEVSTATS_BYTES * len(frames[0]),
+                    "ms_per_step": e2e_total / args.steps * 1e3},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clock_info,
+        }
+    if dist is not None:
+        dist.destroy_process_group()
+    return result
+
+
+def roofline(dom, kmean, m, w, pts, frames):
+    """Algorithmic bytes of the dominant kernel group / its event-timed duration."""
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    cells = w.width * w.height
+    calls = len(frames[0])
+    visits = m.last_visits() * calls
+    # algorithmic bytes per launch group:
+    by = {
+        "ingest": 24 * pts + 40 * pts + 5 * pts,               # xyz in; map-frame xyz+var out; key+flag
+        "drift": 2 * 18 * cells * calls,                       # elev/ub/valid/ubv read+write
+        "sort": 2 * 2 * 8 * pts + 16 * pts,                    # 2 passes (key,val) in+out; payload out
+        "fusion": 16 * pts + 132 * cells * calls // 8,         # payload in; touched cell state r/w
+        "rays": 25 * pts + visits,                             # endpoint + flag per ray, 1 B per visit
+        "cells": 132 * cells * calls,                          # persistent state read + written
+    }
+    idx = ["ingest", "drift", "sort", "fusion", "rays", "cells"].index(dom)
+    dur = kmean[1 + idx]
+    ach = by[dom] / dur / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(dom)
+    return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak, "traffic": traffic, "algorithmic_bytes": int(by[dom]),
+            "duration_us": dur * 1e6, "dda_visits_per_frame": int(visits),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6.65 TB/s"}
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C4", "headline"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from paper_2204_12876_b200 import workloads as wl
+        if not REF_LIB.exists():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librelief_ref.so not built"}))
+            return
+        w = wl.ALL[args.workload]()
+        v, times = time_reference(w, w.config_text, args.steps, args.warmup, mode="par")
+        pts = None
+        cores = cpu_threads_used("par")
+        out = {"metric": METRIC, "value": v, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference renderer)",
+               "config": {"workload": f"{w.name}: {w.description}", "map": f"{w.width}x{w.height}@{w.resolution}m",
+                          "parallelism": "reference CPU, parallelFor threads"},
+               "impl": "reference",
+               "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores, "kind": "reference",
+                                "sample": f"{args.steps} full frames of {w.name} after {args.warmup} warm-up"},
+               "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+
+    res = run_b200(args, rank, world, local_rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -54,6 +54,10 @@ RELIEF_API relief_status relief_gpu_map_kernel_seconds(const relief_map* map, do
 /* Kernel launches issued by the last integrate call (evidence for bench.py). */
 RELIEF_API int64_t relief_gpu_map_last_launches(const relief_map* map);
 
+/* DDA cell visits emitted by the last integrate call's ray pass (roofline
+ * accounting: one class probe per visit). */
+RELIEF_API int64_t relief_gpu_map_last_visits(const relief_map* map);
+
 /* Copies one masked layer (same semantics as relief_map_layer) into device
  * memory of the map's device. */
 RELIEF_API relief_status relief_gpu_map_layer_device(const relief_map* map, const char* layer,

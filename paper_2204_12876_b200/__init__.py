@@ -112,6 +112,7 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_map_phase_seconds": (_I, [_P, _DP]),
     "relief_gpu_map_kernel_seconds": (_I, [_P, _DP]),
     "relief_gpu_map_last_launches": (ctypes.c_int64, [_P]),
+    "relief_gpu_map_last_visits": (ctypes.c_int64, [_P]),
     "relief_gpu_map_layer_device": (_I, [_P, _CS, ctypes.c_void_p, _SZ]),
     "relief_gpu_map_smooth_chain": (_I, [_P, _CS, ctypes.POINTER(_I), ctypes.POINTER(_I), _DP, _I, _DP,
                                          ctypes.POINTER(ctypes.c_uint8)]),
@@ -297,6 +298,9 @@ class ReliefMap:
 
     def last_launches(self) -> int:
         return int(self.lib.relief_gpu_map_last_launches(self.handle))
+
+    def last_visits(self) -> int:
+        return int(self.lib.relief_gpu_map_last_visits(self.handle))
 
     def smooth_chain(self, layer: str, steps: Sequence[tuple]):
         """steps: (kind, radius, sigma) tuples; returns (values, valid)."""

@@ -337,6 +337,10 @@ relief_status relief_gpu_map_kernel_seconds(const relief_map* map, double out[8]
   return RELIEF_OK;
 }
 
+int64_t relief_gpu_map_last_visits(const relief_map* map) {
+  return map ? map->dev->last_visits : 0;
+}
+
 int64_t relief_gpu_map_last_launches(const relief_map* map) {
   return map ? map->dev->last_launches : 0;
 }

@@ -177,7 +177,7 @@ void ensurePointCapacity(DeviceMap& m, std::size_t n) {
   while (cap < n) cap <<= 1;
   cudaFree(m.pslab);
   m.pslab = nullptr;
-  const std::size_t bytes = alignUp(cap * 24) + 4 * alignUp(cap * 8) + 5 * alignUp(cap * 4) +
+  const std::size_t bytes = alignUp(cap * 24) + 6 * alignUp(cap * 8) + 5 * alignUp(cap * 4) +
                             alignUp(cap) + 8 * kAlign;
   checkCuda(cudaMalloc(&m.pslab, bytes), "point scratch allocation");
   Carver c{static_cast<char*>(m.pslab)};
@@ -186,6 +186,8 @@ void ensurePointCapacity(DeviceMap& m, std::size_t n) {
   m.py = c.take<double>(cap);
   m.pz = c.take<double>(cap);
   m.pvar = c.take<double>(cap);
+  m.spz = c.take<double>(cap);
+  m.spv = c.take<double>(cap);
   m.key0 = c.take<uint32_t>(cap);
   m.key1 = c.take<uint32_t>(cap);
   m.val0 = c.take<uint32_t>(cap);

@@ -45,6 +45,7 @@ struct DevStats {
   unsigned long long removed;
   unsigned long long overlap_cleared;
   unsigned long long candidate_rays;  // rays queued for the k* pass
+  unsigned long long visits;          // DDA cells emitted by pass 1
   double drift_offset;                // applied offset (0 when not applied)
   int drift_n;
   int drift_clamped;
@@ -79,6 +80,8 @@ struct DeviceMap {
   double* py = nullptr;
   double* pz = nullptr;
   double* pvar = nullptr;
+  double* spz = nullptr;  // p_z sorted by (cell, scan order)
+  double* spv = nullptr;  // sigma_p^2 sorted likewise
   uint32_t* key0 = nullptr;
   uint32_t* key1 = nullptr;
   uint32_t* val0 = nullptr;
@@ -104,6 +107,7 @@ struct DeviceMap {
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
   long long last_launches = 0;
+  long long last_visits = 0;
 };
 
 GridArgs gridArgs(const Grid& g);

@@ -290,7 +290,10 @@ __global__ void __launch_bounds__(kThreads)
     k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                     uint32_t n, int shift, int bits, const uint32_t* __restrict__ offsets,
                     uint32_t ntiles, uint32_t* __restrict__ keys_out,
-                    uint32_t* __restrict__ vals_out, int first_pass, int write_keys) {
+                    uint32_t* __restrict__ vals_out, int first_pass, int last_pass,
+                    uint32_t sentinel, const double* __restrict__ pz,
+                    const double* __restrict__ pvar, double* __restrict__ spz,
+                    double* __restrict__ spv) {
   extern __shared__ uint16_t wcnt[];  // [8 warps][buckets]
   const int buckets = 1 << bits;
   const uint32_t mask = buckets - 1;
@@ -333,8 +336,14 @@ __global__ void __launch_bounds__(kThreads)
     if (key[r] == 0xffffffffu && wbase + r * 32 + lane >= n) continue;
     const uint32_t d = (key[r] >> shift) & mask;
     const uint32_t pos = offsets[static_cast<size_t>(d) * ntiles + blockIdx.x] + my[d] + rank[r];
-    if (write_keys) keys_out[pos] = key[r];
-    vals_out[pos] = val[r];
+    if (!last_pass) {
+      keys_out[pos] = key[r];
+      vals_out[pos] = val[r];
+    } else if (key[r] < sentinel) {
+      // Final pass: emit the fusion payload in (cell, scan order) order.
+      spz[pos] = pz[val[r]];
+      spv[pos] = pvar[val[r]];
+    }
   }
 }
 
@@ -429,54 +438,92 @@ __global__ void __launch_bounds__(kThreads)
 // ------------------------------------------------------------- K3 fusion
 struct FuseArgs {
   double now;
-  double sigma_init2, sigma_outlier2, sigma_max2, maha;
+  double sigma_init2, sigma_outlier2, sigma_max2, maha, maha2;
   int wall;
 };
 
+// Mahalanobis gate |z - h| / sqrt(v) > maha, decided exactly. The common case
+// is settled by d^2 vs maha^2 v with a 1e-12 relative margin (the rounding of
+// the reference's sqrt and division is below 3e-16 relative, so outside the
+// margin both forms agree); near the boundary, or for magnitudes where d^2
+// could overflow / underflow, the reference's own expression is evaluated.
+__device__ __forceinline__ bool gateOutlier(double d, double cv, const FuseArgs& a) {
+  if (d < 1e100 && cv > 1e-200 && cv < 1e200 && (d > 1e-100 || d == 0.0)) {
+    const double lhs = d * d, rhs = a.maha2 * cv;
+    if (lhs > rhs * (1.0 + 1e-12)) return true;
+    if (lhs < rhs * (1.0 - 1e-12)) return false;
+  }
+  return d / sqrt(cv) > a.maha;
+}
+
+constexpr int kFoldBatch = 8;
+
 // Gated Kalman fold (reference integration.cpp:40-55,142-203, grid.cpp:139-147):
-// one thread per occupied cell walks that cell's points in scan order.
+// one thread per cell walks that cell's points in scan order. The payload is
+// contiguous per cell (written by the last radix pass), loaded in batches of 8
+// with the next batch in flight while the current one is folded, so the
+// dependent fp64 chain does not wait on memory.
 __global__ void __launch_bounds__(kThreads)
     k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
-           const uint32_t* __restrict__ start, const uint32_t* __restrict__ order,
-           const double* __restrict__ pz, const double* __restrict__ pvar, FuseArgs a,
-           DevStats* st) {
+           const uint32_t* __restrict__ start, const double* __restrict__ spz,
+           const double* __restrict__ spv, FuseArgs a, DevStats* st) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const int cnt = i < ncell ? count[i] : 0;
   unsigned long long nf = 0, no = 0, ni = 0, upd = 0;
   if (cnt > 0) {
     bool valid = L.valid[i] != 0;
     double h = L.elev[i], v = L.var[i];
-    bool fused_any = false, var_changed = false;
-    const uint32_t s0 = start[i];
-    for (int j = 0; j < cnt; ++j) {
-      const uint32_t k = order[s0 + j];
-      const double z = pz[k];
-      const double sp = pvar[k];
-      const double ch = valid ? h : z;
-      const double cv = valid ? v : a.sigma_init2;
-      if (cv <= 0.0 || sp <= 0.0) {
-        atomicExch(&st->error_code, 1);
-        break;
-      }
-      if (cnt > a.wall && z < ch) {
-        ++ni;
-        continue;
-      }
-      if (fabs(z - ch) / sqrt(cv) > a.maha) {
-        ++no;
-        if (valid) {
-          v = smin(cv + a.sigma_outlier2, a.sigma_max2);
-          var_changed = true;
-        }
-        continue;
-      }
-      const double denom = cv + sp;
-      h = (sp * ch + cv * z) / denom;
-      v = cv * sp / denom;
-      valid = true;
-      fused_any = true;
-      ++nf;
+    bool fused_any = false, var_changed = false, bad = false;
+    const double* zp = spz + start[i];
+    const double* vp = spv + start[i];
+    const bool wall = cnt > a.wall;
+    double zn[kFoldBatch], vn[kFoldBatch];
+#pragma unroll
+    for (int b = 0; b < kFoldBatch; ++b) {
+      zn[b] = b < cnt ? zp[b] : 0.0;
+      vn[b] = b < cnt ? vp[b] : 0.0;
     }
+    for (int base = 0; base < cnt && !bad; base += kFoldBatch) {
+      double zc[kFoldBatch], vc[kFoldBatch];
+#pragma unroll
+      for (int b = 0; b < kFoldBatch; ++b) {
+        zc[b] = zn[b];
+        vc[b] = vn[b];
+        const int j = base + kFoldBatch + b;
+        zn[b] = j < cnt ? zp[j] : 0.0;
+        vn[b] = j < cnt ? vp[j] : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kFoldBatch; ++b) {
+        if (base + b >= cnt || bad) break;
+        const double z = zc[b], sp = vc[b];
+        const double ch = valid ? h : z;
+        const double cv = valid ? v : a.sigma_init2;
+        if (cv <= 0.0 || sp <= 0.0) {
+          bad = true;
+          break;
+        }
+        if (wall && z < ch) {
+          ++ni;
+          continue;
+        }
+        if (gateOutlier(fabs(z - ch), cv, a)) {
+          ++no;
+          if (valid) {
+            v = smin(cv + a.sigma_outlier2, a.sigma_max2);
+            var_changed = true;
+          }
+          continue;
+        }
+        const double denom = cv + sp;
+        h = (sp * ch + cv * z) / denom;
+        v = cv * sp / denom;
+        valid = true;
+        fused_any = true;
+        ++nf;
+      }
+    }
+    if (bad) atomicExch(&st->error_code, 1);
     if (fused_any) {
       L.elev[i] = h;
       L.var[i] = v;
@@ -571,11 +618,10 @@ __device__ __forceinline__ void walkRay(const GridArgs& g, const double o[3], do
   if (t0 >= t1) return;
 
   const bool end_in = px >= g.ox && px < g.xmax && py >= g.oy && py < g.ymax;
-  int end_row = -1, end_col = -1;
-  if (end_in) {
-    end_row = clampCell(x86_to_int(floor((py - g.oy) / res)), g.H);
-    end_col = clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
-  }
+  uint32_t end_idx = 0xffffffffu;  // never equal to a cell index
+  if (end_in)
+    end_idx = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H)) * g.W +
+              clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
   const double sx = o[0] + t0 * dx;
   const double sy = o[1] + t0 * dy;
   int col = clampCell(x86_to_int(floor((sx - g.ox) / res)), g.W);
@@ -593,24 +639,109 @@ __device__ __forceinline__ void walkRay(const GridArgs& g, const double o[3], do
     tmy = (boundary - o[1]) / dy;
     tdy = res / fabs(dy);
   }
+  // Linear cell index advanced incrementally; the endpoint test compares
+  // indices (row/col are in range inside the loop, so this equals the
+  // reference's CellIndex comparison).
+  uint32_t idx = static_cast<uint32_t>(row) * g.W + col;
+  const int step_idx_row = step_row * g.W;
   double t_enter = t0;
   while (true) {
-    const double t_next = smin3(tmx, tmy, t1);
-    const bool is_end = end_in && row == end_row && col == end_col;
-    if (!is_end && t_next > t_enter)
-      visit(static_cast<uint32_t>(row) * g.W + col, t_enter, t_next, false);
+    double m = tmx;  // std::min({tmx, tmy, t1}): first smallest wins
+    if (tmy < m) m = tmy;
+    const double t_next = (t1 < m) ? t1 : m;
+    if (idx != end_idx && t_next > t_enter) visit(idx, t_enter, t_next, false);
     if (t_next >= t1) break;
     if (tmx < tmy) {
       col += step_col;
       tmx += tdx;
-      if (col < 0 || col >= g.W) break;
+      idx += step_col;
+      if (static_cast<unsigned>(col) >= static_cast<unsigned>(g.W)) break;
     } else {
       row += step_row;
       tmy += tdy;
-      if (row < 0 || row >= g.H) break;
+      idx += step_idx_row;
+      if (static_cast<unsigned>(row) >= static_cast<unsigned>(g.H)) break;
     }
     t_enter = t_next;
   }
+}
+
+// Same traversal for rays whose xy deltas are finite (every ray of a real
+// scan). Without NaNs the first-smallest min of {t_max_x, t_max_y, t1} and the
+// two exit tests collapse to one comparison each: m = (tmx < tmy ? tmx : tmy)
+// equals the reference's min in value (ties are equal values; +-0 only occurs
+// where it is not observable), and t_next >= t1 <=> !(m < t1).
+template <typename Visit>
+__device__ __forceinline__ void walkRayFinite(const GridArgs& g, const double o[3], double px,
+                                              double py, Visit&& visit) {
+  const double dx = px - o[0];
+  const double dy = py - o[1];
+  const double res = g.res;
+  if (libm_hypot(dx, dy) < 1e-12) {
+    if (o[0] >= g.ox && o[0] < g.xmax && o[1] >= g.oy && o[1] < g.ymax) {
+      const int row = clampCell(x86_to_int(floor((o[1] - g.oy) / res)), g.H);
+      const int col = clampCell(x86_to_int(floor((o[0] - g.ox) / res)), g.W);
+      visit(static_cast<uint32_t>(row) * g.W + col, 0.0, 0.0, true);
+    }
+    return;
+  }
+  double t0 = 0.0, t1 = 1.0;
+  if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return;
+  if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return;
+  if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return;
+  if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
+  if (t0 >= t1) return;
+  const bool end_in = px >= g.ox && px < g.xmax && py >= g.oy && py < g.ymax;
+  uint32_t end_idx = 0xffffffffu;
+  if (end_in)
+    end_idx = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H)) * g.W +
+              clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
+  int col = clampCell(x86_to_int(floor(((o[0] + t0 * dx) - g.ox) / res)), g.W);
+  int row = clampCell(x86_to_int(floor(((o[1] + t0 * dy) - g.oy) / res)), g.H);
+  const int step_col = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+  const int step_row = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+  double tmx = kInf, tmy = kInf, tdx = kInf, tdy = kInf;
+  if (step_col != 0) {
+    tmx = ((g.ox + (col + (step_col > 0 ? 1 : 0)) * res) - o[0]) / dx;
+    tdx = res / fabs(dx);
+  }
+  if (step_row != 0) {
+    tmy = ((g.oy + (row + (step_row > 0 ? 1 : 0)) * res) - o[1]) / dy;
+    tdy = res / fabs(dy);
+  }
+  uint32_t idx = static_cast<uint32_t>(row) * g.W + col;
+  const int step_idx_row = step_row * g.W;
+  const unsigned W = static_cast<unsigned>(g.W), H = static_cast<unsigned>(g.H);
+  double t_enter = t0;
+  while (true) {
+    const bool sx = tmx < tmy;
+    const double m = sx ? tmx : tmy;
+    const bool more = m < t1;
+    const double t_next = more ? m : t1;
+    if (idx != end_idx && t_next > t_enter) visit(idx, t_enter, t_next, false);
+    if (!more) break;
+    if (sx) {
+      col += step_col;
+      tmx += tdx;
+      idx += step_col;
+      if (static_cast<unsigned>(col) >= W) break;
+    } else {
+      row += step_row;
+      tmy += tdy;
+      idx += step_idx_row;
+      if (static_cast<unsigned>(row) >= H) break;
+    }
+    t_enter = t_next;
+  }
+}
+
+// Dispatch: the literal walk handles non-finite endpoints (NaN / inf points
+// reach the ray phase exactly as in the reference).
+template <typename Visit>
+__device__ __forceinline__ void walk(const GridArgs& g, const double o[3], double px, double py,
+                                     Visit&& visit) {
+  if (isfinite(px - o[0]) && isfinite(py - o[1])) walkRayFinite(g, o, px, py, visit);
+  else walkRay(g, o, px, py, visit);
 }
 
 __device__ __forceinline__ double rayHeight(double oz, double dz, double te, double tn, bool vertical) {
@@ -618,10 +749,12 @@ __device__ __forceinline__ double rayHeight(double oz, double dz, double te, dou
 }
 
 // Running min of the upper bound with the reference's comparison (raycast.cpp:
-// 167-183): CAS while ray_h < current.
-__device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) {
+// 167-183): CAS while ray_h < current. `seen` is a possibly stale (L1) read of
+// the bound; bounds only decrease, so a stale value is never below the true
+// one and the CAS loop settles on the true minimum.
+__device__ __noinline__ void boundMinSlow(const Layers& L, uint32_t c, double h, double seen) {
   unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.ub + c);
-  double cur = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(addr)));
+  double cur = seen;
   while (h < cur) {
     const unsigned long long want = static_cast<unsigned long long>(__double_as_longlong(cur));
     const unsigned long long got =
@@ -634,51 +767,67 @@ __device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) 
   }
 }
 
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) {
+  const double seen = L.ub[c];
+  if (h < seen) boundMinSlow(L, c, h, seen);
+}
+
+// Removal gates for a candidate cell (reference raycast.cpp:138-150), literal
+// comparison forms; records the ray in k*.
+__device__ __noinline__ void candidateVisit(const Layers& L, uint32_t c, double h, double vx,
+                                            double vy, double vz, double alpha_n, int32_t k,
+                                            int32_t* kstar) {
+  if (h >= L.elev[c] - sqrt(L.var[c])) return;
+  const double n2 = (vx * vx + vy * vy) + vz * vz;
+  double ux = vx, uy = vy, uz = vz;
+  if (n2 > 0.0) {
+    const double nrm = sqrt(n2);
+    ux = vx / nrm;
+    uy = vy / nrm;
+    uz = vz / nrm;
+  }
+  const double align = fabs((ux * L.nx[c] + uy * L.ny[c]) + uz * L.nz[c]);
+  if (align <= alpha_n) return;
+  if (k < kstar[c]) atomicMin(kstar + c, k);
+}
+
+__global__ void __launch_bounds__(kThreads, 4)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
                  DevStats* st) {
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
-  if (k >= n || !kept[k]) return;
-  const double ex = px[k], ey = py[k], ez = pz[k];
-  const double dz = ez - a.o[2];
   bool touched = false;
-  bool dir_ready = false;
-  double ux = 0.0, uy = 0.0, uz = 0.0;
-  walkRay(a.g, a.o, ex, ey, [&](uint32_t c, double te, double tn, bool vertical) {
-    const uint8_t cl = cls[c];
-    if (cl == kClsNone) return;
-    const double h = rayHeight(a.o[2], dz, te, tn, vertical);
-    if (cl == kClsBound) {
-      boundMin(L, c, h);
-      return;
-    }
-    touched = true;
-    // Removal gates (reference raycast.cpp:138-150), literal comparison forms.
-    if (h >= L.elev[c] - sqrt(L.var[c])) return;
-    if (!dir_ready) {
-      const double vx = ex - a.o[0], vy = ey - a.o[1], vz = dz;
-      const double n2 = (vx * vx + vy * vy) + vz * vz;
-      ux = vx;
-      uy = vy;
-      uz = vz;
-      if (n2 > 0.0) {
-        const double nrm = sqrt(n2);
-        ux = vx / nrm;
-        uy = vy / nrm;
-        uz = vz / nrm;
+  unsigned visits = 0;
+  if (k < n && kept[k]) {
+    const double ex = px[k], ey = py[k], ez = pz[k];
+    const double dz = ez - a.o[2];
+    walk(a.g, a.o, ex, ey, [&](uint32_t c, double te, double tn, bool vertical) {
+      ++visits;
+      const uint8_t cl = cls[c];
+      if (cl == kClsNone) return;
+      const double h = rayHeight(a.o[2], dz, te, tn, vertical);
+      if (cl == kClsBound) {
+        boundMin(L, c, h);
+        return;
       }
-      dir_ready = true;
-    }
-    const double align = fabs((ux * L.nx[c] + uy * L.ny[c]) + uz * L.nz[c]);
-    if (align <= a.alpha_n) return;
-    if (static_cast<int32_t>(k) < kstar[c]) atomicMin(kstar + c, static_cast<int32_t>(k));
-  });
-  if (touched && a.bound) {
-    const unsigned slot = static_cast<unsigned>(atomicAdd(&st->candidate_rays, 1ull));
-    raylist[slot] = k;
+      touched = true;
+      candidateVisit(L, c, h, ex - a.o[0], ey - a.o[1], dz, a.alpha_n, static_cast<int32_t>(k),
+                     kstar);
+    });
   }
+  // Queue rays that crossed a removal candidate for the k* pass (one atomic per warp).
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned want = __ballot_sync(0xffffffffu, touched && a.bound);
+  if (want) {
+    unsigned base = 0;
+    if (lane == __ffs(want) - 1)
+      base = static_cast<unsigned>(atomicAdd(&st->candidate_rays, static_cast<unsigned long long>(__popc(want))));
+    base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
+    if (touched && a.bound) raylist[base + __popc(want & ((1u << lane) - 1u))] = k;
+  }
+  unsigned long long v = warpSum(static_cast<unsigned long long>(visits));
+  if (lane == 0 && v) atomicAdd(&st->visits, v);
 }
 
 // Invalidate every cell some ray removed (set is order independent).
@@ -708,7 +857,7 @@ __global__ void __launch_bounds__(kThreads)
   for (unsigned q = blockIdx.x * kThreads + threadIdx.x; q < total; q += gridDim.x * kThreads) {
     const uint32_t k = raylist[q];
     const double dz = pz[k] - a.o[2];
-    walkRay(a.g, a.o, px[k], py[k], [&](uint32_t c, double te, double tn, bool vertical) {
+    walk(a.g, a.o, px[k], py[k], [&](uint32_t c, double te, double tn, bool vertical) {
       if (cls[c] != kClsCandidate) return;
       if (kstar[c] > static_cast<int32_t>(k)) return;
       boundMin(L, c, rayHeight(a.o[2], dz, te, tn, vertical));
@@ -968,12 +1117,13 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
       ++launches;
       scan(hist, hist_n, hist, nullptr);
       k_radix_scatter<<<ntiles, kThreads, 8 * (1u << dbits) * sizeof(uint16_t), s>>>(
-          kin, vin, N, shift, dbits, hist, ntiles, kout, vout, p == 0, last ? 0 : 1);
+          kin, vin, N, shift, dbits, hist, ntiles, kout, vout, p == 0, last ? 1 : 0, WH, m.pz,
+          m.pvar, m.spz, m.spv);
       ++launches;
       std::swap(kin, kout);
       std::swap(vin, vout);
     }
-    // vin now holds point indices sorted by (cell, scan order).
+    // spz / spv now hold (p_z, sigma_p^2) sorted by (cell, scan order).
     scan(reinterpret_cast<const uint32_t*>(m.count), ncell, m.start, m.start + ncell);
     checkCuda(cudaEventRecord(m.ev[4], s), "event");  // sort done
 
@@ -984,9 +1134,10 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     fa.sigma_outlier2 = U.sigma_outlier2;
     fa.sigma_max2 = U.sigma_max2;
     fa.maha = U.mahalanobis_threshold;
+    fa.maha2 = U.mahalanobis_threshold * U.mahalanobis_threshold;
     fa.wall = U.wall_count_threshold;
-    k_fuse<<<gridFor(ncell), kThreads, 0, s>>>(m.cur, ncell, m.count, m.start, vin, m.pz, m.pvar,
-                                               fa, m.stats);
+    k_fuse<<<gridFor(ncell), kThreads, 0, s>>>(m.cur, ncell, m.count, m.start, m.spz, m.spv, fa,
+                                               m.stats);
     ++launches;
     checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done
 
@@ -1089,6 +1240,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   m.phase_seconds[6] = m.kernel_seconds[7];
   out.seconds = m.phase_seconds[6];
   m.last_launches = launches;
+  m.last_visits = static_cast<long long>(d.visits);
   return out;
 }
 
