@@ -73,6 +73,17 @@ RELIEF_API relief_status relief_gpu_map_smooth_chain(const relief_map* map, cons
                                                      const double* sigmas, int n_steps,
                                                      double* values_out, uint8_t* valid_out);
 
+/* Same chain with outputs left in device memory of the map's device
+ * (d_values_out: width*height doubles, d_valid_out: width*height bytes).
+ * Synchronous; relief_gpu_map_chain_seconds() reports its device time. */
+RELIEF_API relief_status relief_gpu_map_smooth_chain_device(const relief_map* map,
+                                                            const char* layer, const int* kinds,
+                                                            const int* radii,
+                                                            const double* sigmas, int n_steps,
+                                                            double* d_values_out,
+                                                            uint8_t* d_valid_out);
+RELIEF_API double relief_gpu_map_chain_seconds(const relief_map* map);
+
 /* Same chain on caller-supplied host data (values + 0/1 validity). */
 RELIEF_API relief_status relief_gpu_smooth_chain(const double* values, const uint8_t* valid,
                                                  int width, int height, const int* kinds,

@@ -116,6 +116,9 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_map_layer_device": (_I, [_P, _CS, ctypes.c_void_p, _SZ]),
     "relief_gpu_map_smooth_chain": (_I, [_P, _CS, ctypes.POINTER(_I), ctypes.POINTER(_I), _DP, _I, _DP,
                                          ctypes.POINTER(ctypes.c_uint8)]),
+    "relief_gpu_map_smooth_chain_device": (_I, [_P, _CS, ctypes.POINTER(_I), ctypes.POINTER(_I), _DP, _I,
+                                                ctypes.c_void_p, ctypes.c_void_p]),
+    "relief_gpu_map_chain_seconds": (_D, [_P]),
     "relief_gpu_smooth_chain": (_I, [_DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, ctypes.POINTER(_I),
                                      ctypes.POINTER(_I), _DP, _I, _DP, ctypes.POINTER(ctypes.c_uint8)]),
     "relief_gpu_sim_render": (ctypes.c_int64, [_CS, _DP, _D, ctypes.c_uint64, ctypes.c_uint64, _DP,
@@ -314,6 +317,16 @@ class ReliefMap:
             self.handle, layer.encode(), kinds, radii, sig, len(steps), _dptr(vals),
             ok.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
         return vals.reshape(self.height, self.width), ok.reshape(self.height, self.width)
+
+    def smooth_chain_device(self, layer: str, steps: Sequence[tuple], d_values: int, d_valid: int) -> float:
+        """Chain with device outputs (raw device pointers); returns its device seconds."""
+        kinds = (ctypes.c_int * len(steps))(*[s[0] for s in steps])
+        radii = (ctypes.c_int * len(steps))(*[s[1] for s in steps])
+        sig = (ctypes.c_double * len(steps))(*[float(s[2]) for s in steps])
+        _check(self.lib, self.lib.relief_gpu_map_smooth_chain_device(
+            self.handle, layer.encode(), kinds, radii, sig, len(steps), ctypes.c_void_p(d_values),
+            ctypes.c_void_p(d_valid)))
+        return float(self.lib.relief_gpu_map_chain_seconds(self.handle))
 
     def close(self) -> None:
         if self.handle:

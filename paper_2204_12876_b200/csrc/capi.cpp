@@ -370,6 +370,23 @@ relief_status relief_gpu_map_smooth_chain(const relief_map* map, const char* lay
   });
 }
 
+relief_status relief_gpu_map_smooth_chain_device(const relief_map* map, const char* layer,
+                                                 const int* kinds, const int* radii,
+                                                 const double* sigmas, int n_steps,
+                                                 double* d_values_out, uint8_t* d_valid_out) {
+  if (map == nullptr || layer == nullptr || d_values_out == nullptr || d_valid_out == nullptr ||
+      (n_steps > 0 && (kinds == nullptr || radii == nullptr || sigmas == nullptr)))
+    return usage("null argument");
+  return guard([&] {
+    rb200::runMapChainDevice(*map->dev, layer, kinds, radii, sigmas, n_steps, d_values_out,
+                             d_valid_out);
+  });
+}
+
+double relief_gpu_map_chain_seconds(const relief_map* map) {
+  return map ? map->dev->last_chain_seconds : 0.0;
+}
+
 relief_status relief_gpu_smooth_chain(const double* values, const uint8_t* valid, int width,
                                       int height, const int* kinds, const int* radii,
                                       const double* sigmas, int n_steps, double* values_out,

@@ -155,6 +155,10 @@ void destroyDeviceMap(DeviceMap* m) {
   cudaFree(m->pslab);
   cudaFree(m->rslab);
   cudaFree(m->export_buf);
+  m->chain.release();
+  cudaFree(m->chain_in);
+  cudaFree(m->chain_out);
+  cudaFree(m->chain_out_ok);
   cudaFree(m->hist);
   cudaFree(m->stats);
   cudaFree(m->drift_offset);

@@ -61,6 +61,21 @@ struct GridArgs {
   double xmax, ymax;  // ox + W*res, oy + H*res
 };
 
+// Device scratch of the post-processing chain (postchain.cu), sized W*H.
+struct ChainScratch {
+  double* va = nullptr;
+  double* vb = nullptr;
+  uint8_t* oa = nullptr;
+  uint8_t* ob = nullptr;
+  int* parent = nullptr;
+  unsigned long long* key = nullptr;
+  uint8_t* border = nullptr;
+  int* flag = nullptr;
+  std::size_t cap = 0;
+  void ensure(std::size_t n);
+  void release();
+};
+
 struct DeviceMap {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -103,7 +118,13 @@ struct DeviceMap {
   double last_stamp = 0.0;
   bool has_last = false;
   double* export_buf = nullptr;  // masked-layer staging for get_layer
-  cudaEvent_t ev[8] = {};
+  ChainScratch chain;            // post-processing chain scratch
+  double* chain_in = nullptr;    // masked input layer of the chain
+  double* chain_out = nullptr;   // chain output staging for host callers
+  uint8_t* chain_out_ok = nullptr;
+  double last_chain_seconds = 0.0;
+  int last_chain_launches = 0;
+  cudaEvent_t ev[12] = {};
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
   long long last_launches = 0;
@@ -147,8 +168,11 @@ struct ChainStep {
   int radius;
   double sigma;
 };
-void smoothChainDevice(int device, cudaStream_t stream, const double* d_values,
+// Enqueues the chain on `s` (no host sync); returns the number of launches.
+int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
                        const uint8_t* d_valid, int W, int H, const ChainStep* steps, int n_steps,
                        double* d_values_out, uint8_t* d_valid_out);
+// Syncs `s` and raises NothingToInpaint if an inpaint step saw no valid cell.
+void smoothChainCheck(cudaStream_t s, ChainScratch& sc);
 
 }  // namespace rb200

@@ -6,6 +6,10 @@
 // valid border. Sums run in the reference's row-major window order, the median
 // sorts the same window values, and the inpaint minimum is order independent,
 // so every step is bit-exact.
+//
+// Everything is enqueued on one stream with scratch owned by the caller (the
+// map keeps one set), so a chain is a handful of launches and no host syncs;
+// a "nothing to inpaint" condition is flagged on the device and raised after.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -15,20 +19,26 @@
 #include "device_map.hpp"
 #include "fp_exact.cuh"
 #include "runners.hpp"
+#include "snapshot.hpp"
 
 namespace rb200 {
 
 namespace {
 
 constexpr int kT = 256;
-constexpr int kMaxMedianWindow = 121;  // radius <= 5
+constexpr int kMaxWindow = 121;  // radius <= 5
+
+struct Weights {
+  double w[kMaxWindow];
+};
 
 __global__ void __launch_bounds__(kT) k_linear(const double* __restrict__ v,
                                                const uint8_t* __restrict__ ok, int W, int H,
-                                               int R, const double* __restrict__ w,
-                                               double* __restrict__ out) {
+                                               int R, Weights wt, double* __restrict__ out,
+                                               uint8_t* __restrict__ ok_out) {
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= W * H) return;
+  ok_out[i] = ok[i];
   if (!ok[i]) {
     out[i] = v[i];
     return;
@@ -43,9 +53,9 @@ __global__ void __launch_bounds__(kT) k_linear(const double* __restrict__ v,
       if (cc < 0 || cc >= W) continue;
       const int j = rr * W + cc;
       if (!ok[j]) continue;
-      const double wt = w[(dr + R) * k + (dc + R)];
-      acc += wt * v[j];
-      ws += wt;
+      const double w = wt.w[(dr + R) * k + (dc + R)];
+      acc += w * v[j];
+      ws += w;
     }
   }
   out[i] = acc / ws;
@@ -53,15 +63,17 @@ __global__ void __launch_bounds__(kT) k_linear(const double* __restrict__ v,
 
 __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
                                                const uint8_t* __restrict__ ok, int W, int H,
-                                               int R, double* __restrict__ out) {
+                                               int R, double* __restrict__ out,
+                                               uint8_t* __restrict__ ok_out) {
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= W * H) return;
+  ok_out[i] = ok[i];
   if (!ok[i]) {
     out[i] = v[i];
     return;
   }
   const int r = i / W, c = i - (i / W) * W;
-  double win[kMaxMedianWindow];
+  double win[kMaxWindow];
   int n = 0;
   for (int dr = -R; dr <= R; ++dr) {
     const int rr = r + dr;
@@ -71,8 +83,7 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
       if (cc < 0 || cc >= W) continue;
       const int j = rr * W + cc;
       if (!ok[j]) continue;
-      // insertion keeps the window sorted ascending
-      const double x = v[j];
+      const double x = v[j];  // insertion keeps the window sorted ascending
       int p = n++;
       while (p > 0 && x < win[p - 1]) {
         win[p] = win[p - 1];
@@ -118,6 +129,7 @@ __device__ __forceinline__ double fromKey(unsigned long long k) {
   const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
   return __longlong_as_double(static_cast<long long>(b));
 }
+constexpr unsigned long long kKeyInf = 0xfff0000000000000ULL;  // orderKey(+inf)
 
 __global__ void __launch_bounds__(kT) k_cc_init(const uint8_t* ok, int n, int* parent,
                                                 unsigned long long* key, uint8_t* border,
@@ -125,7 +137,7 @@ __global__ void __launch_bounds__(kT) k_cc_init(const uint8_t* ok, int n, int* p
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= n) return;
   parent[i] = i;
-  key[i] = 0xfff0000000000000ULL;  // orderKey(+inf)
+  key[i] = kKeyInf;
   border[i] = 0;
   if (ok[i]) *any_valid = 1;
 }
@@ -147,7 +159,7 @@ __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t
   parent[i] = root;
   const int r = i / W, c = i - (i / W) * W;
   bool any = false;
-  unsigned long long best = 0xfff0000000000000ULL;
+  unsigned long long best = kKeyInf;
   for (int dr = -1; dr <= 1; ++dr) {
     for (int dc = -1; dc <= 1; ++dc) {
       if (dr == 0 && dc == 0) continue;
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t
       if (rr < 0 || rr >= H || cc < 0 || cc >= W) continue;
       const int j = rr * W + cc;
       if (!ok[j]) continue;
-      any = true;
+      any = true;  // a NaN neighbour still counts as border (reference has_border)
       const double x = v[j];
       if (x == x) {
         const unsigned long long kx = orderKey(x);
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t
   }
   if (any) {
     border[root] = 1;
-    if (best < 0xfff0000000000000ULL) atomicMin(key + root, best);
+    if (best < kKeyInf) atomicMin(key + root, best);
   }
 }
 
@@ -190,94 +202,112 @@ __global__ void __launch_bounds__(kT) k_cc_fill(const double* v, const uint8_t* 
   }
 }
 
+// flag[0] = any valid cell seen at an inpaint step (per step, OR-ed into
+// flag[1] = "some inpaint step had nothing to inpaint").
+__global__ void k_check_any(int* flag) {
+  if (flag[0] == 0) flag[1] = 1;
+  flag[0] = 0;
+}
+
 }  // namespace
 
-void smoothChainDevice(int device, cudaStream_t s, const double* d_values, const uint8_t* d_valid,
-                       int W, int H, const ChainStep* steps, int n_steps, double* d_values_out,
-                       uint8_t* d_valid_out) {
-  checkCuda(cudaSetDevice(device), "cudaSetDevice");
+void ChainScratch::ensure(std::size_t n) {
+  if (n <= cap) return;
+  release();
+  checkCuda(cudaMalloc(&va, n * sizeof(double)), "chain scratch");
+  checkCuda(cudaMalloc(&vb, n * sizeof(double)), "chain scratch");
+  checkCuda(cudaMalloc(&oa, n), "chain scratch");
+  checkCuda(cudaMalloc(&ob, n), "chain scratch");
+  checkCuda(cudaMalloc(&parent, n * sizeof(int)), "chain scratch");
+  checkCuda(cudaMalloc(&key, n * sizeof(unsigned long long)), "chain scratch");
+  checkCuda(cudaMalloc(&border, n), "chain scratch");
+  checkCuda(cudaMalloc(&flag, 2 * sizeof(int)), "chain scratch");
+  cap = n;
+}
+
+void ChainScratch::release() {
+  cudaFree(va);
+  cudaFree(vb);
+  cudaFree(oa);
+  cudaFree(ob);
+  cudaFree(parent);
+  cudaFree(key);
+  cudaFree(border);
+  cudaFree(flag);
+  va = vb = nullptr;
+  oa = ob = border = nullptr;
+  parent = flag = nullptr;
+  key = nullptr;
+  cap = 0;
+}
+
+int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
+                       const uint8_t* d_valid, int W, int H, const ChainStep* steps, int n_steps,
+                       double* d_values_out, uint8_t* d_valid_out) {
   if (W <= 0 || H <= 0) fail(Err::kUsage, "malformed masked layer");
-  const int n = W * H;
-  const unsigned grid = static_cast<unsigned>((n + kT - 1) / kT);
-  double *va = nullptr, *vb = nullptr, *w = nullptr;
-  uint8_t *oa = nullptr, *ob = nullptr, *border = nullptr;
-  int *parent = nullptr, *flag = nullptr;
-  unsigned long long* key = nullptr;
-  struct Free {
-    std::vector<void*> ptrs;
-    ~Free() {
-      for (void* p : ptrs) cudaFree(p);
-    }
-  } guard;
-  const auto alloc = [&](auto** p, std::size_t bytes) {
-    checkCuda(cudaMalloc(reinterpret_cast<void**>(p), bytes), "chain scratch");
-    guard.ptrs.push_back(*p);
-  };
-  alloc(&va, n * sizeof(double));
-  alloc(&vb, n * sizeof(double));
-  alloc(&oa, n);
-  alloc(&ob, n);
-  checkCuda(cudaMemcpyAsync(va, d_values, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
-  checkCuda(cudaMemcpyAsync(oa, d_valid, n, cudaMemcpyDeviceToDevice, s), "copy");
   for (int k = 0; k < n_steps; ++k) {
     const ChainStep& st = steps[k];
+    if (st.kind < 0 || st.kind > 3) fail(Err::kUsage, "unknown filter kind");
     if (st.kind != 3 && st.radius < 1) fail(Err::kUsage, "filter radius must be >= 1");
     if (st.kind == 0 && !(st.sigma > 0.0)) fail(Err::kUsage, "gaussian sigma must be > 0");
-    if (st.kind == 0 || st.kind == 1) {
-      const int kk = 2 * st.radius + 1;
-      std::vector<double> hw(static_cast<std::size_t>(kk) * kk, 1.0);
-      if (st.kind == 0)
-        for (int dr = -st.radius; dr <= st.radius; ++dr)
-          for (int dc = -st.radius; dc <= st.radius; ++dc)
-            hw[static_cast<std::size_t>(dr + st.radius) * kk + (dc + st.radius)] =
-                std::exp(-(dr * dr + dc * dc) / (2.0 * st.sigma * st.sigma));  // host libm
-      cudaFree(w);
-      w = nullptr;
-      checkCuda(cudaMalloc(&w, hw.size() * sizeof(double)), "weights");
-      checkCuda(cudaMemcpyAsync(w, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, s),
-                "weights");
-      k_linear<<<grid, kT, 0, s>>>(va, oa, W, H, st.radius, w, vb);
-      checkCuda(cudaMemcpyAsync(ob, oa, n, cudaMemcpyDeviceToDevice, s), "copy");
-      checkCuda(cudaStreamSynchronize(s), "linear step");
-    } else if (st.kind == 2) {
-      if ((2 * st.radius + 1) * (2 * st.radius + 1) > kMaxMedianWindow)
-        fail(Err::kUsage, "median radius above 5 is not supported");
-      k_median<<<grid, kT, 0, s>>>(va, oa, W, H, st.radius, vb);
-      checkCuda(cudaMemcpyAsync(ob, oa, n, cudaMemcpyDeviceToDevice, s), "copy");
-    } else {
-      if (parent == nullptr) {
-        alloc(&parent, n * sizeof(int));
-        alloc(&key, n * sizeof(unsigned long long));
-        alloc(&border, n);
-        alloc(&flag, sizeof(int));
-      }
-      checkCuda(cudaMemsetAsync(flag, 0, sizeof(int), s), "memset");
-      k_cc_init<<<grid, kT, 0, s>>>(oa, n, parent, key, border, flag);
-      int any = 0;
-      checkCuda(cudaMemcpyAsync(&any, flag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag");
-      checkCuda(cudaStreamSynchronize(s), "inpaint");
-      if (!any) fail(Err::kNothingToInpaint, "layer has no valid cells");
-      k_cc_union<<<grid, kT, 0, s>>>(oa, W, H, parent);
-      k_cc_border<<<grid, kT, 0, s>>>(va, oa, W, H, parent, key, border);
-      k_cc_fill<<<grid, kT, 0, s>>>(va, oa, n, parent, key, border, vb, ob);
-    }
-    checkCuda(cudaGetLastError(), "chain step");
-    std::swap(va, vb);
-    std::swap(oa, ob);
+    if (st.kind != 3 && (2 * st.radius + 1) * (2 * st.radius + 1) > kMaxWindow)
+      fail(Err::kUsage, "filter radius above 5 is not supported");
   }
-  checkCuda(cudaMemcpyAsync(d_values_out, va, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
-  checkCuda(cudaMemcpyAsync(d_valid_out, oa, n, cudaMemcpyDeviceToDevice, s), "copy");
+  const int n = W * H;
+  sc.ensure(static_cast<std::size_t>(n));
+  const unsigned grid = static_cast<unsigned>((n + kT - 1) / kT);
+  int launches = 0;
+  checkCuda(cudaMemsetAsync(sc.flag, 0, 2 * sizeof(int), s), "memset");
+  const double* cv = d_values;
+  const uint8_t* co = d_valid;
+  double* bufs[2] = {sc.va, sc.vb};
+  uint8_t* oks[2] = {sc.oa, sc.ob};
+  int which = 0;
+  for (int k = 0; k < n_steps; ++k) {
+    const ChainStep& st = steps[k];
+    double* nv = bufs[which];
+    uint8_t* no = oks[which];
+    if (st.kind == 0 || st.kind == 1) {
+      Weights wt{};
+      const int kk = 2 * st.radius + 1;
+      for (int dr = -st.radius; dr <= st.radius; ++dr)
+        for (int dc = -st.radius; dc <= st.radius; ++dc)
+          wt.w[(dr + st.radius) * kk + (dc + st.radius)] =
+              st.kind == 1 ? 1.0 : std::exp(-(dr * dr + dc * dc) / (2.0 * st.sigma * st.sigma));
+      k_linear<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, wt, nv, no);
+      ++launches;
+    } else if (st.kind == 2) {
+      k_median<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, nv, no);
+      ++launches;
+    } else {
+      k_cc_init<<<grid, kT, 0, s>>>(co, n, sc.parent, sc.key, sc.border, sc.flag);
+      k_check_any<<<1, 1, 0, s>>>(sc.flag);
+      k_cc_union<<<grid, kT, 0, s>>>(co, W, H, sc.parent);
+      k_cc_border<<<grid, kT, 0, s>>>(cv, co, W, H, sc.parent, sc.key, sc.border);
+      k_cc_fill<<<grid, kT, 0, s>>>(cv, co, n, sc.parent, sc.key, sc.border, nv, no);
+      launches += 5;
+    }
+    cv = nv;
+    co = no;
+    which ^= 1;
+  }
+  checkCuda(cudaMemcpyAsync(d_values_out, cv, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+  checkCuda(cudaMemcpyAsync(d_valid_out, co, n, cudaMemcpyDeviceToDevice, s), "copy");
+  checkCuda(cudaGetLastError(), "chain launch");
+  return launches;
+}
+
+void smoothChainCheck(cudaStream_t s, ChainScratch& sc) {
+  int flags[2] = {0, 0};
+  checkCuda(cudaMemcpyAsync(flags, sc.flag, sizeof flags, cudaMemcpyDeviceToHost, s), "flag");
   checkCuda(cudaStreamSynchronize(s), "chain");
-  cudaFree(w);
+  if (flags[1]) fail(Err::kNothingToInpaint, "layer has no valid cells");
 }
 
 namespace {
 std::vector<ChainStep> makeSteps(const int* kinds, const int* radii, const double* sigmas, int n) {
   std::vector<ChainStep> steps(n > 0 ? n : 0);
-  for (int k = 0; k < n; ++k) {
-    if (kinds[k] < 0 || kinds[k] > 3) fail(Err::kUsage, "unknown filter kind");
-    steps[k] = {kinds[k], radii[k], sigmas[k]};
-  }
+  for (int k = 0; k < n; ++k) steps[k] = {kinds[k], radii[k], sigmas[k]};
   return steps;
 }
 }  // namespace
@@ -289,55 +319,62 @@ void runHostChain(int device, const double* values, const uint8_t* valid, int W,
   const std::vector<ChainStep> steps = makeSteps(kinds, radii, sigmas, n_steps);
   checkCuda(cudaSetDevice(device), "cudaSetDevice");
   const std::size_t n = static_cast<std::size_t>(W) * H;
-  double* dv = nullptr;
-  uint8_t* dm = nullptr;
-  checkCuda(cudaMalloc(&dv, n * sizeof(double)), "chain input");
-  if (cudaMalloc(&dm, n) != cudaSuccess) {
-    cudaFree(dv);
-    fail(Err::kDevice, "chain input allocation failed");
-  }
-  try {
-    checkCuda(cudaMemcpy(dv, values, n * sizeof(double), cudaMemcpyHostToDevice), "upload");
-    checkCuda(cudaMemcpy(dm, valid, n, cudaMemcpyHostToDevice), "upload");
-    smoothChainDevice(device, nullptr, dv, dm, W, H, steps.data(), n_steps, dv, dm);
-    checkCuda(cudaMemcpy(values_out, dv, n * sizeof(double), cudaMemcpyDeviceToHost), "download");
-    checkCuda(cudaMemcpy(valid_out, dm, n, cudaMemcpyDeviceToHost), "download");
-  } catch (...) {
-    cudaFree(dv);
-    cudaFree(dm);
-    throw;
-  }
-  cudaFree(dv);
-  cudaFree(dm);
+  ChainScratch sc;
+  struct Guard {
+    ChainScratch& sc;
+    double* dv = nullptr;
+    uint8_t* dm = nullptr;
+    ~Guard() {
+      sc.release();
+      cudaFree(dv);
+      cudaFree(dm);
+    }
+  } g{sc};
+  checkCuda(cudaMalloc(&g.dv, n * sizeof(double)), "chain input");
+  checkCuda(cudaMalloc(&g.dm, n), "chain input");
+  checkCuda(cudaMemcpy(g.dv, values, n * sizeof(double), cudaMemcpyHostToDevice), "upload");
+  checkCuda(cudaMemcpy(g.dm, valid, n, cudaMemcpyHostToDevice), "upload");
+  smoothChainEnqueue(nullptr, sc, g.dv, g.dm, W, H, steps.data(), n_steps, g.dv, g.dm);
+  smoothChainCheck(nullptr, sc);
+  checkCuda(cudaMemcpy(values_out, g.dv, n * sizeof(double), cudaMemcpyDeviceToHost), "download");
+  checkCuda(cudaMemcpy(valid_out, g.dm, n, cudaMemcpyDeviceToHost), "download");
+}
+
+void runMapChainDevice(DeviceMap& m, const std::string& layer, const int* kinds, const int* radii,
+                       const double* sigmas, int n_steps, double* d_values_out,
+                       uint8_t* d_valid_out) {
+  const std::vector<ChainStep> steps = makeSteps(kinds, radii, sigmas, n_steps);
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  const std::size_t n = m.grid.cells();
+  m.chain.ensure(n);
+  if (m.chain_in == nullptr) checkCuda(cudaMalloc(&m.chain_in, n * sizeof(double)), "chain input");
+  if (!exportLayerDevice(m, layer.c_str(), m.chain_in))
+    fail(Err::kUsage, unknownLayerMessage(layer));
+  const uint8_t* mask = layer == "upper_bound" ? m.cur.ubv : m.cur.valid;
+  checkCuda(cudaEventRecord(m.ev[8], m.stream), "event");
+  m.last_chain_launches = smoothChainEnqueue(m.stream, m.chain, m.chain_in, mask, m.grid.width,
+                                             m.grid.height, steps.data(), n_steps, d_values_out,
+                                             d_valid_out);
+  checkCuda(cudaEventRecord(m.ev[9], m.stream), "event");
+  smoothChainCheck(m.stream, m.chain);
+  float ms = 0.f;
+  checkCuda(cudaEventElapsedTime(&ms, m.ev[8], m.ev[9]), "timing");
+  m.last_chain_seconds = ms * 1e-3;
 }
 
 void runMapChain(DeviceMap& m, const std::string& layer, const int* kinds, const int* radii,
                  const double* sigmas, int n_steps, double* values_out, uint8_t* valid_out) {
-  const std::vector<ChainStep> steps = makeSteps(kinds, radii, sigmas, n_steps);
-  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
   const std::size_t n = m.grid.cells();
-  double* dv = nullptr;
-  uint8_t* dm = nullptr;
-  checkCuda(cudaMalloc(&dv, n * sizeof(double)), "chain input");
-  if (cudaMalloc(&dm, n) != cudaSuccess) {
-    cudaFree(dv);
-    fail(Err::kDevice, "chain input allocation failed");
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (m.chain_out == nullptr) {
+    checkCuda(cudaMalloc(&m.chain_out, n * sizeof(double)), "chain output");
+    checkCuda(cudaMalloc(&m.chain_out_ok, n), "chain output");
   }
-  try {
-    if (!exportLayerDevice(m, layer.c_str(), dv)) fail(Err::kUsage, "unknown layer '" + layer + "'");
-    const uint8_t* mask = layer == "upper_bound" ? m.cur.ubv : m.cur.valid;
-    checkCuda(cudaMemcpyAsync(dm, mask, n, cudaMemcpyDeviceToDevice, m.stream), "mask");
-    smoothChainDevice(m.device, m.stream, dv, dm, m.grid.width, m.grid.height, steps.data(),
-                      n_steps, dv, dm);
-    checkCuda(cudaMemcpy(values_out, dv, n * sizeof(double), cudaMemcpyDeviceToHost), "download");
-    checkCuda(cudaMemcpy(valid_out, dm, n, cudaMemcpyDeviceToHost), "download");
-  } catch (...) {
-    cudaFree(dv);
-    cudaFree(dm);
-    throw;
-  }
-  cudaFree(dv);
-  cudaFree(dm);
+  runMapChainDevice(m, layer, kinds, radii, sigmas, n_steps, m.chain_out, m.chain_out_ok);
+  checkCuda(cudaMemcpyAsync(values_out, m.chain_out, n * sizeof(double), cudaMemcpyDeviceToHost,
+                            m.stream), "download");
+  checkCuda(cudaMemcpyAsync(valid_out, m.chain_out_ok, n, cudaMemcpyDeviceToHost, m.stream), "download");
+  checkCuda(cudaStreamSynchronize(m.stream), "download");
 }
 
 }  // namespace rb200

@@ -26,6 +26,9 @@ std::size_t runSegment(const std::string& snapshot_path, const char* config_path
 
 void runMapChain(DeviceMap& m, const std::string& layer, const int* kinds, const int* radii,
                  const double* sigmas, int n_steps, double* values_out, uint8_t* valid_out);
+void runMapChainDevice(DeviceMap& m, const std::string& layer, const int* kinds, const int* radii,
+                       const double* sigmas, int n_steps, double* d_values_out,
+                       uint8_t* d_valid_out);
 void runHostChain(int device, const double* values, const uint8_t* valid, int width, int height,
                   const int* kinds, const int* radii, const double* sigmas, int n_steps,
                   double* values_out, uint8_t* valid_out);
