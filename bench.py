@@ -77,9 +77,11 @@ class ClockSampler:
             import pynvml
             import torch
             pynvml.nvmlInit()
-            bus = torch.cuda.get_device_properties(device).pci_bus_id
+            props = torch.cuda.get_device_properties(device)
+            bus = (f"{int(getattr(props, 'pci_domain_id', 0)):08X}:{int(props.pci_bus_id):02X}:"
+                   f"{int(getattr(props, 'pci_device_id', 0)):02X}.0")
             try:
-                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
             except Exception:
                 self.handle = pynvml.nvmlDeviceGetHandleByIndex(device)
             self.nv = pynvml
@@ -365,6 +367,8 @@ def roofline(dom, kmean, m, w, pts, frames):
 
 # ---------------------------------------------------------------- main
 def main():
+    import faulthandler
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

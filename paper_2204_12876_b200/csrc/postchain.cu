@@ -95,30 +95,44 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
   out[i] = (n % 2 == 1) ? win[n / 2] : 0.5 * (win[n / 2 - 1] + win[n / 2]);
 }
 
-// ---- min inpaint
-__device__ __forceinline__ int findRoot(const int* p, int x) {
-  int y = p[x];
-  while (y != x) {
-    x = y;
-    y = p[x];
+// ---- min inpaint: connected components of invalid cells (4-neighbour),
+// ECL-CC style: every parent index is smaller than its child, the initial
+// forest links each cell to its left / upper invalid neighbour, finds use
+// intermediate pointer jumping, and a flatten pass makes parent[i] the root.
+__device__ __forceinline__ int representative(int* p, int x) {
+  int cur = p[x];
+  if (cur != x) {
+    int next, prev = x;
+    while (cur > (next = p[cur])) {
+      p[prev] = next;
+      prev = cur;
+      cur = next;
+    }
   }
-  return x;
+  return cur;
 }
 
-__device__ void unite(int* p, int a, int b) {
-  while (true) {
-    a = findRoot(p, a);
-    b = findRoot(p, b);
-    if (a == b) return;
-    if (a > b) {
-      const int t = a;
-      a = b;
-      b = t;
+__device__ void hook(int* p, int a, int b) {
+  int ra = representative(p, a), rb = representative(p, b);
+  bool repeat;
+  do {
+    repeat = false;
+    if (ra != rb) {
+      if (ra < rb) {
+        const int ret = atomicCAS(p + rb, rb, ra);
+        if (ret != rb) {
+          rb = ret;
+          repeat = true;
+        }
+      } else {
+        const int ret = atomicCAS(p + ra, ra, rb);
+        if (ret != ra) {
+          ra = ret;
+          repeat = true;
+        }
+      }
     }
-    const int old = atomicCAS(p + b, b, a);
-    if (old == b) return;
-    b = old;
-  }
+  } while (repeat);
 }
 
 __device__ __forceinline__ unsigned long long orderKey(double v) {
@@ -131,32 +145,57 @@ __device__ __forceinline__ double fromKey(unsigned long long k) {
 }
 constexpr unsigned long long kKeyInf = 0xfff0000000000000ULL;  // orderKey(+inf)
 
-__global__ void __launch_bounds__(kT) k_cc_init(const uint8_t* ok, int n, int* parent,
+__global__ void __launch_bounds__(kT) k_cc_init(const uint8_t* ok, int W, int H, int* parent,
                                                 unsigned long long* key, uint8_t* border,
                                                 int* any_valid) {
   const int i = blockIdx.x * kT + threadIdx.x;
-  if (i >= n) return;
-  parent[i] = i;
+  if (i >= W * H) return;
   key[i] = kKeyInf;
   border[i] = 0;
-  if (ok[i]) *any_valid = 1;
+  if (ok[i]) {
+    *any_valid = 1;
+    parent[i] = i;
+    return;
+  }
+  const int c = i % W;
+  int p = i;
+  if (c > 0 && !ok[i - 1]) p = i - 1;
+  else if (i >= W && !ok[i - W]) p = i - W;
+  parent[i] = p;
 }
 
 __global__ void __launch_bounds__(kT) k_cc_union(const uint8_t* ok, int W, int H, int* parent) {
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= W * H || ok[i]) return;
-  const int r = i / W, c = i - (i / W) * W;
-  if (c + 1 < W && !ok[i + 1]) unite(parent, i, i + 1);
-  if (r + 1 < H && !ok[i + W]) unite(parent, i, i + W);
+  // The initial forest already joined i to its left neighbour when both are
+  // invalid; the upper neighbour still needs an explicit union then.
+  const int c = i % W;
+  if (c > 0 && !ok[i - 1] && i >= W && !ok[i - W]) hook(parent, i, i - W);
+}
+
+__global__ void __launch_bounds__(kT) k_cc_flatten(const uint8_t* ok, int n, int* parent) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= n || ok[i]) return;
+  parent[i] = representative(parent, i);
+}
+
+// Second flatten without path writes: the compressing pass above can leave an
+// entry pointing at a non-root ancestor when another thread's compression
+// overwrote it; now every chain is short and only own entries are written.
+__global__ void __launch_bounds__(kT) k_cc_flatten2(const uint8_t* ok, int n, int* parent) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= n || ok[i]) return;
+  int r = parent[i];
+  while (parent[r] != r) r = parent[r];
+  parent[i] = r;
 }
 
 __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t* ok, int W, int H,
-                                                  int* parent, unsigned long long* key,
+                                                  const int* parent, unsigned long long* key,
                                                   uint8_t* border) {
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= W * H || ok[i]) return;
-  const int root = findRoot(parent, i);
-  parent[i] = root;
+  const int root = parent[i];
   const int r = i / W, c = i - (i / W) * W;
   bool any = false;
   unsigned long long best = kKeyInf;
@@ -176,8 +215,8 @@ __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t
     }
   }
   if (any) {
-    border[root] = 1;
-    if (best < kKeyInf) atomicMin(key + root, best);
+    if (!border[root]) border[root] = 1;
+    if (best < kKeyInf && best < key[root]) atomicMin(key + root, best);
   }
 }
 
@@ -192,7 +231,7 @@ __global__ void __launch_bounds__(kT) k_cc_fill(const double* v, const uint8_t* 
     ok_out[i] = 1;
     return;
   }
-  const int root = findRoot(parent, i);
+  const int root = parent[i];
   if (border[root]) {
     out[i] = fromKey(key[root]);
     ok_out[i] = 1;
@@ -280,12 +319,14 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
       k_median<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, nv, no);
       ++launches;
     } else {
-      k_cc_init<<<grid, kT, 0, s>>>(co, n, sc.parent, sc.key, sc.border, sc.flag);
+      k_cc_init<<<grid, kT, 0, s>>>(co, W, H, sc.parent, sc.key, sc.border, sc.flag);
       k_check_any<<<1, 1, 0, s>>>(sc.flag);
       k_cc_union<<<grid, kT, 0, s>>>(co, W, H, sc.parent);
+      k_cc_flatten<<<grid, kT, 0, s>>>(co, n, sc.parent);
+      k_cc_flatten2<<<grid, kT, 0, s>>>(co, n, sc.parent);
       k_cc_border<<<grid, kT, 0, s>>>(cv, co, W, H, sc.parent, sc.key, sc.border);
       k_cc_fill<<<grid, kT, 0, s>>>(cv, co, n, sc.parent, sc.key, sc.border, nv, no);
-      launches += 5;
+      launches += 6;
     }
     cv = nv;
     co = no;
