@@ -791,6 +791,108 @@ __device__ __noinline__ void candidateVisit(const Layers& L, uint32_t c, double 
   if (k < kstar[c]) atomicMin(kstar + c, k);
 }
 
+struct Pass1Ctx {
+  const uint8_t* cls;
+  Layers L;
+  int32_t* kstar;
+  double oz, dz, vx, vy, alpha_n;
+  int32_t k;
+};
+
+__device__ __forceinline__ void pass1Visit(const Pass1Ctx& c, uint8_t cl, uint32_t idx, double h,
+                                           bool& touched) {
+  if (cl == kClsBound) {
+    boundMin(c.L, idx, h);
+    return;
+  }
+  touched = true;
+  candidateVisit(c.L, idx, h, c.vx, c.vy, c.dz, c.alpha_n, c.k, c.kstar);
+}
+
+// Pass-1 walk of a ray with finite xy deltas: the traversal of walkRayFinite
+// with the class probe software-pipelined -- the next cell's class byte is
+// loaded before the current cell is handled, so the L1 latency overlaps the
+// current visit. Visit side effects (bound min, k* min) are order independent.
+__device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3], double px,
+                                            double py, const Pass1Ctx& c, bool& touched,
+                                            unsigned& visits) {
+  const double dx = px - o[0];
+  const double dy = py - o[1];
+  const double res = g.res;
+  if (libm_hypot(dx, dy) < 1e-12) {
+    if (o[0] >= g.ox && o[0] < g.xmax && o[1] >= g.oy && o[1] < g.ymax) {
+      const uint32_t idx =
+          static_cast<uint32_t>(clampCell(x86_to_int(floor((o[1] - g.oy) / res)), g.H)) * g.W +
+          clampCell(x86_to_int(floor((o[0] - g.ox) / res)), g.W);
+      ++visits;
+      const uint8_t cl = c.cls[idx];
+      if (cl) pass1Visit(c, cl, idx, o[2] + 0.5 * c.dz, touched);
+    }
+    return;
+  }
+  double t0 = 0.0, t1 = 1.0;
+  if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return;
+  if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return;
+  if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return;
+  if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
+  if (t0 >= t1) return;
+  const bool end_in = px >= g.ox && px < g.xmax && py >= g.oy && py < g.ymax;
+  uint32_t end_idx = 0xffffffffu;
+  if (end_in)
+    end_idx = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H)) * g.W +
+              clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
+  int col = clampCell(x86_to_int(floor(((o[0] + t0 * dx) - g.ox) / res)), g.W);
+  int row = clampCell(x86_to_int(floor(((o[1] + t0 * dy) - g.oy) / res)), g.H);
+  const int step_col = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+  const int step_row = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+  double tmx = kInf, tmy = kInf, tdx = kInf, tdy = kInf;
+  if (step_col != 0) {
+    tmx = ((g.ox + (col + (step_col > 0 ? 1 : 0)) * res) - o[0]) / dx;
+    tdx = res / fabs(dx);
+  }
+  if (step_row != 0) {
+    tmy = ((g.oy + (row + (step_row > 0 ? 1 : 0)) * res) - o[1]) / dy;
+    tdy = res / fabs(dy);
+  }
+  uint32_t idx = static_cast<uint32_t>(row) * g.W + col;
+  const int step_idx_row = step_row * g.W;
+  const unsigned W = static_cast<unsigned>(g.W), H = static_cast<unsigned>(g.H);
+  const uint8_t* __restrict__ cls = c.cls;
+  uint8_t cl = cls[idx];
+  double t_enter = t0;
+  while (true) {
+    const bool sx = tmx < tmy;
+    const double m = sx ? tmx : tmy;
+    const bool more = m < t1;
+    const double t_next = more ? m : t1;
+    const bool emit = idx != end_idx && t_next > t_enter;
+    const uint32_t cur = idx;
+    const uint8_t ccl = cl;
+    const double te = t_enter;
+    bool stop = !more;
+    if (!stop) {
+      if (sx) {
+        col += step_col;
+        tmx += tdx;
+        idx += step_col;
+        stop = static_cast<unsigned>(col) >= W;
+      } else {
+        row += step_row;
+        tmy += tdy;
+        idx += step_idx_row;
+        stop = static_cast<unsigned>(row) >= H;
+      }
+      if (!stop) cl = cls[idx];  // prefetch the next cell's class
+    }
+    if (emit) {
+      ++visits;
+      if (ccl) pass1Visit(c, ccl, cur, c.oz + (0.5 * (te + t_next)) * c.dz, touched);
+    }
+    if (stop) break;
+    t_enter = t_next;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 4)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
@@ -801,20 +903,17 @@ __global__ void __launch_bounds__(kThreads, 4)
   unsigned visits = 0;
   if (k < n && kept[k]) {
     const double ex = px[k], ey = py[k], ez = pz[k];
-    const double dz = ez - a.o[2];
-    walk(a.g, a.o, ex, ey, [&](uint32_t c, double te, double tn, bool vertical) {
-      ++visits;
-      const uint8_t cl = cls[c];
-      if (cl == kClsNone) return;
-      const double h = rayHeight(a.o[2], dz, te, tn, vertical);
-      if (cl == kClsBound) {
-        boundMin(L, c, h);
-        return;
-      }
-      touched = true;
-      candidateVisit(L, c, h, ex - a.o[0], ey - a.o[1], dz, a.alpha_n, static_cast<int32_t>(k),
-                     kstar);
-    });
+    Pass1Ctx c{cls, L, kstar, a.o[2], ez - a.o[2], ex - a.o[0], ey - a.o[1], a.alpha_n,
+               static_cast<int32_t>(k)};
+    if (isfinite(c.vx) && isfinite(c.vy)) {
+      pass1Finite(a.g, a.o, ex, ey, c, touched, visits);
+    } else {
+      walkRay(a.g, a.o, ex, ey, [&](uint32_t cell, double te, double tn, bool vertical) {
+        ++visits;
+        const uint8_t cl = cls[cell];
+        if (cl) pass1Visit(c, cl, cell, rayHeight(a.o[2], c.dz, te, tn, vertical), touched);
+      });
+    }
   }
   // Queue rays that crossed a removal candidate for the k* pass (one atomic per warp).
   const unsigned lane = threadIdx.x & 31;
