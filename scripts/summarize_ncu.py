@@ -1,0 +1,74 @@
+"""Summarises ncu captures into profiles/ (committed evidence).
+
+    python scripts/summarize_ncu.py <full.ncu-rep> <launches.csv> <tag>
+
+Writes profiles/<tag>_kernels.md (per-kernel duration, DRAM traffic, occupancy, IPC, top stall
+reasons from the --set full capture), profiles/<tag>_launches.csv (copy of the
+gpu__time_duration launch list of the bench command) and profiles/ncu_traffic.json (DRAM bytes
+per launch per bench kernel group, read by bench.py for roofline.traffic)."""
+from __future__ import annotations
+
+import csv
+import json
+import shutil
+import subprocess
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+GROUP = {"k_ingest": "ingest", "k_fuse": "fusion", "k_rays_pass1": "rays", "k_cells": "cells",
+         "k_radix_scatter": "sort", "k_radix_hist": "sort", "k_shift": "shift"}
+
+
+def raw_rows(rep):
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    return rows[0], rows[1], rows[2:]
+
+
+def main(rep, launches, tag):
+    prof = ROOT / "profiles"
+    prof.mkdir(exist_ok=True)
+    h, units, rows = raw_rows(rep)
+    col = {n: i for i, n in enumerate(h)}
+
+    def val(r, n):
+        try:
+            return float(r[col[n]].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+
+    stall_cols = [n for n in h if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
+    lines = [f"# ncu summary ({tag})", "",
+             f"Source: `{Path(rep).name}` (`ncu --set full --clock-control none --import-source on`, one GPU). "
+             "Per-launch times here are cold-cache and serialised; compare shares, not absolutes.", "",
+             "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM GB/s | achieved occupancy % | IPC | regs | top stalls (samples) |",
+             "|---|---|---|---|---|---|---|---|---|"]
+    traffic = defaultdict(list)
+    for r in rows:
+        k = r[col["Kernel Name"]].split("(")[0].split("::")[-1]
+        dur = val(r, "gpu__time_duration.sum")
+        rd = val(r, "dram__bytes_read.sum")
+        wr = val(r, "dram__bytes_write.sum")
+        occ = val(r, "sm__warps_active.avg.pct_of_peak_sustained_active")
+        ipc = val(r, "sm__inst_executed.avg.per_cycle_active")
+        regs = val(r, "launch__registers_per_thread")
+        stalls = sorted(((val(r, n) or 0.0, n.replace("smsp__pcsamp_warps_issue_stalled_", "")) for n in stall_cols),
+                        reverse=True)[:3]
+        bw = (rd + wr) * 1e6 / (dur * 1e-6) / 1e9 if dur and rd is not None else None
+        lines.append(f"| {k} | {dur:.1f} | {rd:.2f} | {wr:.2f} | {bw:.0f} | {occ:.1f} | {ipc:.2f} | {regs:.0f} | "
+                     + ", ".join(f"{n} {v:.0f}" for v, n in stalls) + " |")
+        if k in GROUP:
+            traffic[GROUP[k]].append((rd + wr) * 1e6)
+    (prof / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
+    tj = {g: sum(v) / len(v) for g, v in traffic.items()}
+    tj["_source"] = f"profiles/{tag}_kernels.md (dram__bytes_read.sum + dram__bytes_write.sum per launch, bytes)"
+    (prof / "ncu_traffic.json").write_text(json.dumps(tj, indent=1) + "\n")
+    shutil.copy(launches, prof / f"{tag}_launches.csv")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:4])

@@ -1,0 +1,31 @@
+"""Drop-in check: the reference's own C API suite (proj/tests/test_capi.cpp, unmodified) built
+against librelief_b200.so (oracle/Makefile target capi-on-b200) and run on the GPU.
+
+Expected: every check passes except the plane-segmentation runner (relief_run_segment), which
+is outside the B200 path and returns RELIEF_ERROR_USAGE."""
+from __future__ import annotations
+
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+BIN = ROOT / "oracle" / "_ref" / "capi_tests_on_b200"
+
+
+def test_reference_capi_suite_against_b200(gpu, tmp_path):
+    if not BIN.exists():
+        pytest.skip("capi_tests_on_b200 not built (needs /root/reference at build time)")
+    proc = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=300, cwd=tmp_path)
+    failures = [l for l in proc.stderr.splitlines() if "FAILED" in l]
+    summary = proc.stdout.strip().splitlines()[-1]
+    m = re.search(r"checks: (\d+) \| failed checks: (\d+)", summary)
+    assert m, summary
+    # only the segmentation runner may fail
+    assert all("relief_run_segment" in l for l in failures), failures
+    assert len(failures) <= 1, failures
+    assert int(m.group(1)) > 11000, summary  # the layer round-trip checks ran
