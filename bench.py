@@ -224,12 +224,10 @@ def run_b200(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
 
+    from paper_2204_12876_b200 import multigpu as mg
+
     def max_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return mg.max_over_ranks(v, dist)
 
     # ---------------- value leg: inputs resident in HBM
     m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
@@ -256,7 +254,7 @@ def run_b200(args, rank, world, local_rank):
     barrier()
     clock_info = clocks.summary()
     dev_total = max_over_ranks(sum(dev_t))
-    value = world * pts_per_frame * args.steps / dev_total
+    value = mg.weak_scaling_value(pts_per_frame, args.steps, world, dev_total)
     ms_per_step = dev_total / args.steps * 1e3
 
     # Dominant kernel group + roofline
@@ -291,7 +289,7 @@ def run_b200(args, rank, world, local_rank):
         e2e_t.append(time.perf_counter() - t0)
     barrier()
     e2e_total = max_over_ranks(sum(e2e_t))
-    e2e_value = world * pts_per_frame * args.steps / e2e_total
+    e2e_value = mg.weak_scaling_value(pts_per_frame, args.steps, world, e2e_total)
 
     result = None
     if rank == 0:
