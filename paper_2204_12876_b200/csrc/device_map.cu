@@ -123,16 +123,18 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
   m->grid = grid;
   try {
     checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
+    checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     const std::size_t n = grid.cells();
-    const std::size_t bytes = 2 * layerBytes(n) + 2 * alignUp(n * 4) + alignUp((n + 1) * 4) +
-                              alignUp(n) + 4 * kAlign;
+    const std::size_t bytes = 2 * layerBytes(n) + 3 * alignUp(n * 4) + alignUp((n + 1) * 4) +
+                              alignUp(n) + 5 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
     Carver c{static_cast<char*>(m->slab)};
     carveLayers(c, m->cur, n);
     carveLayers(c, m->alt, n);
     m->count = c.take<int32_t>(n);
     m->kstar = c.take<int32_t>(n);
+    m->heavy = c.take<uint32_t>(n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
@@ -166,6 +168,7 @@ void destroyDeviceMap(DeviceMap* m) {
   for (auto& e : m->ev)
     if (e) cudaEventDestroy(e);
   if (m->stream) cudaStreamDestroy(m->stream);
+  if (m->stream2) cudaStreamDestroy(m->stream2);
   delete m;
 }
 

@@ -46,11 +46,12 @@ struct DevStats {
   unsigned long long overlap_cleared;
   unsigned long long candidate_rays;  // rays queued for the k* pass
   unsigned long long visits;          // DDA cells emitted by pass 1
+  unsigned long long heavy_cells;     // cells folded by k_fuse_heavy
   double drift_offset;                // applied offset (0 when not applied)
   int drift_n;
   int drift_clamped;
   int error_code;                     // 0 ok, 1 non-positive variance
-  int pad;
+  int respeculate;                    // a heavy cell fused nothing: redo the ray pass
 };
 
 // Geometry + parameters passed by value to kernels.
@@ -79,6 +80,7 @@ struct ChainScratch {
 struct DeviceMap {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // long-cell fold, overlapped with the ray pass
   Grid grid;
   Layers cur, alt;
   void* slab = nullptr;  // backing allocation of both layer sets + cell scratch
@@ -87,6 +89,7 @@ struct DeviceMap {
   uint32_t* start = nullptr;
   uint8_t* cls = nullptr;
   int32_t* kstar = nullptr;
+  uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold
   // per-point scratch (grown on demand)
   std::size_t cap = 0;
   void* pslab = nullptr;

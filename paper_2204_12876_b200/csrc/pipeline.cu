@@ -458,22 +458,33 @@ __device__ __forceinline__ bool gateOutlier(double d, double cv, const FuseArgs&
 
 constexpr int kFoldBatch = 8;
 
-// Gated Kalman fold (reference integration.cpp:40-55,142-203, grid.cpp:139-147):
-// one thread per cell walks that cell's points in scan order. The payload is
+// Cells with more points than this fold on the side stream (k_fuse_heavy).
+constexpr int kHeavyCell = 64;
+constexpr int kHeavyBlocks = 256;  // one warp each
+
+struct FoldCounts {
+  unsigned long long nf = 0, no = 0, ni = 0, upd = 0;
+};
+
+// Gated Kalman fold of one cell (reference integration.cpp:40-55,142-203,
+// grid.cpp:139-147): the cell's points in scan order. The payload is
 // contiguous per cell (written by the last radix pass), loaded in batches of 8
 // with the next batch in flight while the current one is folded, so the
-// dependent fp64 chain does not wait on memory.
-__global__ void __launch_bounds__(kThreads)
-    k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
-           const uint32_t* __restrict__ start, const double* __restrict__ spz,
-           const double* __restrict__ spv, FuseArgs a, DevStats* st) {
-  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-  const int cnt = i < ncell ? count[i] : 0;
-  unsigned long long nf = 0, no = 0, ni = 0, upd = 0;
-  if (cnt > 0) {
+// dependent fp64 chain does not wait on memory. Returns whether any point fused.
+__device__ __forceinline__ bool foldCell(const Layers& L, size_t i, int cnt,
+                                         const uint32_t* __restrict__ start,
+                                         const double* __restrict__ spz,
+                                         const double* __restrict__ spv, const FuseArgs& a,
+                                         DevStats* st, FoldCounts& k) {
+  unsigned long long& nf = k.nf;
+  unsigned long long& no = k.no;
+  unsigned long long& ni = k.ni;
+  unsigned long long& upd = k.upd;
+  bool fused_any = false;
+  {
     bool valid = L.valid[i] != 0;
     double h = L.elev[i], v = L.var[i];
-    bool fused_any = false, var_changed = false, bad = false;
+    bool var_changed = false, bad = false;
     const double* zp = spz + start[i];
     const double* vp = spv + start[i];
     const bool wall = cnt > a.wall;
@@ -536,16 +547,67 @@ __global__ void __launch_bounds__(kThreads)
       L.var[i] = v;
     }
   }
-  nf = warpSum(nf);
-  no = warpSum(no);
-  ni = warpSum(ni);
-  upd = warpSum(upd);
-  if ((threadIdx.x & 31) == 0 && (nf | no | ni | upd)) {
-    if (nf) atomicAdd(&st->fused, nf);
-    if (no) atomicAdd(&st->outlier, no);
-    if (ni) atomicAdd(&st->ignored_low, ni);
-    if (upd) atomicAdd(&st->cells_updated, upd);
+  return fused_any;
+}
+
+__device__ __forceinline__ void flushCounts(FoldCounts k, DevStats* st) {
+  k.nf = warpSum(k.nf);
+  k.no = warpSum(k.no);
+  k.ni = warpSum(k.ni);
+  k.upd = warpSum(k.upd);
+  if ((threadIdx.x & 31) == 0 && (k.nf | k.no | k.ni | k.upd)) {
+    if (k.nf) atomicAdd(&st->fused, k.nf);
+    if (k.no) atomicAdd(&st->outlier, k.no);
+    if (k.ni) atomicAdd(&st->ignored_low, k.ni);
+    if (k.upd) atomicAdd(&st->cells_updated, k.upd);
   }
+}
+
+// Cells with at most `heavy` points are folded here, one thread per cell;
+// longer cells are queued for k_fuse_heavy, which runs on a second stream
+// concurrently with the ray pass.
+__global__ void __launch_bounds__(kThreads)
+    k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
+           const uint32_t* __restrict__ start, const double* __restrict__ spz,
+           const double* __restrict__ spv, FuseArgs a, DevStats* st, int heavy,
+           uint32_t* heavy_list) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const int cnt = i < ncell ? count[i] : 0;
+  const bool is_heavy = cnt > heavy;
+  const unsigned hv = __ballot_sync(0xffffffffu, is_heavy);
+  if (hv) {
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == __ffs(hv) - 1)
+      base = static_cast<unsigned>(atomicAdd(&st->heavy_cells, static_cast<unsigned long long>(__popc(hv))));
+    base = __shfl_sync(0xffffffffu, base, __ffs(hv) - 1);
+    if (is_heavy) heavy_list[base + __popc(hv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+  }
+  FoldCounts k;
+  if (cnt > 0 && !is_heavy) foldCell(L, i, cnt, start, spz, spv, a, st, k);
+  flushCounts(k, st);
+}
+
+// Long cells (queued by k_fuse). The concurrent ray pass treated them as ray
+// class "none"; if a cell's post-fusion class is anything else (it fused
+// nothing and is invalid, or stale with a normal) that is flagged and the ray
+// pass is re-run after the join.
+__global__ void __launch_bounds__(32)
+    k_fuse_heavy(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
+                 const DevStats* st_in, const uint32_t* __restrict__ start,
+                 const double* __restrict__ spz, const double* __restrict__ spv, FuseArgs a,
+                 DevStats* st, double t_free, int cleanup, int bound) {
+  const unsigned total = static_cast<unsigned>(st_in->heavy_cells);
+  FoldCounts k;
+  for (unsigned q = blockIdx.x * 32 + threadIdx.x; q < total; q += gridDim.x * 32) {
+    const uint32_t i = list[q];
+    foldCell(L, i, count[i], start, spz, spv, a, st, k);
+    const bool none = L.valid[i] ? !(cleanup && !(a.now - L.last[i] <= t_free) &&
+                                     (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0))
+                                 : !bound;
+    if (!none) atomicExch(&st->respeculate, 1);
+  }
+  flushCounts(k, st);
 }
 
 // ------------------------------------------------------------- K5/K6 rays
@@ -560,12 +622,31 @@ struct RayArgs {
 
 // Post-fusion ray class per cell; also resets k* (reference raycast.cpp:
 // 132-183 gates that do not depend on the ray).
+//
+// Speculation (heavy >= 0): cells longer than `heavy` are still being folded
+// by k_fuse_heavy when this runs. A cell that fuses at least one point ends
+// valid with last_update = now, i.e. class "none" whenever t_free >= 0, so
+// those cells are classified "none" up front; k_fuse_heavy flags any heavy
+// cell that fused nothing and the ray pass is then redone (retry = 1: this
+// kernel and pass 1 run only if the flag is set).
 __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayArgs a, uint8_t* cls,
-                                                       int32_t* kstar) {
+                                                       int32_t* kstar,
+                                                       const int32_t* __restrict__ count,
+                                                       int heavy, int retry, DevStats* st) {
+  if (retry) {
+    if (!st->respeculate) return;
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // pass 1 runs again from scratch
+      st->candidate_rays = 0;
+      st->visits = 0;
+    }
+  }
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     uint8_t c = kClsNone;
-    if (!L.valid[i]) {
+    if (heavy >= 0 && count[i] > heavy) {
+      c = kClsNone;
+    } else if (!L.valid[i]) {
       c = a.bound ? kClsBound : kClsNone;
     } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
                (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
@@ -752,7 +833,7 @@ __device__ __forceinline__ double rayHeight(double oz, double dz, double te, dou
 // 167-183): CAS while ray_h < current. `seen` is a possibly stale (L1) read of
 // the bound; bounds only decrease, so a stale value is never below the true
 // one and the CAS loop settles on the true minimum.
-__device__ __noinline__ void boundMinSlow(const Layers& L, uint32_t c, double h, double seen) {
+__device__ __forceinline__ void boundMinSlow(const Layers& L, uint32_t c, double h, double seen) {
   unsigned long long* addr = reinterpret_cast<unsigned long long*>(L.ub + c);
   double cur = seen;
   while (h < cur) {
@@ -774,7 +855,7 @@ __device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) 
 
 // Removal gates for a candidate cell (reference raycast.cpp:138-150), literal
 // comparison forms; records the ray in k*.
-__device__ __noinline__ void candidateVisit(const Layers& L, uint32_t c, double h, double vx,
+__device__ __forceinline__ void candidateVisit(const Layers& L, uint32_t c, double h, double vx,
                                             double vy, double vz, double alpha_n, int32_t k,
                                             int32_t* kstar) {
   if (h >= L.elev[c] - sqrt(L.var[c])) return;
@@ -856,39 +937,34 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   }
   uint32_t idx = static_cast<uint32_t>(row) * g.W + col;
   const int step_idx_row = step_row * g.W;
-  const unsigned W = static_cast<unsigned>(g.W), H = static_cast<unsigned>(g.H);
+  // Steps left along each axis before the walk leaves the grid (the
+  // reference's bounds test after a step, raycast.cpp:121,125).
+  int xl = step_col > 0 ? g.W - 1 - col : (step_col < 0 ? col : 0);
+  int yl = step_row > 0 ? g.H - 1 - row : (step_row < 0 ? row : 0);
   const uint8_t* __restrict__ cls = c.cls;
   uint8_t cl = cls[idx];
   double t_enter = t0;
   while (true) {
+    ++visits;  // DDA steps (accounting)
     const bool sx = tmx < tmy;
     const double m = sx ? tmx : tmy;
     const bool more = m < t1;
     const double t_next = more ? m : t1;
-    const bool emit = idx != end_idx && t_next > t_enter;
-    const uint32_t cur = idx;
-    const uint8_t ccl = cl;
-    const double te = t_enter;
-    bool stop = !more;
-    if (!stop) {
-      if (sx) {
-        col += step_col;
-        tmx += tdx;
-        idx += step_col;
-        stop = static_cast<unsigned>(col) >= W;
-      } else {
-        row += step_row;
-        tmy += tdy;
-        idx += step_idx_row;
-        stop = static_cast<unsigned>(row) >= H;
-      }
-      if (!stop) cl = cls[idx];  // prefetch the next cell's class
+    if (cl != 0 && idx != end_idx && t_next > t_enter)
+      pass1Visit(c, cl, idx, c.oz + (0.5 * (t_enter + t_next)) * c.dz, touched);
+    if (!more) break;
+    if (sx) {
+      if (xl == 0) break;
+      --xl;
+      tmx += tdx;
+      idx += step_col;
+    } else {
+      if (yl == 0) break;
+      --yl;
+      tmy += tdy;
+      idx += step_idx_row;
     }
-    if (emit) {
-      ++visits;
-      if (ccl) pass1Visit(c, ccl, cur, c.oz + (0.5 * (te + t_next)) * c.dz, touched);
-    }
-    if (stop) break;
+    cl = cls[idx];
     t_enter = t_next;
   }
 }
@@ -897,7 +973,8 @@ __global__ void __launch_bounds__(kThreads, 4)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
-                 DevStats* st) {
+                 DevStats* st, int retry) {
+  if (retry && !st->respeculate) return;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   bool touched = false;
   unsigned visits = 0;
@@ -1235,13 +1312,27 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     fa.maha = U.mahalanobis_threshold;
     fa.maha2 = U.mahalanobis_threshold * U.mahalanobis_threshold;
     fa.wall = U.wall_count_threshold;
+    // Short cells here; cells with more than kHeavyCell points fold on the side
+    // stream while the ray pass runs (needs: a ray pass, and cells fused this
+    // scan being class "none", i.e. t_free >= 0 when cleanup is on).
+    const bool cleanup = P.cleanup.cleanup_enabled, bound = P.cleanup.upper_bound_enabled;
+    const bool overlap = (cleanup || bound) && (!cleanup || P.cleanup.t_free >= 0.0);
+    const int heavy = overlap ? kHeavyCell : INT_MAX;
     k_fuse<<<gridFor(ncell), kThreads, 0, s>>>(m.cur, ncell, m.count, m.start, m.spz, m.spv, fa,
-                                               m.stats);
+                                               m.stats, heavy, m.heavy);
     ++launches;
-    checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done
+    if (overlap) {
+      checkCuda(cudaEventRecord(m.ev[10], s), "event");
+      checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
+      k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.stats, m.start,
+                                                        m.spz, m.spv, fa, m.stats,
+                                                        P.cleanup.t_free, cleanup, bound);
+      ++launches;
+      checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
+    }
+    checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done (short cells when overlapped)
 
     // K5/K6 ray casting.
-    const bool cleanup = P.cleanup.cleanup_enabled, bound = P.cleanup.upper_bound_enabled;
     if (cleanup || bound) {
       RayArgs ra;
       ra.g = g;
@@ -1251,10 +1342,21 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
       ra.alpha_n = P.cleanup.alpha_n;
       ra.cleanup = cleanup;
       ra.bound = bound;
-      k_classify<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, ra, m.cls, m.kstar);
+      k_classify<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, ra, m.cls, m.kstar, m.count,
+                                                        overlap ? heavy : -1, 0, m.stats);
       k_rays_pass1<<<gridFor(n), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats);
+                                                   m.kstar, m.raylist, m.stats, 0);
       launches += 2;
+      if (overlap) {
+        // Join the long-cell fold; redo the ray pass only if a heavy cell fused
+        // nothing (both kernels return immediately otherwise).
+        checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
+        k_classify<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, ra, m.cls, m.kstar, m.count,
+                                                          -1, 1, m.stats);
+        k_rays_pass1<<<gridFor(n), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+                                                     m.kstar, m.raylist, m.stats, 1);
+        launches += 2;
+      }
       if (cleanup) {
         k_remove<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, m.kstar, m.stats);
         ++launches;
@@ -1344,3 +1446,4 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
 }
 
 }  // namespace rb200
+
