@@ -969,7 +969,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 5)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,

@@ -232,3 +232,38 @@ def test_snapshot_cross_compatible(gpu, reference, tmp_path):
     assert np.nanmax(np.abs(a - b)) <= 1e-12
     loaded = pk.ReliefMap.load(gpu, tmp_path / "r.relief")
     assert_layers_match(loaded.layers(), rm.layers(), tol_trav=0.0, context="loaded snapshot")
+
+
+def test_overlapped_fold_retry_path(gpu, reference, tmp_path):
+    """A long cell (> 64 points) that fuses nothing and stays a removal candidate: the ray pass
+    that ran concurrently with its fold treated it as class none, so the exact retry must run
+    and reproduce the reference (removal + upper bound)."""
+    import snapshots as snap
+    res, W, H = 0.1, 40, 40
+    layers = snap.fresh(H, W)
+    for r in range(H):
+        for c in range(W):
+            snap.set_cell(layers, r, c, 0.0, 0.01, 5.0, (0.0, 0.0, 1.0), 0.9)
+    snap.set_cell(layers, 20, 25, 1.0, 0.01, 0.0, (0.0, 0.0, 1.0), 0.9)  # stale tall cell at x=0.55
+    text = ("drift.enabled = false\noverlap.enabled = false\nexclusion.enabled = false\n"
+            "update.wall_count_threshold = 5\nupdate.sigma_t2 = 0\n")
+    p = tmp_path / "r.config"
+    p.write_text(text)
+    maps, cfgs = [], []
+    for i, lib in enumerate((gpu, reference)):
+        f = tmp_path / f"m{i}.relief"
+        f.write_text(snap.text(layers, res))
+        maps.append(pk.ReliefMap.load(lib, f))
+        cfgs.append(pk.Config.load(lib, p))
+    sensor = (0.05, 0.05, 0.8)
+    pose = wl.pose34(np.eye(3), sensor)
+    # 100 low points inside the tall cell (all ignored by the wall rule) ...
+    low = np.tile([0.55 - 0.05, 0.05 - 0.05, 0.2 - 0.8], (100, 1))
+    # ... and rays passing through it below its surface towards the ground beyond.
+    far = np.array([[1.45 - 0.05, 0.05 - 0.05, 0.0 - 0.8 + 0.01 * k] for k in range(8)])
+    xyz = np.concatenate([low, far])
+    got = maps[0].integrate(xyz, pose, 5.0, cfgs[0])
+    want = maps[1].integrate(xyz, pose, 5.0, cfgs[1])
+    assert_stats_match(got, want)
+    assert got.points_ignored_low == 100 and got.cells_removed_by_cleanup >= 1
+    assert_layers_match(maps[0].layers(), maps[1].layers())
