@@ -258,99 +258,17 @@ __global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, c
 }
 
 // ------------------------------------------------ K2 stable radix sort
-// LSD radix sort of 32-bit cell keys carrying the point index. Tiles of
-// 4096 keys; per pass: tile digit histograms -> exclusive scan (digit-major,
-// tile-minor) -> stable scatter, ranking inside the tile with per-warp
-// counters and __match_any_sync. Stability across passes keeps scan order
-// within each cell, which is what the gated fold needs.
-constexpr int kSortItems = 16;
+// LSD radix sort of 32-bit cell keys carrying the point index, onesweep
+// style: one kernel reads the keys once for the digit histograms of every
+// pass; each pass is then ONE kernel whose tiles (2048 keys, taken in ticket
+// order) rank their keys stably with per-warp counters and __match_any_sync,
+// publish per-digit tile counts, and obtain their global offsets by decoupled
+// look-back over the preceding tiles. Stability keeps scan order within each
+// cell, which the gated fold needs. The last pass writes the fusion payload in
+// (cell, scan order) order and each cell's segment start (atomic min).
+constexpr int kSortItems = 8;
 constexpr int kTile = kThreads * kSortItems;
-
-__global__ void __launch_bounds__(kThreads)
-    k_radix_hist(const uint32_t* __restrict__ keys, uint32_t n, int shift, int bits,
-                 uint32_t* __restrict__ hist, uint32_t ntiles) {
-  extern __shared__ uint32_t sh[];
-  const int buckets = 1 << bits;
-  const uint32_t mask = buckets - 1;
-  for (int i = threadIdx.x; i < buckets; i += kThreads) sh[i] = 0;
-  __syncthreads();
-  const uint32_t base = blockIdx.x * kTile;
-#pragma unroll 4
-  for (int j = 0; j < kSortItems; ++j) {
-    const uint32_t idx = base + j * kThreads + threadIdx.x;
-    const uint32_t d = idx < n ? (keys[idx] >> shift) & mask : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (d != 0xffffffffu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[d], __popc(peers));
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < buckets; i += kThreads) hist[static_cast<size_t>(i) * ntiles + blockIdx.x] = sh[i];
-}
-
-__global__ void __launch_bounds__(kThreads)
-    k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                    uint32_t n, int shift, int bits, const uint32_t* __restrict__ offsets,
-                    uint32_t ntiles, uint32_t* __restrict__ keys_out,
-                    uint32_t* __restrict__ vals_out, int first_pass, int last_pass,
-                    uint32_t sentinel, const double* __restrict__ pz,
-                    const double* __restrict__ pvar, double* __restrict__ spz,
-                    double* __restrict__ spv) {
-  extern __shared__ uint16_t wcnt[];  // [8 warps][buckets]
-  const int buckets = 1 << bits;
-  const uint32_t mask = buckets - 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 8 * buckets; i += kThreads) wcnt[i] = 0;
-  __syncthreads();
-  uint16_t* my = wcnt + warp * buckets;
-  const unsigned lt = (1u << lane) - 1u;
-  const uint32_t wbase = blockIdx.x * kTile + warp * (kTile / 8);
-  uint32_t key[kSortItems], val[kSortItems];
-  uint16_t rank[kSortItems];
-#pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
-    const uint32_t idx = wbase + r * 32 + lane;
-    const bool ok = idx < n;
-    key[r] = ok ? keys_in[idx] : 0xffffffffu;
-    val[r] = ok ? (first_pass ? idx : vals_in[idx]) : 0u;
-    const uint32_t d = ok ? (key[r] >> shift) & mask : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    uint16_t before = 0;
-    if (ok) before = my[d];
-    __syncwarp();
-    rank[r] = before + __popc(peers & lt);
-    if (ok && lane == __ffs(peers) - 1) my[d] = before + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  // Exclusive prefix over warps per digit.
-  for (int d = threadIdx.x; d < buckets; d += kThreads) {
-    uint16_t run = 0;
-    for (int w = 0; w < 8; ++w) {
-      const uint16_t t = wcnt[w * buckets + d];
-      wcnt[w * buckets + d] = run;
-      run += t;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
-    if (key[r] == 0xffffffffu && wbase + r * 32 + lane >= n) continue;
-    const uint32_t d = (key[r] >> shift) & mask;
-    const uint32_t pos = offsets[static_cast<size_t>(d) * ntiles + blockIdx.x] + my[d] + rank[r];
-    if (!last_pass) {
-      keys_out[pos] = key[r];
-      vals_out[pos] = val[r];
-    } else if (key[r] < sentinel) {
-      // Final pass: emit the fusion payload in (cell, scan order) order.
-      spz[pos] = pz[val[r]];
-      spv[pos] = pvar[val[r]];
-    }
-  }
-}
-
-// Exclusive scan of u32 (three kernels: tile sums, scan of tile sums, tile
-// rescans). Used for radix offsets and for cell segment starts.
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kThreads * kScanItems;
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValueMask = (1u << 30) - 1;
 
 __device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* total) {
   __shared__ uint32_t s_warp[kThreads / 32];
@@ -373,66 +291,147 @@ __device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* tot
   return wpre + incl - v;
 }
 
-__global__ void __launch_bounds__(kThreads) k_scan_reduce(const uint32_t* __restrict__ in, size_t n,
-                                                          uint32_t* __restrict__ part) {
-  const size_t base = blockIdx.x * static_cast<size_t>(kScanTile);
-  uint32_t s = 0;
-  for (int j = 0; j < kScanItems; ++j) {
-    const size_t idx = base + j * kThreads + threadIdx.x;
-    if (idx < n) s += in[idx];
-  }
-  s = warpSum(s);
-  __shared__ uint32_t sw[kThreads / 32];
-  if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+// Digit histograms of all passes (ghist[p * buckets + d]).
+__global__ void __launch_bounds__(kThreads)
+    k_sort_hist(const uint32_t* __restrict__ keys, uint32_t n, int dbits, int passes,
+                uint32_t* __restrict__ ghist) {
+  extern __shared__ uint32_t sh[];
+  const int buckets = 1 << dbits;
+  const uint32_t mask = buckets - 1;
+  for (int i = threadIdx.x; i < passes * buckets; i += kThreads) sh[i] = 0;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < kThreads / 32; ++w) t += sw[w];
-    part[blockIdx.x] = t;
+  const uint32_t stride = gridDim.x * kThreads;
+  const uint32_t end = (n + stride - 1) / stride * stride;  // whole warps iterate together
+  for (uint32_t idx = blockIdx.x * kThreads + threadIdx.x; idx < end; idx += stride) {
+    const bool ok = idx < n;
+    const uint32_t key = ok ? keys[idx] : 0u;
+    for (int p = 0; p < passes; ++p) {
+      const uint32_t d = ok ? (key >> (p * dbits)) & mask : 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[p * buckets + d], __popc(peers));
+    }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * buckets; i += kThreads)
+    if (sh[i]) atomicAdd(&ghist[i], sh[i]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_scan_top(uint32_t* part, int nparts) {
-  uint32_t carry = 0;
-  for (int base = 0; base < nparts; base += kThreads) {
-    const int i = base + threadIdx.x;
-    const uint32_t v = i < nparts ? part[i] : 0;
-    uint32_t total;
-    const uint32_t ex = blockExclusiveScan(v, &total);
-    if (i < nparts) part[i] = carry + ex;
-    carry += total;
-  }
+__device__ __forceinline__ uint32_t loadStatus(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+__device__ __forceinline__ void storeStatus(uint32_t* p, uint32_t v) {
+  *reinterpret_cast<volatile uint32_t*>(p) = v;
 }
 
 __global__ void __launch_bounds__(kThreads)
-    k_scan_down(const uint32_t* __restrict__ in, size_t n, const uint32_t* __restrict__ part,
-                uint32_t* __restrict__ out, uint32_t* __restrict__ total_out) {
-  __shared__ uint32_t tile[kScanTile];
-  const size_t base = blockIdx.x * static_cast<size_t>(kScanTile);
-  for (int j = 0; j < kScanItems; ++j) {
-    const size_t idx = base + j * kThreads + threadIdx.x;
-    tile[j * kThreads + threadIdx.x] = idx < n ? in[idx] : 0u;
+    k_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+               uint32_t n, int shift, int dbits, const uint32_t* __restrict__ ghist,
+               uint32_t* status, uint32_t* ticket, uint32_t* __restrict__ keys_out,
+               uint32_t* __restrict__ vals_out, int first_pass, int last_pass, uint32_t sentinel,
+               const double* __restrict__ pz, const double* __restrict__ pvar,
+               double* __restrict__ spz, double* __restrict__ spv, uint32_t* start) {
+  extern __shared__ unsigned char smem[];
+  const int buckets = 1 << dbits;
+  const uint32_t mask = buckets - 1;
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem);                      // [8][buckets]
+  uint32_t* offs = reinterpret_cast<uint32_t*>(smem + 16 * buckets);        // [buckets]
+  __shared__ uint32_t s_tile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  for (int i = threadIdx.x; i < 8 * buckets; i += kThreads) wcnt[i] = 0;
+  // Global exclusive prefix of this pass's digit counts (block-local scan).
+  {
+    const int per = (buckets + kThreads - 1) / kThreads;
+    uint32_t loc = 0;
+    for (int j = 0; j < per; ++j) {
+      const int d = threadIdx.x * per + j;
+      if (d < buckets) loc += ghist[d];
+    }
+    uint32_t total;
+    uint32_t run = blockExclusiveScan(loc, &total);
+    for (int j = 0; j < per; ++j) {
+      const int d = threadIdx.x * per + j;
+      if (d < buckets) {
+        offs[d] = run;
+        run += ghist[d];
+      }
+    }
   }
   __syncthreads();
-  uint32_t loc[kScanItems];
-  uint32_t s = 0;
+  const uint32_t tile = s_tile;
+  uint16_t* my = wcnt + warp * buckets;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t wbase = tile * kTile + warp * (kTile / 8);
+  uint32_t key[kSortItems], val[kSortItems];
+  uint16_t rank[kSortItems];
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    loc[j] = s;
-    s += tile[threadIdx.x * kScanItems + j];
+  for (int r = 0; r < kSortItems; ++r) {
+    const uint32_t idx = wbase + r * 32 + lane;
+    const bool ok = idx < n;
+    key[r] = ok ? keys_in[idx] : 0xffffffffu;
+    val[r] = ok ? (first_pass ? idx : vals_in[idx]) : 0u;
+    const uint32_t d = ok ? (key[r] >> shift) & mask : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    uint16_t before = 0;
+    if (ok) before = my[d];
+    __syncwarp();
+    rank[r] = before + __popc(peers & lt);
+    if (ok && lane == __ffs(peers) - 1) my[d] = before + __popc(peers);
+    __syncwarp();
   }
-  uint32_t block_total;
-  const uint32_t ex = blockExclusiveScan(s, &block_total) + part[blockIdx.x];
+  __syncthreads();
+  // Per digit: prefix over warps, publish the tile count, look back for the
+  // tile's exclusive offset, publish the inclusive prefix.
+  uint32_t* my_status = status + static_cast<size_t>(tile) * buckets;
+  for (int d = threadIdx.x; d < buckets; d += kThreads) {
+    uint16_t run = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint16_t t = wcnt[w * buckets + d];
+      wcnt[w * buckets + d] = run;
+      run += t;
+    }
+    storeStatus(my_status + d, (tile == 0 ? kFlagPrefix : kFlagAgg) | run);
+  }
+  __threadfence();
+  for (int d = threadIdx.x; d < buckets; d += kThreads) {
+    const uint32_t cnt = loadStatus(my_status + d) & kValueMask;
+    uint32_t excl = 0;
+    if (tile > 0) {
+      for (int t = static_cast<int>(tile) - 1; t >= 0; --t) {
+        uint32_t sv;
+        do {
+          sv = loadStatus(status + static_cast<size_t>(t) * buckets + d);
+        } while ((sv & ~kValueMask) == 0);
+        excl += sv & kValueMask;
+        if ((sv & ~kValueMask) == kFlagPrefix) break;
+      }
+      storeStatus(my_status + d, kFlagPrefix | (excl + cnt));
+    }
+    offs[d] += excl;  // global digit prefix + this tile's offset within the digit
+  }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) tile[threadIdx.x * kScanItems + j] = ex + loc[j];
-  __syncthreads();
-  for (int j = 0; j < kScanItems; ++j) {
-    const size_t idx = base + j * kThreads + threadIdx.x;
-    if (idx < n) out[idx] = tile[j * kThreads + threadIdx.x];
+  for (int r = 0; r < kSortItems; ++r) {
+    const bool ok = wbase + r * 32 + lane < n;
+    const uint32_t d = (key[r] >> shift) & mask;
+    const uint32_t pos = ok ? offs[d] + my[d] + rank[r] : 0u;
+    if (!last_pass) {
+      if (ok) {
+        keys_out[pos] = key[r];
+        vals_out[pos] = val[r];
+      }
+    } else {
+      const bool cell = ok && key[r] < sentinel;
+      if (cell) {
+        // Final pass: the fusion payload in (cell, scan order) order.
+        spz[pos] = pz[val[r]];
+        spv[pos] = pvar[val[r]];
+      }
+      // Segment start = smallest position of the cell (lowest lane of a run).
+      const unsigned peers = __match_any_sync(0xffffffffu, cell ? key[r] : 0xffffffffu);
+      if (cell && lane == __ffs(peers) - 1) atomicMin(start + key[r], pos);
+    }
   }
-  if (total_out != nullptr && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
-    *total_out = part[blockIdx.x] + block_total;
 }
 
 // ------------------------------------------------------------- K3 fusion
@@ -1268,39 +1267,35 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     const int passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
     const int dbits = (bits + passes - 1) / passes;
     const uint32_t ntiles = (N + kTile - 1) / kTile;
-    const std::size_t hist_n = static_cast<std::size_t>(1u << dbits) * ntiles;
-    const std::size_t need = hist_n + (hist_n / kScanTile + 2) + 2 * (ncell / kScanTile + 2) + 64;
+    const uint32_t buckets = 1u << dbits;
+    // scratch: [passes * buckets] histograms, [passes] tickets, [passes * ntiles * buckets] status
+    const std::size_t need = passes * (buckets + 1 + static_cast<std::size_t>(ntiles) * buckets) + 64;
     if (m.hist_cap < need) {
       cudaFree(m.hist);
       m.hist_cap = need;
       checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
     }
-    uint32_t* hist = m.hist;
-    uint32_t* part = m.hist + hist_n;
+    uint32_t* ghist = m.hist;
+    uint32_t* tickets = ghist + passes * buckets;
+    uint32_t* status = tickets + passes;
+    checkCuda(cudaMemsetAsync(m.hist, 0, need * sizeof(uint32_t), s), "memset");
+    checkCuda(cudaMemsetAsync(m.start, 0xff, ncell * sizeof(uint32_t), s), "memset");
+    k_sort_hist<<<148 * 4, kThreads, passes * buckets * sizeof(uint32_t), s>>>(m.key0, N, dbits,
+                                                                              passes, ghist);
+    ++launches;
+    const std::size_t os_smem = 20 * static_cast<std::size_t>(buckets);
     uint32_t *kin = m.key0, *kout = m.key1, *vin = m.val0, *vout = m.val1;
-    const auto scan = [&](const uint32_t* in, std::size_t len, uint32_t* out, uint32_t* total) {
-      const unsigned nb = static_cast<unsigned>((len + kScanTile - 1) / kScanTile);
-      k_scan_reduce<<<nb, kThreads, 0, s>>>(in, len, part);
-      k_scan_top<<<1, kThreads, 0, s>>>(part, static_cast<int>(nb));
-      k_scan_down<<<nb, kThreads, 0, s>>>(in, len, part, out, total);
-      launches += 3;
-    };
     for (int p = 0; p < passes; ++p) {
-      const int shift = p * dbits;
-      const bool last = p == passes - 1;
-      k_radix_hist<<<ntiles, kThreads, (1u << dbits) * sizeof(uint32_t), s>>>(kin, N, shift, dbits,
-                                                                              hist, ntiles);
-      ++launches;
-      scan(hist, hist_n, hist, nullptr);
-      k_radix_scatter<<<ntiles, kThreads, 8 * (1u << dbits) * sizeof(uint16_t), s>>>(
-          kin, vin, N, shift, dbits, hist, ntiles, kout, vout, p == 0, last ? 1 : 0, WH, m.pz,
-          m.pvar, m.spz, m.spv);
+      k_onesweep<<<ntiles, kThreads, os_smem, s>>>(
+          kin, vin, N, p * dbits, dbits, ghist + p * buckets,
+          status + static_cast<std::size_t>(p) * ntiles * buckets, tickets + p, kout, vout, p == 0,
+          p == passes - 1, WH, m.pz, m.pvar, m.spz, m.spv, m.start);
       ++launches;
       std::swap(kin, kout);
       std::swap(vin, vout);
     }
-    // spz / spv now hold (p_z, sigma_p^2) sorted by (cell, scan order).
-    scan(reinterpret_cast<const uint32_t*>(m.count), ncell, m.start, m.start + ncell);
+    // spz / spv now hold (p_z, sigma_p^2) sorted by (cell, scan order); start[c]
+    // is the first sorted position of cell c (cells with points).
     checkCuda(cudaEventRecord(m.ev[4], s), "event");  // sort done
 
     // K3 gated fusion.
