@@ -139,6 +139,9 @@ def load_library(path: Optional[os.PathLike] = None, gpu_api: Optional[bool] = N
     ``gpu_api`` binds relief_gpu.h too; it defaults to True for the product library.
     Raises FileNotFoundError when the library is missing -- there is no fallback.
     """
+    if path is None and os.environ.get("RELIEF_B200_LIB"):
+        path = os.environ["RELIEF_B200_LIB"]  # development override (A/B builds)
+        gpu_api = True if gpu_api is None else gpu_api
     p = Path(path) if path is not None else DEFAULT_LIB
     if not p.exists():
         raise FileNotFoundError(
