@@ -46,6 +46,19 @@ __device__ __forceinline__ T warpSum(T v) {
   return v;
 }
 
+// Radix-sort tile geometry (K2): kTile consecutive keys per tile.
+constexpr int kSortItems = 8;
+constexpr int kTile = kThreads * kSortItems;
+
+// Tile digit count tc[d * pitch + tile] += 1 for every lane with ok, one
+// atomic per (digit, tile) run in the warp; every lane must call.
+__device__ __forceinline__ void countTileDigit(uint32_t* tc, uint32_t pitch, uint32_t d,
+                                               uint32_t tile, bool ok) {
+  const uint32_t slot = ok ? d * pitch + tile : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, slot);
+  if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&tc[slot], __popc(peers));
+}
+
 // Invalidate one cell (reference grid.cpp:126-137).
 __device__ __forceinline__ void invalidateCell(const Layers& L, size_t i) {
   L.valid[i] = 0;
@@ -119,7 +132,8 @@ __global__ void __launch_bounds__(kThreads)
              int32_t* __restrict__ count, double* __restrict__ px, double* __restrict__ py,
              double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
              uint8_t* __restrict__ kept, double* __restrict__ drift_part,
-             int* __restrict__ drift_npart, DevStats* st) {
+             int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
+             uint32_t dmask, DevStats* st) {
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   int oor = 0, exc = 0, oom = 0, dn = 0;
@@ -167,6 +181,8 @@ __global__ void __launch_bounds__(kThreads)
   // Per-cell point count, one atomic per run of equal cells in the warp.
   const unsigned peers = __match_any_sync(0xffffffffu, cell);
   if (cell < WH && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
+  // First radix pass's tile digit counts (K2).
+  countTileDigit(tc0, pitch, cell & dmask, k / kTile, cell < WH);
 
   // Fixed-shape block reduction: deterministic drift partial per block.
   __shared__ double s_sum[kThreads / 32];
@@ -258,17 +274,31 @@ __global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, c
 }
 
 // ------------------------------------------------ K2 stable radix sort
-// LSD radix sort of 32-bit cell keys carrying the point index, onesweep
-// style: one kernel reads the keys once for the digit histograms of every
-// pass; each pass is then ONE kernel whose tiles (2048 keys, taken in ticket
-// order) rank their keys stably with per-warp counters and __match_any_sync,
-// publish per-digit tile counts, and obtain their global offsets by decoupled
-// look-back over the preceding tiles. Stability keeps scan order within each
-// cell, which the gated fold needs. The last pass writes the fusion payload in
-// (cell, scan order) order and each cell's segment start (atomic min).
-constexpr int kSortItems = 8;
-constexpr int kTile = kThreads * kSortItems;
-constexpr uint32_t kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValueMask = (1u << 30) - 1;
+// LSD radix sort of the in-map kept points by cell, carrying the point index,
+// reduce-then-scan style so that no tile waits on another:
+//  * tile counts tc[p][d][t] = keys of tile t (kTile consecutive keys of pass
+//    p's input) with digit d. Pass 0's are built by k_ingest, pass p+1's by
+//    pass p's scatter (it knows where every key lands); warp-aggregated
+//    atomics in both.
+//  * k_sort_rowscan: one block per digit turns its row into exclusive tile
+//    offsets and writes the row total (the digit's global count).
+//  * k_sort_scatter: one block per tile ranks its keys stably (per-warp
+//    counters + __match_any_sync), adds the digit base (block scan of the row
+//    totals) and its row offset, and scatters.
+// Stability keeps scan order within each cell, which the gated fold needs. The
+// last pass writes the fusion payload in (cell, scan order) order and each
+// cell's segment start (atomic min).
+struct SortGeom {
+  int passes = 0, dbits = 0;
+  uint32_t ntiles = 0;  // tiles of the N input keys (bounds every pass)
+  uint32_t pitch = 0;   // row pitch of tc (ntiles rounded up to 4)
+  uint32_t* tc = nullptr;      // [passes][buckets][pitch]
+  uint32_t* rowsum = nullptr;  // [passes][buckets]
+  __host__ __device__ uint32_t buckets() const { return 1u << dbits; }
+  __host__ __device__ uint32_t* counts(int p) const {
+    return tc + static_cast<size_t>(p) * buckets() * pitch;
+  }
+};
 
 __device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* total) {
   __shared__ uint32_t s_warp[kThreads / 32];
@@ -291,74 +321,69 @@ __device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* tot
   return wpre + incl - v;
 }
 
-// Digit histograms of all passes (ghist[p * buckets + d]).
+// Row d of tc -> exclusive offsets within the digit; rowsum[d] = row total.
 __global__ void __launch_bounds__(kThreads)
-    k_sort_hist(const uint32_t* __restrict__ keys, uint32_t n, int dbits, int passes,
-                uint32_t* __restrict__ ghist) {
-  extern __shared__ uint32_t sh[];
-  const int buckets = 1 << dbits;
-  const uint32_t mask = buckets - 1;
-  for (int i = threadIdx.x; i < passes * buckets; i += kThreads) sh[i] = 0;
-  __syncthreads();
-  const uint32_t stride = gridDim.x * kThreads;
-  const uint32_t end = (n + stride - 1) / stride * stride;  // whole warps iterate together
-  for (uint32_t idx = blockIdx.x * kThreads + threadIdx.x; idx < end; idx += stride) {
-    const bool ok = idx < n;
-    const uint32_t key = ok ? keys[idx] : 0u;
-    for (int p = 0; p < passes; ++p) {
-      const uint32_t d = ok ? (key >> (p * dbits)) & mask : 0xffffffffu;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[p * buckets + d], __popc(peers));
+    k_sort_rowscan(uint32_t* __restrict__ tc, uint32_t pitch, uint32_t* __restrict__ rowsum) {
+  uint4* row = reinterpret_cast<uint4*>(tc + static_cast<size_t>(blockIdx.x) * pitch);
+  const uint32_t nq = pitch / 4;
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < nq; b += kThreads) {
+    const uint32_t q = b + threadIdx.x;
+    uint4 v = q < nq ? row[q] : make_uint4(0, 0, 0, 0);
+    uint32_t total;
+    const uint32_t run = carry + blockExclusiveScan(v.x + v.y + v.z + v.w, &total);
+    if (q < nq) {
+      uint4 o;
+      o.x = run;
+      o.y = o.x + v.x;
+      o.z = o.y + v.y;
+      o.w = o.z + v.z;
+      row[q] = o;
     }
+    carry += total;
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < passes * buckets; i += kThreads)
-    if (sh[i]) atomicAdd(&ghist[i], sh[i]);
-}
-
-__device__ __forceinline__ uint32_t loadStatus(const uint32_t* p) {
-  return *reinterpret_cast<const volatile uint32_t*>(p);
-}
-__device__ __forceinline__ void storeStatus(uint32_t* p, uint32_t v) {
-  *reinterpret_cast<volatile uint32_t*>(p) = v;
+  if (threadIdx.x == 0) rowsum[blockIdx.x] = carry;
 }
 
 __global__ void __launch_bounds__(kThreads)
-    k_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-               uint32_t n, int shift, int dbits, const uint32_t* __restrict__ ghist,
-               uint32_t* status, uint32_t* ticket, uint32_t* __restrict__ keys_out,
-               uint32_t* __restrict__ vals_out, int first_pass, int last_pass, uint32_t sentinel,
-               const double* __restrict__ pz, const double* __restrict__ pvar,
-               double* __restrict__ spz, double* __restrict__ spv, uint32_t* start) {
+    k_sort_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                   uint32_t n_in, int pass, SortGeom sg, uint32_t sentinel,
+                   uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                   const double* __restrict__ pz, const double* __restrict__ pvar,
+                   double* __restrict__ spz, double* __restrict__ spv, uint32_t* start) {
   extern __shared__ unsigned char smem[];
+  const int dbits = sg.dbits, shift = pass * dbits;
   const int buckets = 1 << dbits;
   const uint32_t mask = buckets - 1;
-  uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem);                      // [8][buckets]
-  uint32_t* offs = reinterpret_cast<uint32_t*>(smem + 16 * buckets);        // [buckets]
-  __shared__ uint32_t s_tile;
+  const bool last = pass == sg.passes - 1;
+  const uint32_t* __restrict__ tc = sg.counts(pass);
+  const uint32_t* __restrict__ rowsum = sg.rowsum + static_cast<size_t>(pass) * buckets;
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem);                // [8][buckets]
+  uint32_t* offs = reinterpret_cast<uint32_t*>(smem + 16 * buckets);  // [buckets]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  const uint32_t tile = blockIdx.x;
   for (int i = threadIdx.x; i < 8 * buckets; i += kThreads) wcnt[i] = 0;
-  // Global exclusive prefix of this pass's digit counts (block-local scan).
+  // Digit bases: exclusive scan of the row totals; their sum is the number of
+  // keys being sorted (pass 0 reads N keys and skips the sentinel ones).
+  uint32_t nkeys;
   {
     const int per = (buckets + kThreads - 1) / kThreads;
     uint32_t loc = 0;
     for (int j = 0; j < per; ++j) {
       const int d = threadIdx.x * per + j;
-      if (d < buckets) loc += ghist[d];
+      if (d < buckets) loc += rowsum[d];
     }
-    uint32_t total;
-    uint32_t run = blockExclusiveScan(loc, &total);
+    uint32_t run = blockExclusiveScan(loc, &nkeys);
     for (int j = 0; j < per; ++j) {
       const int d = threadIdx.x * per + j;
       if (d < buckets) {
-        offs[d] = run;
-        run += ghist[d];
+        offs[d] = run + tc[static_cast<size_t>(d) * sg.pitch + tile];
+        run += rowsum[d];
       }
     }
   }
+  const uint32_t n = pass == 0 ? n_in : nkeys;
   __syncthreads();
-  const uint32_t tile = s_tile;
   uint16_t* my = wcnt + warp * buckets;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t wbase = tile * kTile + warp * (kTile / 8);
@@ -367,9 +392,9 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
     const uint32_t idx = wbase + r * 32 + lane;
-    const bool ok = idx < n;
-    key[r] = ok ? keys_in[idx] : 0xffffffffu;
-    val[r] = ok ? (first_pass ? idx : vals_in[idx]) : 0u;
+    key[r] = idx < n ? keys_in[idx] : sentinel;
+    const bool ok = key[r] < sentinel;
+    val[r] = ok ? (pass == 0 ? idx : vals_in[idx]) : 0u;
     const uint32_t d = ok ? (key[r] >> shift) & mask : 0xffffffffu;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     uint16_t before = 0;
@@ -380,9 +405,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncwarp();
   }
   __syncthreads();
-  // Per digit: prefix over warps, publish the tile count, look back for the
-  // tile's exclusive offset, publish the inclusive prefix.
-  uint32_t* my_status = status + static_cast<size_t>(tile) * buckets;
+  // Per digit: exclusive prefix over the warps of this tile.
   for (int d = threadIdx.x; d < buckets; d += kThreads) {
     uint16_t run = 0;
     for (int w = 0; w < 8; ++w) {
@@ -390,46 +413,29 @@ __global__ void __launch_bounds__(kThreads)
       wcnt[w * buckets + d] = run;
       run += t;
     }
-    storeStatus(my_status + d, (tile == 0 ? kFlagPrefix : kFlagAgg) | run);
-  }
-  __threadfence();
-  for (int d = threadIdx.x; d < buckets; d += kThreads) {
-    const uint32_t cnt = loadStatus(my_status + d) & kValueMask;
-    uint32_t excl = 0;
-    if (tile > 0) {
-      for (int t = static_cast<int>(tile) - 1; t >= 0; --t) {
-        uint32_t sv;
-        do {
-          sv = loadStatus(status + static_cast<size_t>(t) * buckets + d);
-        } while ((sv & ~kValueMask) == 0);
-        excl += sv & kValueMask;
-        if ((sv & ~kValueMask) == kFlagPrefix) break;
-      }
-      storeStatus(my_status + d, kFlagPrefix | (excl + cnt));
-    }
-    offs[d] += excl;  // global digit prefix + this tile's offset within the digit
   }
   __syncthreads();
+  uint32_t* tc_next = last ? nullptr : sg.counts(pass + 1);
 #pragma unroll
   for (int r = 0; r < kSortItems; ++r) {
-    const bool ok = wbase + r * 32 + lane < n;
+    const bool ok = key[r] < sentinel;
     const uint32_t d = (key[r] >> shift) & mask;
     const uint32_t pos = ok ? offs[d] + my[d] + rank[r] : 0u;
-    if (!last_pass) {
+    if (!last) {
       if (ok) {
         keys_out[pos] = key[r];
         vals_out[pos] = val[r];
       }
+      countTileDigit(tc_next, sg.pitch, (key[r] >> (shift + dbits)) & mask, pos / kTile, ok);
     } else {
-      const bool cell = ok && key[r] < sentinel;
-      if (cell) {
+      if (ok) {
         // Final pass: the fusion payload in (cell, scan order) order.
         spz[pos] = pz[val[r]];
         spv[pos] = pvar[val[r]];
       }
       // Segment start = smallest position of the cell (lowest lane of a run).
-      const unsigned peers = __match_any_sync(0xffffffffu, cell ? key[r] : 0xffffffffu);
-      if (cell && lane == __ffs(peers) - 1) atomicMin(start + key[r], pos);
+      const unsigned peers = __match_any_sync(0xffffffffu, ok ? key[r] : 0xffffffffu);
+      if (ok && lane == __ffs(peers) - 1) atomicMin(start + key[r], pos);
     }
   }
 }
@@ -968,7 +974,10 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 5)
+#ifndef RB_PASS1_MIN_BLOCKS
+#define RB_PASS1_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
@@ -1222,6 +1231,28 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     }
   }
   checkCuda(cudaMemsetAsync(m.count, 0, ncell * sizeof(int32_t), s), "memset");
+  // K2 geometry: 1-3 LSD passes over the bits of the cell id; tile digit
+  // counts are accumulated from K1 on, so they are zeroed here.
+  const uint32_t WH = static_cast<uint32_t>(ncell);
+  SortGeom sg;
+  if (n > 0) {
+    const int bits = 32 - __builtin_clz(WH);
+    sg.passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
+    sg.dbits = (bits + sg.passes - 1) / sg.passes;
+    sg.ntiles = (N + kTile - 1) / kTile;
+    sg.pitch = (sg.ntiles + 3) & ~3u;
+    const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
+    const std::size_t need = tcn + static_cast<std::size_t>(sg.passes) * sg.buckets();
+    if (m.hist_cap < need) {
+      cudaFree(m.hist);
+      m.hist = nullptr;
+      m.hist_cap = need;
+      checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
+    }
+    sg.tc = m.hist;
+    sg.rowsum = m.hist + tcn;
+    checkCuda(cudaMemsetAsync(sg.tc, 0, tcn * sizeof(uint32_t), s), "memset");
+  }
   checkCuda(cudaEventRecord(m.ev[1], s), "event");  // upload done
 
   // K1 ingest.
@@ -1245,7 +1276,8 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     ia.drift_thr = P.drift.traversability_threshold;
     k_ingest<<<gridFor(n), kThreads, 0, s>>>(d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz,
                                              m.pvar, m.key0, m.kept, m.drift_sum_part,
-                                             m.drift_n_part, m.stats);
+                                             m.drift_n_part, sg.tc, sg.pitch,
+                                             sg.buckets() - 1, m.stats);
     ++launches;
   }
   checkCuda(cudaEventRecord(m.ev[2], s), "event");  // ingest done
@@ -1262,35 +1294,15 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
 
   if (n > 0) {
     // K2: stable sort of point indices by cell, then segment starts.
-    const uint32_t WH = static_cast<uint32_t>(ncell);
-    int bits = 32 - __builtin_clz(WH);
-    const int passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
-    const int dbits = (bits + passes - 1) / passes;
-    const uint32_t ntiles = (N + kTile - 1) / kTile;
-    const uint32_t buckets = 1u << dbits;
-    // scratch: [passes * buckets] histograms, [passes] tickets, [passes * ntiles * buckets] status
-    const std::size_t need = passes * (buckets + 1 + static_cast<std::size_t>(ntiles) * buckets) + 64;
-    if (m.hist_cap < need) {
-      cudaFree(m.hist);
-      m.hist_cap = need;
-      checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
-    }
-    uint32_t* ghist = m.hist;
-    uint32_t* tickets = ghist + passes * buckets;
-    uint32_t* status = tickets + passes;
-    checkCuda(cudaMemsetAsync(m.hist, 0, need * sizeof(uint32_t), s), "memset");
     checkCuda(cudaMemsetAsync(m.start, 0xff, ncell * sizeof(uint32_t), s), "memset");
-    k_sort_hist<<<148 * 4, kThreads, passes * buckets * sizeof(uint32_t), s>>>(m.key0, N, dbits,
-                                                                              passes, ghist);
-    ++launches;
-    const std::size_t os_smem = 20 * static_cast<std::size_t>(buckets);
+    const std::size_t sc_smem = 20 * static_cast<std::size_t>(sg.buckets());
     uint32_t *kin = m.key0, *kout = m.key1, *vin = m.val0, *vout = m.val1;
-    for (int p = 0; p < passes; ++p) {
-      k_onesweep<<<ntiles, kThreads, os_smem, s>>>(
-          kin, vin, N, p * dbits, dbits, ghist + p * buckets,
-          status + static_cast<std::size_t>(p) * ntiles * buckets, tickets + p, kout, vout, p == 0,
-          p == passes - 1, WH, m.pz, m.pvar, m.spz, m.spv, m.start);
-      ++launches;
+    for (int p = 0; p < sg.passes; ++p) {
+      k_sort_rowscan<<<sg.buckets(), kThreads, 0, s>>>(sg.counts(p), sg.pitch,
+                                                       sg.rowsum + p * sg.buckets());
+      k_sort_scatter<<<sg.ntiles, kThreads, sc_smem, s>>>(kin, vin, N, p, sg, WH, kout, vout,
+                                                          m.pz, m.pvar, m.spz, m.spv, m.start);
+      launches += 2;
       std::swap(kin, kout);
       std::swap(vin, vout);
     }

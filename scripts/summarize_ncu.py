@@ -17,8 +17,11 @@ from collections import defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-GROUP = {"k_ingest": "ingest", "k_fuse": "fusion", "k_rays_pass1": "rays", "k_cells": "cells",
-         "k_radix_scatter": "sort", "k_radix_hist": "sort", "k_shift": "shift"}
+# kernel -> bench.py kernel group (the event-timed phases of integrateScanDevice)
+GROUP = {"k_ingest": "ingest", "k_drift_finalize": "drift", "k_apply_offset": "drift",
+         "k_sort_hist": "sort", "k_onesweep": "sort", "k_fuse": "fusion", "k_fuse_heavy": "rays",
+         "k_classify": "rays", "k_rays_pass1": "rays", "k_remove": "rays", "k_rays_pass2": "rays",
+         "k_cells": "cells", "k_shift": "shift"}
 
 
 def raw_rows(rep):
@@ -63,8 +66,11 @@ def main(rep, launches, tag):
         if k in GROUP:
             traffic[GROUP[k]].append((rd + wr) * 1e6)
     (prof / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
-    tj = {g: sum(v) / len(v) for g, v in traffic.items()}
-    tj["_source"] = f"profiles/{tag}_kernels.md (dram__bytes_read.sum + dram__bytes_write.sum per launch, bytes)"
+    # per frame: every captured frame launches k_ingest exactly once
+    frames = max(1, len(traffic.get("ingest", [])))
+    tj = {g: sum(v) / frames for g, v in traffic.items()}
+    tj["_source"] = (f"profiles/{tag}_kernels.md (dram__bytes_read.sum + dram__bytes_write.sum summed over "
+                     f"the group's launches, per frame; {frames} frame(s) captured)")
     (prof / "ncu_traffic.json").write_text(json.dumps(tj, indent=1) + "\n")
     shutil.copy(launches, prof / f"{tag}_launches.csv")
     print("\n".join(lines))
