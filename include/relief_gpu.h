@@ -91,6 +91,21 @@ RELIEF_API relief_status relief_gpu_smooth_chain(const double* values, const uin
                                                  int n_steps, double* values_out,
                                                  uint8_t* valid_out);
 
+/* Conv-net traversability (reference analysis.cpp:138-290). Loads the weight
+ * file into the config and switches the pipeline to the learned filter, so
+ * relief_map_integrate runs it (the reference reaches it only through its
+ * runners, runner.cpp:53-60: its relief_config_load records the path but never
+ * loads the layers). Errors: RELIEF_ERROR_IO (cannot open), ..._INVALID_MODEL. */
+RELIEF_API relief_status relief_gpu_config_load_convnet(relief_config* config,
+                                                        const char* model_path);
+
+/* convFilterInference on caller-supplied host data with the config's model:
+ * nearest-valid fill of `layer` by `valid`, the layer stack, clamp to [0,1];
+ * writes width*height values. */
+RELIEF_API relief_status relief_gpu_convnet_infer(const relief_config* config, const double* layer,
+                                                  const uint8_t* valid, int width, int height,
+                                                  double* out);
+
 /* Synthetic scan: scene + sensor of a reliefmap config file, rendered from
  * pose (row-major [R|t]) at `time` with splitmix64 stream (seed, scan_index)
  * per ray. Returns the point count (only min(count, capacity) points are

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "relief/core/analysis.hpp"
 #include "relief/core/config.hpp"
 #include "relief/core/integration.hpp"
 #include "relief/core/postprocess.hpp"
@@ -141,3 +142,26 @@ REF_API int ref_smooth_chain(const double* values, const uint8_t* valid, int wid
     return -1;
   }
 }
+
+// loadConvNetSpecFile + convFilterInference (analysis.cpp:138-290). Returns 0,
+// or the reference ErrorCode + 1 as a negative number (-1 for anything that
+// is not a relief::Error) with ref_last_error() set.
+REF_API int ref_convnet_infer(const char* model_path, const double* layer, const uint8_t* valid,
+                              int width, int height, double* out) {
+  try {
+    const relief::ConvNetSpec spec = relief::loadConvNetSpecFile(model_path);
+    const std::size_t n = static_cast<std::size_t>(width) * height;
+    const std::vector<double> in(layer, layer + n);
+    const std::vector<std::uint8_t> ok(valid, valid + n);
+    const std::vector<double> res = relief::convFilterInference(in, ok, width, height, spec);
+    std::memcpy(out, res.data(), n * sizeof(double));
+    return 0;
+  } catch (const relief::Error& e) {
+    g_err = e.what();
+    return -(static_cast<int>(e.code()) + 1);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1000;
+  }
+}
+

@@ -769,3 +769,95 @@ int relief_run_segment(const char* a, const char* b, const char* c, size_t* d) {
   (void)a; (void)b; (void)c; (void)d;
   return fail_with(ST_USAGE, "runners are not part of the oracle restatement");
 }
+
+/* --------------------------------------------------------------- conv-net */
+/* fillNearestValid (analysis.cpp:138-170): FIFO BFS from the valid cells in
+ * index order over the 8-neighbourhood, (dr, dc) in row-major order; the first
+ * popped neighbour claims a cell and hands it its value. */
+static void fill_nearest_valid(const double* layer, const uint8_t* valid, int w, int h,
+                               double* filled) {
+  const size_t n = (size_t)w * h;
+  uint8_t* known = calloc(n, 1);
+  size_t* queue = malloc(n * sizeof *queue);
+  size_t head = 0, tail = 0;
+  for (size_t i = 0; i < n; ++i) {
+    filled[i] = 0.0;
+    if (valid[i]) {
+      filled[i] = layer[i];
+      known[i] = 1;
+      queue[tail++] = i;
+    }
+  }
+  while (head < tail) {
+    const size_t i = queue[head++];
+    const int r = (int)i / w, c = (int)i % w;
+    for (int dr = -1; dr <= 1; ++dr)
+      for (int dc = -1; dc <= 1; ++dc) {
+        if (dr == 0 && dc == 0) continue;
+        const int rr = r + dr, cc = c + dc;
+        if (rr < 0 || rr >= h || cc < 0 || cc >= w) continue;
+        const size_t j = (size_t)rr * w + cc;
+        if (known[j]) continue;
+        known[j] = 1;
+        filled[j] = filled[i];
+        queue[tail++] = j;
+      }
+  }
+  free(known);
+  free(queue);
+}
+
+/* applyActivation (analysis.cpp:172-179). */
+static double activate(double x, int act) {
+  if (act == 0) return x > 0.0 ? x : 0.0;
+  if (act == 1) return 1.0 / (1.0 + exp(-x));
+  return x;
+}
+
+/* convFilterInference (analysis.cpp:183-216) and ConvNetSpec::validate
+ * (analysis.cpp:27-39). */
+int oracle_convnet_infer(int n_layers, const int* ksize, const double* weights, const double* bias,
+                         const int* act, const double* layer, const uint8_t* valid, int w, int h,
+                         double* out) {
+  if (n_layers < 1) return fail_with(ST_MODEL, "model has no layers");
+  size_t off = 0;
+  for (int li = 0; li < n_layers; ++li) {
+    const int k = ksize[li];
+    if (k < 1 || k % 2 == 0) return fail_with(ST_MODEL, "kernel size must be odd and positive");
+    for (size_t q = 0; q < (size_t)k * k; ++q)
+      if (!isfinite(weights[off + q])) return fail_with(ST_MODEL, "non-finite kernel weight");
+    if (!isfinite(bias[li])) return fail_with(ST_MODEL, "non-finite bias");
+    off += (size_t)k * k;
+  }
+  if (w <= 0 || h <= 0) return fail_with(ST_USAGE, "layer size does not match grid dimensions");
+  const size_t n = (size_t)w * h;
+  double* cur = malloc(n * sizeof *cur);
+  double* nxt = malloc(n * sizeof *nxt);
+  fill_nearest_valid(layer, valid, w, h, cur);
+  off = 0;
+  for (int li = 0; li < n_layers; ++li) {
+    const int k = ksize[li], rad = k / 2;
+    const double* kw = weights + off;
+    for (int r = 0; r < h; ++r)
+      for (int c = 0; c < w; ++c) {
+        double acc = bias[li];
+        for (int kr = -rad; kr <= rad; ++kr) {
+          const int rr = r + kr < 0 ? 0 : (r + kr > h - 1 ? h - 1 : r + kr); /* border replicate */
+          for (int kc = -rad; kc <= rad; ++kc) {
+            const int cc = c + kc < 0 ? 0 : (c + kc > w - 1 ? w - 1 : c + kc);
+            acc += kw[(size_t)(kr + rad) * k + (kc + rad)] * cur[(size_t)rr * w + cc];
+          }
+        }
+        nxt[(size_t)r * w + c] = activate(acc, act[li]);
+      }
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
+    off += (size_t)k * k;
+  }
+  for (size_t i = 0; i < n; ++i) out[i] = clampd(cur[i], 0.0, 1.0);
+  free(cur);
+  free(nxt);
+  return ST_OK;
+}
+

@@ -47,6 +47,13 @@ ORACLE_API int relief_map_layer(const relief_map* m, const char* layer, double* 
 ORACLE_API int relief_map_integrate(relief_map* m, const relief_config* c, const double* xyz,
                                     size_t n, const double pose[12], double stamp,
                                     relief_scan_stats* stats);
+/* convFilterInference (analysis.cpp:138-216) with an explicit model: layer li
+ * has kernel ksize[li] x ksize[li] at weights + sum of the previous layers'
+ * k^2, bias[li], activation act[li] (0 relu, 1 sigmoid, 2 identity). The fill
+ * is the reference's literal FIFO BFS. Returns 0, or ST_MODEL / ST_USAGE. */
+ORACLE_API int oracle_convnet_infer(int n_layers, const int* ksize, const double* weights,
+                                    const double* bias, const int* act, const double* layer,
+                                    const uint8_t* valid, int w, int h, double* out);
 /* Not restated (out of the path); present so the shared binding resolves. */
 ORACLE_API relief_map* relief_map_load(const char* path);
 ORACLE_API int relief_map_save(const relief_map* m, const char* path);

@@ -121,6 +121,8 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_map_chain_seconds": (_D, [_P]),
     "relief_gpu_smooth_chain": (_I, [_DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, ctypes.POINTER(_I),
                                      ctypes.POINTER(_I), _DP, _I, _DP, ctypes.POINTER(ctypes.c_uint8)]),
+    "relief_gpu_config_load_convnet": (_I, [_P, _CS]),
+    "relief_gpu_convnet_infer": (_I, [_P, _DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, _DP]),
     "relief_gpu_sim_render": (ctypes.c_int64, [_CS, _DP, _D, ctypes.c_uint64, ctypes.c_uint64, _DP,
                                                ctypes.c_int64]),
 }
@@ -204,6 +206,10 @@ class Config:
 
     def set_seed(self, seed: int) -> None:
         _check(self.lib, self.lib.relief_config_set_seed(self.handle, seed))
+
+    def load_convnet(self, model_path) -> None:
+        """Attach a conv-net weight file; the pipeline then uses the learned filter."""
+        _check(self.lib, self.lib.relief_gpu_config_load_convnet(self.handle, str(model_path).encode()))
 
     def close(self) -> None:
         if self.handle:
@@ -357,6 +363,18 @@ def smooth_chain(lib, values: np.ndarray, valid: np.ndarray, steps: Sequence[tup
     _check(lib, lib.relief_gpu_smooth_chain(_dptr(values), valid.ctypes.data_as(u8), W, H, kinds, radii,
                                             sig, len(steps), _dptr(vo), ko.ctypes.data_as(u8)))
     return vo, ko
+
+
+def convnet_infer(lib, config: "Config", layer: np.ndarray, valid: np.ndarray) -> np.ndarray:
+    """relief_gpu_convnet_infer: the config's conv-net over a host layer (H, W)."""
+    layer = np.ascontiguousarray(layer, dtype=np.float64)
+    valid = np.ascontiguousarray(valid, dtype=np.uint8)
+    H, W = layer.shape
+    out = np.empty_like(layer)
+    _check(lib, lib.relief_gpu_convnet_infer(config.handle, _dptr(layer),
+                                             valid.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), W, H,
+                                             _dptr(out)))
+    return out
 
 
 def sim_render(lib, config_path, pose, time: float, seed: int, scan_index: int,

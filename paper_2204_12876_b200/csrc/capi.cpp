@@ -93,9 +93,13 @@ void validateScan(const rb200::PipelineParams& p, const rb200::Pose& pose) {
   p.cleanup.validate();
   if (!pose.isValid()) rb200::fail(rb200::Err::kInvalidPose, "rotation is not orthonormal");
   if (p.overlap.enabled) p.overlap.validate();
-  if (p.use_convnet_traversability)
-    rb200::fail(rb200::Err::kInvalidModel, "model has no layers");
-  p.traversability.validate();
+  // The reference validates whichever traversability filter runs
+  // (analysis.cpp:89 / 187). A config loaded through relief_config_load names
+  // the model file but carries no layers, so the conv-net path fails with
+  // "model has no layers" exactly as the reference's C API does, unless the
+  // model was attached with relief_gpu_config_load_convnet.
+  if (p.use_convnet_traversability) p.convnet.validate();
+  else p.traversability.validate();
 }
 
 void fillStats(const rb200::ScanResult& r, relief_scan_stats* s) {
@@ -397,6 +401,27 @@ relief_status relief_gpu_smooth_chain(const double* values, const uint8_t* valid
   return guard([&] {
     rb200::runHostChain(currentDevice(), values, valid, width, height, kinds, radii, sigmas,
                         n_steps, values_out, valid_out);
+  });
+}
+
+relief_status relief_gpu_config_load_convnet(relief_config* config, const char* model_path) {
+  if (config == nullptr || model_path == nullptr) return usage("null argument");
+  return guard([&] {
+    rb200::ConvNetSpec spec = rb200::loadConvNetSpecFile(model_path);
+    config->config.convnet_path = model_path;
+    config->config.pipeline.convnet = std::move(spec);
+    config->config.pipeline.use_convnet_traversability = true;
+  });
+}
+
+relief_status relief_gpu_convnet_infer(const relief_config* config, const double* layer,
+                                       const uint8_t* valid, int width, int height,
+                                       double* out) {
+  if (config == nullptr || layer == nullptr || valid == nullptr || out == nullptr)
+    return usage("null argument");
+  return guard([&] {
+    rb200::runHostConvnet(currentDevice(), config->config.pipeline.convnet, layer, valid, width,
+                          height, out);
   });
 }
 

@@ -158,6 +158,7 @@ void destroyDeviceMap(DeviceMap* m) {
   cudaFree(m->rslab);
   cudaFree(m->export_buf);
   m->chain.release();
+  m->conv.release();
   cudaFree(m->chain_in);
   cudaFree(m->chain_out);
   cudaFree(m->chain_out_ok);

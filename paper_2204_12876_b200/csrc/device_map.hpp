@@ -77,6 +77,24 @@ struct ChainScratch {
   void release();
 };
 
+// Device scratch of the conv-net traversability executor (convnet.cu).
+struct ConvScratch {
+  uint32_t* root = nullptr;   // BFS: smallest root index reaching the cell
+  uint32_t* level = nullptr;  // BFS level (Chebyshev distance to a valid cell)
+  uint32_t* fa = nullptr;     // frontier ping-pong
+  uint32_t* fb = nullptr;
+  uint32_t* cnt = nullptr;    // level sizes (3 rotating counters)
+  double* va = nullptr;       // layer activations ping-pong
+  double* vb = nullptr;
+  double* weights = nullptr;    // all layers' kernels, concatenated
+  double* h_weights = nullptr;  // pinned staging copy
+  std::size_t cap = 0, wcap = 0;
+  int bfs_blocks = 0;
+  cudaEvent_t upload_done = nullptr;
+  void ensure(std::size_t n, std::size_t n_weights);
+  void release();
+};
+
 struct DeviceMap {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -122,12 +140,13 @@ struct DeviceMap {
   bool has_last = false;
   double* export_buf = nullptr;  // masked-layer staging for get_layer
   ChainScratch chain;            // post-processing chain scratch
+  ConvScratch conv;              // conv-net traversability scratch
   double* chain_in = nullptr;    // masked input layer of the chain
   double* chain_out = nullptr;   // chain output staging for host callers
   uint8_t* chain_out_ok = nullptr;
   double last_chain_seconds = 0.0;
   int last_chain_launches = 0;
-  cudaEvent_t ev[12] = {};
+  cudaEvent_t ev[13] = {};
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
   long long last_launches = 0;
@@ -175,6 +194,16 @@ struct ChainStep {
 int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
                        const uint8_t* d_valid, int W, int H, const ChainStep* steps, int n_steps,
                        double* d_values_out, uint8_t* d_valid_out);
+// Conv-net traversability (convnet.cu): nearest-valid fill of d_layer by
+// d_valid, then the spec's layer stack; writes all W*H cells of d_out.
+// Enqueued on `s`; returns the number of launches.
+int convnetEnqueue(cudaStream_t s, ConvScratch& cs, const double* d_layer, const uint8_t* d_valid,
+                   int W, int H, const ConvNetSpec& spec, double* d_out);
+
+// Same on caller-supplied host arrays, on `device` (synchronous).
+void runHostConvnet(int device, const ConvNetSpec& spec, const double* layer, const uint8_t* valid,
+                    int W, int H, double* out);
+
 // Syncs `s` and raises NothingToInpaint if an inpaint step saw no valid cell.
 void smoothChainCheck(cudaStream_t s, ChainScratch& sc);
 

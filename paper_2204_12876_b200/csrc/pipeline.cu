@@ -1059,6 +1059,7 @@ struct CellArgs {
   double slope_max, step_max, rough_max, w_slope, w_step, w_rough;
   int time_var;
   double growth, sigma_max2;
+  int geo_trav;  // geometric traversability (off when the conv-net writes the layer)
 };
 
 constexpr int kTileX = 32, kTileY = 8;
@@ -1137,7 +1138,7 @@ __global__ void __launch_bounds__(kTileX* kTileY)
       L.ny[i] = ny;
       L.nz[i] = nz;
       double trav = 0.0;
-      if (nx != 0.0 || ny != 0.0 || nz != 0.0) {
+      if (a.geo_trav && (nx != 0.0 || ny != 0.0 || nz != 0.0)) {
         const double slope = acos(sclamp(nz, -1.0, 1.0));
         const double s_slope = sclamp(1.0 - slope / a.slope_max, 0.0, 1.0);
         double max_step = 0.0, sum = 0.0, sum_sq = 0.0;
@@ -1163,7 +1164,7 @@ __global__ void __launch_bounds__(kTileX* kTileY)
         const double s_rough = sclamp(1.0 - sqrt(var) / a.rough_max, 0.0, 1.0);
         trav = a.w_slope * s_slope + a.w_step * s_step + a.w_rough * s_rough;
       }
-      L.trav[i] = trav;
+      if (a.geo_trav) L.trav[i] = trav;
       if (a.time_var && count[i] == 0) L.var[i] = smin(L.var[i] + a.growth, a.sigma_max2);
     }
   }
@@ -1392,7 +1393,8 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     ca.ov_r2 = P.overlap.radius * P.overlap.radius;
     ca.ov_thr = P.overlap.height_threshold;
     const TraversabilityParams& T = P.traversability;
-    ca.radius = T.window / 2;
+    ca.geo_trav = P.use_convnet_traversability ? 0 : 1;
+    ca.radius = ca.geo_trav ? T.window / 2 : 1;
     ca.slope_max = T.slope_max;
     ca.step_max = T.step_max;
     ca.rough_max = T.roughness_max;
@@ -1413,6 +1415,11 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     ++launches;
   }
   checkCuda(cudaEventRecord(m.ev[7], s), "event");  // cell phases done
+  // Conv-net traversability (reference integration.cpp:242-244): reads the
+  // post-overlap elevation, writes the traversability of every cell.
+  if (P.use_convnet_traversability)
+    launches += convnetEnqueue(s, m.conv, m.cur.elev, m.cur.valid, g.W, g.H, P.convnet, m.cur.trav);
+  checkCuda(cudaEventRecord(m.ev[12], s), "event");  // traversability done
   checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s), "stats");
   checkCuda(cudaGetLastError(), "kernel launch");
   checkCuda(cudaStreamSynchronize(s), "integrate");
@@ -1434,16 +1441,18 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   out.drift_clamped = d.drift_clamped != 0;
   out.drift_points = d.drift_n;
 
-  float ms[7];
+  float ms[7], ms_trav = 0.0f;
   for (int k = 0; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
+  checkCuda(cudaEventElapsedTime(&ms_trav, m.ev[7], m.ev[12]), "timing");
   // ms: upload, ingest(+shift), drift, sort, fusion, rays, cell phases
-  for (int k = 0; k < 7; ++k) m.kernel_seconds[k] = ms[k] * 1e-3;
-  m.kernel_seconds[7] = (ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6]) * 1e-3;
+  for (int k = 0; k < 6; ++k) m.kernel_seconds[k] = ms[k] * 1e-3;
+  m.kernel_seconds[6] = (ms[6] + ms_trav) * 1e-3;
+  m.kernel_seconds[7] = (ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6] + ms_trav) * 1e-3;
   m.phase_seconds[0] = ms[1] * 1e-3;                    // point transform & z error count
   m.phase_seconds[1] = ms[2] * 1e-3;                    // drift compensation
   m.phase_seconds[2] = (ms[3] + ms[4] + ms[5]) * 1e-3;  // height update & ray casting
-  m.phase_seconds[3] = ms[6] * 1e-3;                    // overlap + normals + traversability (fused)
-  m.phase_seconds[4] = 0.0;
+  m.phase_seconds[3] = ms[6] * 1e-3;                    // overlap + normals (+ geometric traversability, fused)
+  m.phase_seconds[4] = ms_trav * 1e-3;                  // conv-net traversability
   m.phase_seconds[5] = 0.0;
   m.phase_seconds[6] = m.kernel_seconds[7];
   out.seconds = m.phase_seconds[6];

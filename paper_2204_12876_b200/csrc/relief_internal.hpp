@@ -144,6 +144,27 @@ struct OverlapParams {
 
 enum class ExecMode { kDeterministic, kParallel };
 
+// Learned traversability filter: a stack of k x k border-replicate
+// convolutions over the nearest-valid-filled elevation (reference
+// analysis.hpp:44-65, analysis.cpp:27-39,138-216).
+enum class Activation { kRelu, kSigmoid, kIdentity };
+
+struct ConvLayer {
+  int kernel_size = 1;          // odd
+  std::vector<double> kernel;   // kernel_size^2, row-major
+  double bias = 0.0;
+  Activation activation = Activation::kIdentity;
+};
+
+struct ConvNetSpec {
+  std::vector<ConvLayer> layers;
+  void validate() const;
+};
+
+// Weight file reader (reference analysis.cpp:218-290), same grammar and errors.
+ConvNetSpec loadConvNetSpecText(const std::string& text);
+ConvNetSpec loadConvNetSpecFile(const std::string& path);
+
 struct PipelineParams {
   UpdateParams update;
   DriftParams drift;
@@ -152,6 +173,7 @@ struct PipelineParams {
   OverlapParams overlap;
   ExecMode mode = ExecMode::kDeterministic;
   bool use_convnet_traversability = false;
+  ConvNetSpec convnet;  // loaded by the runners / relief_gpu_config_load_convnet
 };
 
 struct PlaneSegParams {

@@ -42,10 +42,7 @@ int currentDevice() {
 // Stateful wrapper tracking the inter-scan dt (reference integration.hpp:146-169).
 class Pipeline {
  public:
-  Pipeline(const Grid& g, const PipelineParams& p) : map_(createDeviceMap(currentDevice(), g)), params_(p) {
-    if (p.use_convnet_traversability)
-      fail(Err::kInvalidModel, "conv-net traversability is not available in the B200 build");
-  }
+  Pipeline(const Grid& g, const PipelineParams& p) : map_(createDeviceMap(currentDevice(), g)), params_(p) {}
   ScanResult integrate(const std::vector<double>& xyz, const Pose& pose, double stamp) {
     if (!pose.isValid()) fail(Err::kInvalidPose, "rotation is not orthonormal");
     const double dt = has_prev_ ? std::max(0.0, stamp - last_) : 0.0;
@@ -176,6 +173,16 @@ std::vector<TimedPose> loadPosesCsv(const std::string& path) {
 
 }  // namespace
 
+// Loads the conv-net weights named by the config (reference runner.cpp:53-60).
+static PipelineParams preparePipeline(const RunConfig& cfg) {
+  PipelineParams p = cfg.pipeline;
+  if (p.use_convnet_traversability && p.convnet.layers.empty()) {
+    if (cfg.convnet_path.empty()) fail(Err::kUsage, "convnet traversability requested without a model");
+    p.convnet = loadConvNetSpecFile(cfg.convnet_path);
+  }
+  return p;
+}
+
 bool parseMode(const std::string& m, ExecMode& out) {
   if (m == "det" || m == "deterministic") out = ExecMode::kDeterministic;
   else if (m == "par" || m == "parallel") out = ExecMode::kParallel;
@@ -189,10 +196,8 @@ void runSimulate(const std::string& config_path, const std::string& out_dir, std
   if (has_seed) cfg.seed = seed;
   cfg.validate();
   cfg.trajectory.validate();
-  if (cfg.pipeline.use_convnet_traversability && cfg.convnet_path.empty())
-    fail(Err::kUsage, "convnet traversability requested without a model");
   ensureDir(out_dir);
-  Pipeline pipe(cfg.map, cfg.pipeline);
+  Pipeline pipe(cfg.map, preparePipeline(cfg));
   std::ofstream stats(out_dir + "/stats.csv");
   if (!stats) fail(Err::kIo, "cannot write stats.csv in " + out_dir);
   statsHeader(stats);
@@ -215,9 +220,7 @@ void runReplay(const std::string& config_path, const std::vector<std::string>& c
   cfg.validate();
   ensureDir(out_dir);
   const std::vector<TimedPose> poses = loadPosesCsv(poses_path);
-  if (cfg.pipeline.use_convnet_traversability && cfg.convnet_path.empty())
-    fail(Err::kUsage, "convnet traversability requested without a model");
-  Pipeline pipe(cfg.map, cfg.pipeline);
+  Pipeline pipe(cfg.map, preparePipeline(cfg));
   std::ofstream stats(out_dir + "/stats.csv");
   if (!stats) fail(Err::kIo, "cannot write stats.csv in " + out_dir);
   statsHeader(stats);
@@ -242,8 +245,6 @@ void runBench(const std::string& config_path, const std::vector<std::size_t>& co
   RunConfig cfg = configWithMode(config_path, mode);
   cfg.validate();
   if (repetitions < 1) fail(Err::kUsage, "repetitions must be >= 1");
-  if (cfg.pipeline.use_convnet_traversability && cfg.convnet_path.empty())
-    fail(Err::kUsage, "convnet traversability requested without a model");
   Scene scene = cfg.scene;
   if (!scene.has_ground && scene.solids.empty()) scene.addGround(0.0);
   Pose pose;
@@ -263,7 +264,7 @@ void runBench(const std::string& config_path, const std::vector<std::size_t>& co
       const std::size_t pick = rng.next() % nref;
       cloud.insert(cloud.end(), ref.begin() + 3 * pick, ref.begin() + 3 * pick + 3);
     }
-    Pipeline pipe(cfg.map, cfg.pipeline);
+    Pipeline pipe(cfg.map, preparePipeline(cfg));
     {
       // Warm start: one untimed scan with a point at every cell centre.
       const Grid& g = pipe.map().grid;
