@@ -6,18 +6,24 @@
 //      index order. The BFS queue is ordered by (root index, offset chain)
 //      lexicographically -- level 0 is index order, and each level is ordered
 //      by (parent rank, neighbour offset) -- so the first neighbour popped is
-//      the previous-level neighbour with the smallest ROOT. Hence the filled
-//      value is elev[root(j)] with root(j) = min over previous-level
-//      neighbours p of root(p): an order-free min that a level-synchronous
-//      device BFS computes exactly with atomicMin (levels = Chebyshev distance
-//      to the nearest valid cell). One cooperative persistent kernel runs all
-//      levels with a grid barrier between them.
+//      the previous-level neighbour with the smallest ROOT, and by induction
+//      root(j) = the smallest index among the valid cells at the minimum
+//      Chebyshev distance D from j (the BFS level of j: on a full grid every
+//      source at distance D lies on a shortest 8-path to j). No BFS is run:
+//        * D = the smallest k whose (2k+1)^2 square around j holds a valid
+//          cell -- binary search over k with O(1) square counts from a
+//          summed-area table of the validity mask;
+//        * the sources at distance exactly D lie on the square ring of radius
+//          D, so the smallest index is the first hit among: the top row
+//          (next valid column >= c-D within c+D), then the two side columns
+//          (next valid row >= r-D+1 within r+D-1, left column first on a tie),
+//          then the bottom row -- O(1) with per-row "next valid column" and
+//          per-column "next valid row" tables.
 //   2. the layer stack: k x k border-replicate convolution, acc = bias then
 //      acc += w * x in (kr, kc) row-major order (fp64, no FMA: bit-exact),
 //      relu / sigmoid / identity, and the final clamp to [0, 1]. Every cell is
 //      written, valid or not (test_io.cpp:237-238). Sigmoid uses the device
 //      exp (≤ 1 ulp from glibc's), the only inexact step.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,85 +32,154 @@
 #include "device_map.hpp"
 #include "fp_exact.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace rb200 {
 
 namespace {
 
 constexpr int kThreads = 256;
-constexpr uint32_t kUnknown = 0xffffffffu;
 constexpr int kConvTX = 32, kConvTY = 8;
 
-// Level 0: every valid cell, its own root. Queue order is irrelevant here:
-// the min-root rule makes the result independent of it.
+// Per row (one warp each): inclusive prefix count of valid cells (the first
+// summed-area pass) and next_col[r][c] = smallest valid column >= c (W if none).
 __global__ void __launch_bounds__(kThreads)
-    k_cn_seed(const uint8_t* __restrict__ valid, uint32_t n, uint32_t* __restrict__ level,
-              uint32_t* __restrict__ root, uint32_t* __restrict__ frontier, uint32_t* cnt) {
-  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  const bool v = i < n && valid[i] != 0;
-  if (i < n) {
-    level[i] = v ? 0u : kUnknown;
-    root[i] = v ? i : kUnknown;
-  }
-  const unsigned mask = __ballot_sync(0xffffffffu, v);
-  if (mask == 0) return;
+    k_cn_rows(const uint8_t* __restrict__ valid, int W, int H, uint32_t* __restrict__ sat,
+              uint32_t* __restrict__ next_col) {
+  const int r = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(cnt, static_cast<uint32_t>(__popc(mask)));
-  base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
-  if (v) frontier[base + __popc(mask & ((1u << lane) - 1u))] = i;
-}
-
-// All BFS levels. cnt[d % 3] holds the size of level d; the counter of level
-// d + 2 is cleared while level d is expanded (nobody reads or writes it then).
-__global__ void __launch_bounds__(kThreads)
-    k_cn_bfs(uint32_t* level, uint32_t* root, uint32_t* fa, uint32_t* fb, uint32_t* cnt, int W,
-             int H) {
-  cg::grid_group grid = cg::this_grid();
-  const uint32_t stride = gridDim.x * kThreads;
-  const uint32_t tid = blockIdx.x * kThreads + threadIdx.x;
-  for (uint32_t d = 1;; ++d) {
-    const uint32_t n = *reinterpret_cast<volatile uint32_t*>(&cnt[(d - 1) % 3]);
-    if (n == 0) break;
-    const uint32_t* cur = (d & 1) ? fa : fb;
-    uint32_t* nxt = (d & 1) ? fb : fa;
-    uint32_t* ncnt = &cnt[d % 3];
-    if (tid == 0) cnt[(d + 1) % 3] = 0;
-    for (uint32_t q = tid; q < n; q += stride) {
-      const uint32_t p = cur[q];
-      const uint32_t rp = root[p];
-      const int r = static_cast<int>(p / static_cast<uint32_t>(W));
-      const int c = static_cast<int>(p - static_cast<uint32_t>(r) * W);
-      for (int dr = -1; dr <= 1; ++dr) {
-        const int rr = r + dr;
-        if (rr < 0 || rr >= H) continue;
-        for (int dc = -1; dc <= 1; ++dc) {
-          const int cc = c + dc;
-          if ((dr == 0 && dc == 0) || cc < 0 || cc >= W) continue;
-          const uint32_t j = static_cast<uint32_t>(rr) * W + cc;
-          uint32_t lv = *reinterpret_cast<volatile uint32_t*>(&level[j]);
-          if (lv < d) continue;  // reached at an earlier level
-          if (lv == kUnknown) {
-            lv = atomicCAS(&level[j], kUnknown, d);
-            if (lv == kUnknown) nxt[atomicAdd(ncnt, 1u)] = j;
-            else if (lv < d) continue;
-          }
-          atomicMin(&root[j], rp);
-        }
-      }
+  if (r >= H) return;
+  const size_t row = static_cast<size_t>(r) * W;
+  uint32_t carry = 0;
+  for (int c0 = 0; c0 < W; c0 += 32) {
+    const int c = c0 + lane;
+    uint32_t v = (c < W && valid[row + c]) ? 1u : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
     }
-    grid.sync();
+    if (c < W) sat[row + c] = carry + v;
+    carry += __shfl_sync(0xffffffffu, v, 31);
+  }
+  uint32_t next = static_cast<uint32_t>(W);
+  for (int c0 = ((W - 1) / 32) * 32; c0 >= 0; c0 -= 32) {
+    const int c = c0 + lane;
+    uint32_t v = (c < W && valid[row + c]) ? static_cast<uint32_t>(c) : next;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_down_sync(0xffffffffu, v, o);
+      if (lane + o < 32) v = min(v, t);
+    }
+    if (c < W) next_col[row + c] = v;
+    next = __shfl_sync(0xffffffffu, v, 0);
   }
 }
 
+// Per column: the second summed-area pass and next_row[r][c] = smallest valid
+// row >= r in column c (H if none). A block covers 32 columns (lanes) x 32
+// row strips (warps): strip totals / first valid rows are combined through
+// shared memory, then each strip is rewritten with its carry.
+constexpr int kStrips = 32;
+__global__ void __launch_bounds__(32 * kStrips)
+    k_cn_cols(const uint8_t* __restrict__ valid, int W, int H, uint32_t* __restrict__ sat,
+              uint32_t* __restrict__ next_row) {
+  __shared__ uint32_t s_sum[kStrips][33];
+  __shared__ uint32_t s_first[kStrips][33];
+  const int lane = threadIdx.x & 31, strip = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const int len = (H + kStrips - 1) / kStrips;
+  const int rb = strip * len, re = min(rb + len, H);
+  uint32_t sum = 0, first = static_cast<uint32_t>(H);
+  if (c < W) {
+    for (int r = rb; r < re; ++r) {
+      const size_t i = static_cast<size_t>(r) * W + c;
+      sum += sat[i];
+      if (first == static_cast<uint32_t>(H) && valid[i]) first = static_cast<uint32_t>(r);
+    }
+  }
+  s_sum[strip][lane] = sum;
+  s_first[strip][lane] = first;
+  __syncthreads();
+  if (c >= W) return;
+  uint32_t acc = 0, next = static_cast<uint32_t>(H);
+  for (int k = 0; k < strip; ++k) acc += s_sum[k][lane];
+  for (int k = kStrips - 1; k > strip; --k) next = min(next, s_first[k][lane]);
+  for (int r = rb; r < re; ++r) {
+    const size_t i = static_cast<size_t>(r) * W + c;
+    acc += sat[i];
+    sat[i] = acc;
+  }
+  for (int r = re - 1; r >= rb; --r) {
+    const size_t i = static_cast<size_t>(r) * W + c;
+    if (valid[i]) next = static_cast<uint32_t>(r);
+    next_row[i] = next;
+  }
+}
+
+struct FillTables {
+  const uint8_t* valid;
+  const uint32_t* sat;
+  const uint32_t* next_col;
+  const uint32_t* next_row;
+  int W, H;
+};
+
+// Valid cells in rows [r1, r2] x cols [c1, c2] (already clipped to the grid).
+__device__ __forceinline__ uint32_t squareCount(const FillTables& t, int r1, int c1, int r2, int c2) {
+  const uint32_t* S = t.sat;
+  const int W = t.W;
+  uint32_t v = S[static_cast<size_t>(r2) * W + c2];
+  if (r1 > 0) v -= S[static_cast<size_t>(r1 - 1) * W + c2];
+  if (c1 > 0) v -= S[static_cast<size_t>(r2) * W + c1 - 1];
+  if (r1 > 0 && c1 > 0) v += S[static_cast<size_t>(r1 - 1) * W + c1 - 1];
+  return v;
+}
+
+// fillNearestValid + the first conv layer's input: out[i] = layer[root(i)].
 __global__ void __launch_bounds__(kThreads)
-    k_cn_gather(const double* __restrict__ elev, const uint32_t* __restrict__ root, uint32_t n,
-                double* __restrict__ out) {
-  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t r = root[i];
-  out[i] = r == kUnknown ? 0.0 : elev[r];  // no valid cell at all: zeros
+    k_cn_fill(FillTables t, const double* __restrict__ layer, double* __restrict__ out) {
+  const size_t i = blockIdx.x * static_cast<size_t>(kThreads) + threadIdx.x;
+  const int W = t.W, H = t.H;
+  if (i >= static_cast<size_t>(W) * H) return;
+  if (t.valid[i]) {
+    out[i] = layer[i];
+    return;
+  }
+  const uint32_t total = t.sat[static_cast<size_t>(W) * H - 1];
+  if (total == 0) {
+    out[i] = 0.0;  // no valid cell at all
+    return;
+  }
+  const int r = static_cast<int>(i / W), c = static_cast<int>(i % W);
+  // smallest D >= 1 with a valid cell in the square of radius D
+  int lo = 1, hi = max(max(r, H - 1 - r), max(c, W - 1 - c));
+  while (lo < hi) {
+    const int k = (lo + hi) >> 1;
+    if (squareCount(t, max(r - k, 0), max(c - k, 0), min(r + k, H - 1), min(c + k, W - 1)) > 0)
+      hi = k;
+    else
+      lo = k + 1;
+  }
+  const int D = lo;
+  const int cl = max(c - D, 0), cr = min(c + D, W - 1);
+  size_t root;
+  if (r - D >= 0 && t.next_col[static_cast<size_t>(r - D) * W + cl] <= static_cast<uint32_t>(cr)) {
+    root = static_cast<size_t>(r - D) * W + t.next_col[static_cast<size_t>(r - D) * W + cl];
+  } else {
+    root = ~static_cast<size_t>(0);
+    const int top = max(r - D + 1, 0), bottom = min(r + D - 1, H - 1);
+    if (c - D >= 0) {
+      const uint32_t y = t.next_row[static_cast<size_t>(top) * W + (c - D)];
+      if (y <= static_cast<uint32_t>(bottom)) root = static_cast<size_t>(y) * W + (c - D);
+    }
+    if (c + D < W) {
+      const uint32_t y = t.next_row[static_cast<size_t>(top) * W + (c + D)];
+      if (y <= static_cast<uint32_t>(bottom))
+        root = min(root, static_cast<size_t>(y) * W + (c + D));
+    }
+    if (root == ~static_cast<size_t>(0))  // bottom row (exists: D is the minimum distance)
+      root = static_cast<size_t>(r + D) * W + t.next_col[static_cast<size_t>(r + D) * W + cl];
+  }
+  out[i] = layer[root];
 }
 
 __device__ __forceinline__ double activate(double x, int act) {
@@ -142,6 +217,57 @@ __global__ void __launch_bounds__(kConvTX* kConvTY)
   out[static_cast<size_t>(r) * W + c] = v;
 }
 
+// Fixed-K layer: each thread produces 4 outputs of one tile row at columns
+// tx, tx+32, tx+64, tx+96 (conflict-free shared loads), so every weight read
+// from shared memory feeds 4 multiply-adds; the (kr, kc) loops are unrolled.
+// Each output still sums bias + w*x in (kr, kc) row-major order.
+constexpr int kWideX = 4 * kConvTX;
+template <int K>
+__global__ void __launch_bounds__(kConvTX* kConvTY)
+    k_cn_conv_k(const double* __restrict__ in, double* __restrict__ out, int W, int H,
+                const double* __restrict__ w, double bias, int act, int clamp01) {
+  constexpr int R = K / 2, TW = kWideX + 2 * R, TH = kConvTY + 2 * R;
+  __shared__ double tile[TW * TH];
+  __shared__ double sw[K * K];
+  const int c0 = blockIdx.x * kWideX - R, r0 = blockIdx.y * kConvTY - R;
+  const int tid = threadIdx.y * kConvTX + threadIdx.x;
+  for (int q = tid; q < K * K; q += kConvTX * kConvTY) sw[q] = w[q];
+  for (int q = tid; q < TW * TH; q += kConvTX * kConvTY) {
+    const int rr = min(max(r0 + q / TW, 0), H - 1);
+    const int cc = min(max(c0 + q % TW, 0), W - 1);
+    tile[q] = in[static_cast<size_t>(rr) * W + cc];
+  }
+  __syncthreads();
+  double acc[4] = {bias, bias, bias, bias};
+#pragma unroll
+  for (int kr = 0; kr < K; ++kr) {
+    const double* trow = tile + (threadIdx.y + kr) * TW + threadIdx.x;
+#pragma unroll
+    for (int kc = 0; kc < K; ++kc) {
+      const double wv = sw[kr * K + kc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = acc[j] + wv * trow[kc + 32 * j];
+    }
+  }
+  const int r = blockIdx.y * kConvTY + threadIdx.y;
+  if (r >= H) return;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = blockIdx.x * kWideX + threadIdx.x + 32 * j;
+    if (c >= W) continue;
+    double v = activate(acc[j], act);
+    if (clamp01) v = sclamp(v, 0.0, 1.0);
+    out[static_cast<size_t>(r) * W + c] = v;
+  }
+}
+
+template <int K>
+void launchConvK(cudaStream_t s, const double* in, double* out, int W, int H, const double* w,
+                 double bias, int act, int clamp01) {
+  const dim3 grid((W + kWideX - 1) / kWideX, (H + kConvTY - 1) / kConvTY);
+  k_cn_conv_k<K><<<grid, dim3(kConvTX, kConvTY), 0, s>>>(in, out, W, H, w, bias, act, clamp01);
+}
+
 // Same layer straight from global memory, for kernels whose halo tile would
 // not fit in shared memory.
 __global__ void __launch_bounds__(kThreads)
@@ -168,23 +294,20 @@ __global__ void __launch_bounds__(kThreads)
 
 void ConvScratch::ensure(std::size_t n, std::size_t n_weights) {
   if (n > cap) {
-    cudaFree(root);
-    cudaFree(level);
-    cudaFree(fa);
-    cudaFree(fb);
+    cudaFree(sat);
+    cudaFree(next_col);
+    cudaFree(next_row);
     cudaFree(va);
     cudaFree(vb);
-    root = level = fa = fb = nullptr;
+    sat = next_col = next_row = nullptr;
     va = vb = nullptr;
-    checkCuda(cudaMalloc(&root, n * sizeof(uint32_t)), "convnet scratch");
-    checkCuda(cudaMalloc(&level, n * sizeof(uint32_t)), "convnet scratch");
-    checkCuda(cudaMalloc(&fa, n * sizeof(uint32_t)), "convnet scratch");
-    checkCuda(cudaMalloc(&fb, n * sizeof(uint32_t)), "convnet scratch");
+    checkCuda(cudaMalloc(&sat, n * sizeof(uint32_t)), "convnet scratch");
+    checkCuda(cudaMalloc(&next_col, n * sizeof(uint32_t)), "convnet scratch");
+    checkCuda(cudaMalloc(&next_row, n * sizeof(uint32_t)), "convnet scratch");
     checkCuda(cudaMalloc(&va, n * sizeof(double)), "convnet scratch");
     checkCuda(cudaMalloc(&vb, n * sizeof(double)), "convnet scratch");
     cap = n;
   }
-  if (cnt == nullptr) checkCuda(cudaMalloc(&cnt, 4 * sizeof(uint32_t)), "convnet scratch");
   if (n_weights > wcap) {
     cudaFree(weights);
     cudaFreeHost(h_weights);
@@ -196,21 +319,18 @@ void ConvScratch::ensure(std::size_t n, std::size_t n_weights) {
 }
 
 void ConvScratch::release() {
-  cudaFree(root);
-  cudaFree(level);
-  cudaFree(fa);
-  cudaFree(fb);
+  cudaFree(sat);
+  cudaFree(next_col);
+  cudaFree(next_row);
   cudaFree(va);
   cudaFree(vb);
-  cudaFree(cnt);
   cudaFree(weights);
   if (h_weights) cudaFreeHost(h_weights);
   if (upload_done) cudaEventDestroy(upload_done);
   upload_done = nullptr;
-  root = level = fa = fb = cnt = nullptr;
+  sat = next_col = next_row = nullptr;
   va = vb = weights = h_weights = nullptr;
   cap = wcap = 0;
-  bfs_blocks = 0;
 }
 
 int convnetEnqueue(cudaStream_t s, ConvScratch& cs, const double* d_layer, const uint8_t* d_valid,
@@ -218,7 +338,7 @@ int convnetEnqueue(cudaStream_t s, ConvScratch& cs, const double* d_layer, const
   spec.validate();
   if (W <= 0 || H <= 0) fail(Err::kUsage, "layer size does not match grid dimensions");
   const std::size_t n = static_cast<std::size_t>(W) * H;
-  if (n >= kUnknown) fail(Err::kUsage, "layer too large for the conv-net executor");
+  if (n >= 0xffffffffu) fail(Err::kUsage, "layer too large for the conv-net executor");
   std::size_t nw = 0;
   for (const ConvLayer& l : spec.layers) nw += l.kernel.size();
   // Weights are staged through pinned memory; the previous call's copy may
@@ -237,29 +357,13 @@ int convnetEnqueue(cudaStream_t s, ConvScratch& cs, const double* d_layer, const
   checkCuda(cudaEventRecord(cs.upload_done, s), "event");
 
   // 1. nearest-valid fill.
-  checkCuda(cudaMemsetAsync(cs.cnt, 0, 4 * sizeof(uint32_t), s), "memset");
+  k_cn_rows<<<(H + kThreads / 32 - 1) / (kThreads / 32), kThreads, 0, s>>>(d_valid, W, H, cs.sat,
+                                                                           cs.next_col);
+  k_cn_cols<<<(W + 31) / 32, 32 * kStrips, 0, s>>>(d_valid, W, H, cs.sat, cs.next_row);
   const unsigned nb = static_cast<unsigned>((n + kThreads - 1) / kThreads);
-  k_cn_seed<<<nb, kThreads, 0, s>>>(d_valid, static_cast<uint32_t>(n), cs.level, cs.root, cs.fa,
-                                     cs.cnt);
-  ++launches;
-  if (cs.bfs_blocks == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    checkCuda(cudaGetDevice(&dev), "device");
-    checkCuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attribute");
-    checkCuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cn_bfs, kThreads, 0),
-              "occupancy");
-    cs.bfs_blocks = std::max(1, sms * std::min(per_sm, 4));
-  }
-  {
-    int Wi = W, Hi = H;
-    void* args[] = {&cs.level, &cs.root, &cs.fa, &cs.fb, &cs.cnt, &Wi, &Hi};
-    checkCuda(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cn_bfs), dim3(cs.bfs_blocks),
-                                          dim3(kThreads), args, 0, s),
-              "convnet fill launch");
-    ++launches;
-  }
-  k_cn_gather<<<nb, kThreads, 0, s>>>(d_layer, cs.root, static_cast<uint32_t>(n), cs.va);
-  ++launches;
+  k_cn_fill<<<nb, kThreads, 0, s>>>(FillTables{d_valid, cs.sat, cs.next_col, cs.next_row, W, H},
+                                    d_layer, cs.va);
+  launches += 3;
 
   // 2. the layer stack; the last layer clamps and writes the output.
   const double* cur = cs.va;
@@ -272,7 +376,19 @@ int convnetEnqueue(cudaStream_t s, ConvScratch& cs, const double* d_layer, const
     const std::size_t smem =
         static_cast<std::size_t>(kConvTX + 2 * rad) * (kConvTY + 2 * rad) * sizeof(double);
     const int act = static_cast<int>(l.activation);
-    if (smem <= 200 * 1024) {
+    const double* wl = cs.weights + off;
+    switch (l.kernel_size) {
+      case 1: launchConvK<1>(s, cur, dst, W, H, wl, l.bias, act, last); break;
+      case 3: launchConvK<3>(s, cur, dst, W, H, wl, l.bias, act, last); break;
+      case 5: launchConvK<5>(s, cur, dst, W, H, wl, l.bias, act, last); break;
+      case 7: launchConvK<7>(s, cur, dst, W, H, wl, l.bias, act, last); break;
+      case 9: launchConvK<9>(s, cur, dst, W, H, wl, l.bias, act, last); break;
+      case 11: launchConvK<11>(s, cur, dst, W, H, wl, l.bias, act, last); break;
+      default: break;
+    }
+    if (l.kernel_size <= 11) {
+      // launched above
+    } else if (smem <= 200 * 1024) {
       if (smem > 48 * 1024)
         checkCuda(cudaFuncSetAttribute(k_cn_conv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)),

@@ -79,17 +79,14 @@ struct ChainScratch {
 
 // Device scratch of the conv-net traversability executor (convnet.cu).
 struct ConvScratch {
-  uint32_t* root = nullptr;   // BFS: smallest root index reaching the cell
-  uint32_t* level = nullptr;  // BFS level (Chebyshev distance to a valid cell)
-  uint32_t* fa = nullptr;     // frontier ping-pong
-  uint32_t* fb = nullptr;
-  uint32_t* cnt = nullptr;    // level sizes (3 rotating counters)
+  uint32_t* sat = nullptr;       // summed-area table of the validity mask
+  uint32_t* next_col = nullptr;  // per row: next valid column >= c
+  uint32_t* next_row = nullptr;  // per column: next valid row >= r
   double* va = nullptr;       // layer activations ping-pong
   double* vb = nullptr;
   double* weights = nullptr;    // all layers' kernels, concatenated
   double* h_weights = nullptr;  // pinned staging copy
   std::size_t cap = 0, wcap = 0;
-  int bfs_blocks = 0;
   cudaEvent_t upload_done = nullptr;
   void ensure(std::size_t n, std::size_t n_weights);
   void release();
