@@ -106,6 +106,52 @@ RELIEF_API relief_status relief_gpu_convnet_infer(const relief_config* config, c
                                                   const uint8_t* valid, int width, int height,
                                                   double* out);
 
+/* ---- Exact point-batch sharding of one frame -----------------
+ * Every rank (one process per GPU) keeps a full replica of the map and feeds
+ * its contiguous batch [ray_offset, ray_offset + n_local) of the frame's
+ * n_total points (scan order). Per frame, in order:
+ *   1. relief_gpu_shard_ingest  -> io: n_records, drift[2], counters[3] (host);
+ *      rec_cell / rec_z / rec_var (device, n_records, scan order).
+ *      Exchange: all-gather drift pairs and records in rank order, sum counters.
+ *   2. relief_gpu_shard_update(all ranks' drift pairs, all records) -> fusion of
+ *      every cell (identical on all ranks) + ray pass 1 over the local rays;
+ *      io.kstar / io.upper_bound / io.upper_bound_valid (device, cells).
+ *      Exchange: all-reduce MIN kstar, MIN upper_bound, MAX upper_bound_valid.
+ *   3. relief_gpu_shard_remove -> removal + ray pass 2 over the local rays;
+ *      *removed (identical on all ranks). If > 0, exchange again:
+ *      all-reduce MIN upper_bound, MAX upper_bound_valid.
+ *   4. relief_gpu_shard_finish(summed counters, n_total) -> cell phases, stats.
+ * The result equals relief_map_integrate of the whole frame on one GPU (bit for
+ * bit; with drift enabled the offset is the ranks' partial sums added in rank
+ * order, so heights agree to the drift tolerance). Device pointers stay valid
+ * until the next integrate / shard call on the map. */
+typedef struct relief_gpu_shard_io {
+  int64_t n_records;
+  double drift[2];       /* local drift vote: sum, count */
+  int64_t counters[3];   /* local points_out_of_range, points_excluded, points_out_of_map */
+  uint32_t* rec_cell;
+  double* rec_z;
+  double* rec_var;
+  int32_t* kstar;
+  double* upper_bound;
+  uint8_t* upper_bound_valid;
+  size_t cells;
+} relief_gpu_shard_io;
+
+RELIEF_API relief_status relief_gpu_shard_ingest(relief_map* map, const relief_config* config,
+                                                 const double* xyz, size_t n_local,
+                                                 int xyz_on_device, uint64_t ray_offset,
+                                                 uint64_t n_total, const double pose[12],
+                                                 double stamp, relief_gpu_shard_io* io);
+RELIEF_API relief_status relief_gpu_shard_update(relief_map* map, const double* drift_pairs,
+                                                 int n_ranks, const uint32_t* rec_cell,
+                                                 const double* rec_z, const double* rec_var,
+                                                 size_t n_records, relief_gpu_shard_io* io);
+RELIEF_API relief_status relief_gpu_shard_remove(relief_map* map, int64_t* removed,
+                                                 relief_gpu_shard_io* io);
+RELIEF_API relief_status relief_gpu_shard_finish(relief_map* map, const int64_t counters_total[3],
+                                                 uint64_t points_total, relief_scan_stats* stats);
+
 /* Synthetic scan: scene + sensor of a reliefmap config file, rendered from
  * pose (row-major [R|t]) at `time` with splitmix64 stream (seed, scan_index)
  * per ray. Returns the point count (only min(count, capacity) points are

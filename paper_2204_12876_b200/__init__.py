@@ -104,6 +104,14 @@ RELIEF_H_SIGNATURES = {
 }
 
 # Additive relief_gpu.h symbols.
+class ShardIO(ctypes.Structure):
+    """relief_gpu_shard_io (include/relief_gpu.h)."""
+    _fields_ = [("n_records", ctypes.c_int64), ("drift", ctypes.c_double * 2), ("counters", ctypes.c_int64 * 3),
+                ("rec_cell", ctypes.c_void_p), ("rec_z", ctypes.c_void_p), ("rec_var", ctypes.c_void_p),
+                ("kstar", ctypes.c_void_p), ("upper_bound", ctypes.c_void_p),
+                ("upper_bound_valid", ctypes.c_void_p), ("cells", ctypes.c_size_t)]
+
+
 RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_device_count": (_I, []),
     "relief_gpu_map_create_on": (_P, [_I, _D, _I, _I, _D, _D]),
@@ -123,6 +131,13 @@ RELIEF_GPU_H_SIGNATURES = {
                                      ctypes.POINTER(_I), _DP, _I, _DP, ctypes.POINTER(ctypes.c_uint8)]),
     "relief_gpu_config_load_convnet": (_I, [_P, _CS]),
     "relief_gpu_convnet_infer": (_I, [_P, _DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, _DP]),
+    "relief_gpu_shard_ingest": (_I, [_P, _P, ctypes.c_void_p, _SZ, _I, ctypes.c_uint64, ctypes.c_uint64, _DP, _D,
+                                     ctypes.c_void_p]),
+    "relief_gpu_shard_update": (_I, [_P, _DP, _I, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _SZ,
+                                     ctypes.c_void_p]),
+    "relief_gpu_shard_remove": (_I, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p]),
+    "relief_gpu_shard_finish": (_I, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.c_uint64,
+                                     ctypes.POINTER(ScanStats)]),
     "relief_gpu_sim_render": (ctypes.c_int64, [_CS, _DP, _D, ctypes.c_uint64, ctypes.c_uint64, _DP,
                                                ctypes.c_int64]),
 }

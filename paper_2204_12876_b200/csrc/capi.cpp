@@ -102,6 +102,20 @@ void validateScan(const rb200::PipelineParams& p, const rb200::Pose& pose) {
   else p.traversability.validate();
 }
 
+void exportShardIO(const rb200::ShardIO& s, relief_gpu_shard_io* io) {
+  io->n_records = s.n_records;
+  io->drift[0] = s.drift[0];
+  io->drift[1] = s.drift[1];
+  for (int k = 0; k < 3; ++k) io->counters[k] = s.counters[k];
+  io->rec_cell = s.rec_cell;
+  io->rec_z = s.rec_z;
+  io->rec_var = s.rec_var;
+  io->kstar = s.kstar;
+  io->upper_bound = s.ub;
+  io->upper_bound_valid = s.ubv;
+  io->cells = s.cells;
+}
+
 void fillStats(const rb200::ScanResult& r, relief_scan_stats* s) {
   if (s == nullptr) return;
   s->points_in = r.points_in;
@@ -422,6 +436,57 @@ relief_status relief_gpu_convnet_infer(const relief_config* config, const double
   return guard([&] {
     rb200::runHostConvnet(currentDevice(), config->config.pipeline.convnet, layer, valid, width,
                           height, out);
+  });
+}
+
+relief_status relief_gpu_shard_ingest(relief_map* map, const relief_config* config,
+                                      const double* xyz, size_t n_local, int xyz_on_device,
+                                      uint64_t ray_offset, uint64_t n_total, const double pose[12],
+                                      double stamp, relief_gpu_shard_io* io) {
+  if (map == nullptr || pose == nullptr || io == nullptr || (xyz == nullptr && n_local > 0))
+    return usage("null argument");
+  return guard([&] {
+    const rb200::Pose p = rb200::Pose::fromRowMajor34(pose);
+    const rb200::PipelineParams params = config ? config->config.pipeline : rb200::PipelineParams{};
+    validateScan(params, p);
+    rb200::ShardIO sio;
+    rb200::shardIngest(*map->dev, params, xyz, n_local, xyz_on_device != 0, ray_offset, n_total, p,
+                       stamp, sio);
+    exportShardIO(sio, io);
+  });
+}
+
+relief_status relief_gpu_shard_update(relief_map* map, const double* drift_pairs, int n_ranks,
+                                      const uint32_t* rec_cell, const double* rec_z,
+                                      const double* rec_var, size_t n_records,
+                                      relief_gpu_shard_io* io) {
+  if (map == nullptr || io == nullptr ||
+      (n_records > 0 && (rec_cell == nullptr || rec_z == nullptr || rec_var == nullptr)))
+    return usage("null argument");
+  return guard([&] {
+    rb200::ShardIO sio;
+    rb200::shardUpdate(*map->dev, drift_pairs, n_ranks, rec_cell, rec_z, rec_var, n_records, sio);
+    exportShardIO(sio, io);
+  });
+}
+
+relief_status relief_gpu_shard_remove(relief_map* map, int64_t* removed, relief_gpu_shard_io* io) {
+  if (map == nullptr || io == nullptr) return usage("null argument");
+  return guard([&] {
+    rb200::ShardIO sio;
+    const int64_t r = rb200::shardRemove(*map->dev, sio);
+    if (removed) *removed = r;
+    io->upper_bound = sio.ub;
+    io->upper_bound_valid = sio.ubv;
+  });
+}
+
+relief_status relief_gpu_shard_finish(relief_map* map, const int64_t counters_total[3],
+                                      uint64_t points_total, relief_scan_stats* stats) {
+  if (map == nullptr || counters_total == nullptr) return usage("null argument");
+  return guard([&] {
+    const rb200::ScanResult r = rb200::shardFinish(*map->dev, counters_total, points_total);
+    fillStats(r, stats);
   });
 }
 

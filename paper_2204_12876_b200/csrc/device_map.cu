@@ -185,8 +185,8 @@ void ensurePointCapacity(DeviceMap& m, std::size_t n) {
   while (cap < n) cap <<= 1;
   cudaFree(m.pslab);
   m.pslab = nullptr;
-  const std::size_t bytes = alignUp(cap * 24) + 6 * alignUp(cap * 8) + 5 * alignUp(cap * 4) +
-                            alignUp(cap) + 8 * kAlign;
+  const std::size_t bytes = alignUp(cap * 24) + 8 * alignUp(cap * 8) + 6 * alignUp(cap * 4) +
+                            alignUp(cap) + 16 * kAlign;
   checkCuda(cudaMalloc(&m.pslab, bytes), "point scratch allocation");
   Carver c{static_cast<char*>(m.pslab)};
   m.xyz_in = c.take<double>(cap * 3);
@@ -202,6 +202,9 @@ void ensurePointCapacity(DeviceMap& m, std::size_t n) {
   m.val1 = c.take<uint32_t>(cap);
   m.raylist = c.take<uint32_t>(cap);
   m.kept = c.take<uint8_t>(cap);
+  m.rec_cell = c.take<uint32_t>(cap);
+  m.rec_z = c.take<double>(cap);
+  m.rec_var = c.take<double>(cap);
   m.cap = cap;
 }
 

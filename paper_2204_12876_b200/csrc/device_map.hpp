@@ -92,6 +92,21 @@ struct ConvScratch {
   void release();
 };
 
+// Cross-call state of a sharded frame (pipeline.cu, relief_gpu_shard_*).
+struct ShardState {
+  int stage = 0;  // 0 idle, 1 ingested, 2 updated, 3 removed
+  PipelineParams params;
+  Pose pose;
+  double stamp = 0.0, dt = 0.0;
+  std::size_t n_local = 0;
+  uint32_t ray_base = 0;
+  bool overlap = false;
+  long long launches = 0;
+  double drift_offset = 0.0;
+  int drift_n = 0;
+  bool drift_clamped = false;
+};
+
 struct DeviceMap {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -121,11 +136,16 @@ struct DeviceMap {
   uint32_t* val1 = nullptr;
   uint32_t* raylist = nullptr;
   uint8_t* kept = nullptr;
+  uint32_t* rec_cell = nullptr;  // sharded frames: this batch's fusion records
+  double* rec_z = nullptr;
+  double* rec_var = nullptr;
   // reduction scratch
   void* rslab = nullptr;
   std::size_t rcap = 0;
   double* drift_sum_part = nullptr;
   int* drift_n_part = nullptr;
+  uint32_t* blk = nullptr;        // compaction block counts / offsets (+1: total)
+  double* drift_local = nullptr;  // [2] local drift vote of a sharded batch
   uint32_t* hist = nullptr;
   uint32_t* scan_part = nullptr;
   std::size_t hist_cap = 0;
@@ -138,6 +158,7 @@ struct DeviceMap {
   double* export_buf = nullptr;  // masked-layer staging for get_layer
   ChainScratch chain;            // post-processing chain scratch
   ConvScratch conv;              // conv-net traversability scratch
+  ShardState shard;              // sharded-frame bookkeeping
   double* chain_in = nullptr;    // masked input layer of the chain
   double* chain_out = nullptr;   // chain output staging for host callers
   uint8_t* chain_out_ok = nullptr;
@@ -180,6 +201,29 @@ struct ScanResult {
 ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& params, const double* xyz,
                                std::size_t n, bool xyz_on_device, const Pose& pose,
                                double stamp, double dt);
+
+// Exact point-batch sharding of one frame: every rank holds a
+// full replica and runs its contiguous batch of the frame's points; the host
+// exchanges the buffers named in ShardIO between the phases (pipeline.cu).
+struct ShardIO {
+  int64_t n_records = 0;      // this batch's in-map kept points
+  double drift[2] = {0, 0};   // local drift vote (sum, count)
+  int64_t counters[3] = {0, 0, 0};  // local out_of_range, excluded, out_of_map
+  uint32_t* rec_cell = nullptr;     // device, n_records (scan order)
+  double* rec_z = nullptr;
+  double* rec_var = nullptr;
+  int32_t* kstar = nullptr;   // device, cells: first removing ray per cell
+  double* ub = nullptr;       // device, cells: upper-bound layer
+  uint8_t* ubv = nullptr;     // device, cells: upper-bound validity
+  std::size_t cells = 0;
+};
+void shardIngest(DeviceMap& m, const PipelineParams& params, const double* xyz, std::size_t n,
+                 bool xyz_on_device, uint64_t ray_offset, uint64_t n_total, const Pose& pose,
+                 double stamp, ShardIO& io);
+void shardUpdate(DeviceMap& m, const double* drift_pairs, int n_ranks, const uint32_t* d_cells,
+                 const double* d_z, const double* d_var, std::size_t n_records, ShardIO& io);
+int64_t shardRemove(DeviceMap& m, ShardIO& io);
+ScanResult shardFinish(DeviceMap& m, const int64_t counters_total[3], uint64_t points_total);
 
 // Post-processing chain on a masked layer held in device memory (postchain.cu).
 struct ChainStep {

@@ -59,6 +59,28 @@ __device__ __forceinline__ void countTileDigit(uint32_t* tc, uint32_t pitch, uin
   if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&tc[slot], __popc(peers));
 }
 
+// Exclusive scan over a kThreads block; *total = block sum.
+__device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t s_warp[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) wpre += s_warp[w];
+    tot += s_warp[w];
+  }
+  __syncthreads();
+  *total = tot;
+  return wpre + incl - v;
+}
+
 // Invalidate one cell (reference grid.cpp:126-137).
 __device__ __forceinline__ void invalidateCell(const Layers& L, size_t i) {
   L.valid[i] = 0;
@@ -133,7 +155,7 @@ __global__ void __launch_bounds__(kThreads)
              double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
              uint8_t* __restrict__ kept, double* __restrict__ drift_part,
              int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
-             uint32_t dmask, DevStats* st) {
+             uint32_t dmask, int count_cells, DevStats* st) {
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   int oor = 0, exc = 0, oom = 0, dn = 0;
@@ -178,11 +200,14 @@ __global__ void __launch_bounds__(kThreads)
     key[k] = cell;
     kept[k] = keep ? 1 : 0;
   }
-  // Per-cell point count, one atomic per run of equal cells in the warp.
-  const unsigned peers = __match_any_sync(0xffffffffu, cell);
-  if (cell < WH && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
-  // First radix pass's tile digit counts (K2).
-  countTileDigit(tc0, pitch, cell & dmask, k / kTile, cell < WH);
+  // Per-cell point count, one atomic per run of equal cells in the warp, and
+  // the first radix pass's tile digit counts (K2). A sharded frame counts the
+  // gathered records instead (k_records_count).
+  if (count_cells) {
+    const unsigned peers = __match_any_sync(0xffffffffu, cell);
+    if (cell < WH && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
+    countTileDigit(tc0, pitch, cell & dmask, k / kTile, cell < WH);
+  }
 
   // Fixed-shape block reduction: deterministic drift partial per block.
   __shared__ double s_sum[kThreads / 32];
@@ -273,6 +298,108 @@ __global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, c
   }
 }
 
+// Drift offset known on the host (sharded frames: the ranks' votes summed in
+// rank order).
+__global__ void __launch_bounds__(kThreads) k_apply_offset_value(Layers L, size_t n, double off) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (L.valid[i]) L.elev[i] += off;
+    if (L.ubv[i]) L.ub[i] += off;
+  }
+}
+
+// Local drift vote of a sharded batch: the same fixed-shape reduction as
+// k_drift_finalize, reported instead of applied.
+__global__ void __launch_bounds__(1024)
+    k_drift_local(const double* part, const int* npart, int nblocks, double* out) {
+  __shared__ double s_sum[32];
+  __shared__ long long s_cnt[32];
+  double sum = 0.0;
+  long long c = 0;
+  for (int b = threadIdx.x; b < nblocks; b += 1024) {
+    sum += part[b];
+    c += npart[b];
+  }
+  sum = warpSum(sum);
+  c = warpSum(c);
+  if ((threadIdx.x & 31) == 0) {
+    s_sum[threadIdx.x >> 5] = sum;
+    s_cnt[threadIdx.x >> 5] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = s_sum[0];
+    long long cnt = s_cnt[0];
+    for (int w = 1; w < 32; ++w) {
+      total += s_sum[w];
+      cnt += s_cnt[w];
+    }
+    out[0] = total;
+    out[1] = static_cast<double>(cnt);
+  }
+}
+
+// Stable compaction of a batch's in-map kept points into fusion records
+// (cell, p_z, sigma_p^2) in scan order: per-1024-point block counts, one
+// block scan of the counts, then the write.
+constexpr int kCompact = 1024;
+__global__ void __launch_bounds__(kCompact)
+    k_compact_count(const uint32_t* __restrict__ key, uint32_t n, uint32_t WH,
+                    uint32_t* __restrict__ blk) {
+  const uint32_t i = blockIdx.x * kCompact + threadIdx.x;
+  const int c = __syncthreads_count(i < n && key[i] < WH);
+  if (threadIdx.x == 0) blk[blockIdx.x] = static_cast<uint32_t>(c);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_compact_scan(uint32_t* blk, uint32_t nblk, uint32_t* total) {
+  uint32_t carry = 0;
+  for (uint32_t b0 = 0; b0 < nblk; b0 += kThreads) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint32_t v = b < nblk ? blk[b] : 0u;
+    uint32_t tot;
+    const uint32_t ex = blockExclusiveScan(v, &tot);
+    if (b < nblk) blk[b] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(kCompact)
+    k_compact_write(const uint32_t* __restrict__ key, const double* __restrict__ pz,
+                    const double* __restrict__ pvar, uint32_t n, uint32_t WH,
+                    const uint32_t* __restrict__ blk_off, uint32_t* __restrict__ rcell,
+                    double* __restrict__ rz, double* __restrict__ rvar) {
+  __shared__ uint32_t s_warp[kCompact / 32];
+  const uint32_t i = blockIdx.x * kCompact + threadIdx.x;
+  const bool keep = i < n && key[i] < WH;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  if (lane == 0) s_warp[warp] = __popc(mask);
+  __syncthreads();
+  uint32_t base = blk_off[blockIdx.x];
+  for (unsigned w = 0; w < warp; ++w) base += s_warp[w];
+  if (keep) {
+    const uint32_t pos = base + __popc(mask & ((1u << lane) - 1u));
+    rcell[pos] = key[i];
+    rz[pos] = pz[i];
+    rvar[pos] = pvar[i];
+  }
+}
+
+// Per-cell counts and the first radix pass's tile digit counts of the
+// gathered records of a sharded frame (the records are the sort's input).
+__global__ void __launch_bounds__(kThreads)
+    k_records_count(const uint32_t* __restrict__ rcell, uint32_t m, int32_t* __restrict__ count,
+                    uint32_t* __restrict__ tc0, uint32_t pitch, uint32_t dmask) {
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  const bool ok = k < m;
+  const uint32_t cell = ok ? rcell[k] : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, cell);
+  if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
+  countTileDigit(tc0, pitch, cell & dmask, k / kTile, ok);
+}
+
 // ------------------------------------------------ K2 stable radix sort
 // LSD radix sort of the in-map kept points by cell, carrying the point index,
 // reduce-then-scan style so that no tile waits on another:
@@ -300,26 +427,6 @@ struct SortGeom {
   }
 };
 
-__device__ __forceinline__ uint32_t blockExclusiveScan(uint32_t v, uint32_t* total) {
-  __shared__ uint32_t s_warp[kThreads / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  uint32_t wpre = 0, tot = 0;
-  for (int w = 0; w < kThreads / 32; ++w) {
-    if (w < warp) wpre += s_warp[w];
-    tot += s_warp[w];
-  }
-  __syncthreads();
-  *total = tot;
-  return wpre + incl - v;
-}
 
 // Row d of tc -> exclusive offsets within the digit; rowsum[d] = row total.
 __global__ void __launch_bounds__(kThreads)
@@ -981,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
-                 DevStats* st, int retry) {
+                 DevStats* st, int retry, uint32_t ray_base) {
   if (retry && !st->respeculate) return;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   bool touched = false;
@@ -989,7 +1096,7 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
   if (k < n && kept[k]) {
     const double ex = px[k], ey = py[k], ez = pz[k];
     Pass1Ctx c{cls, L, kstar, a.o[2], ez - a.o[2], ex - a.o[0], ey - a.o[1], a.alpha_n,
-               static_cast<int32_t>(k)};
+               static_cast<int32_t>(ray_base + k)};  // global ray id (sharded frames)
     if (isfinite(c.vx) && isfinite(c.vy)) {
       pass1Finite(a.g, a.o, ex, ey, c, touched, visits);
     } else {
@@ -1035,7 +1142,8 @@ __global__ void __launch_bounds__(kThreads)
     k_rays_pass2(const uint32_t* __restrict__ raylist, const DevStats* st_in,
                  const double* __restrict__ px, const double* __restrict__ py,
                  const double* __restrict__ pz, RayArgs a, Layers L,
-                 const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar) {
+                 const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar,
+                 uint32_t ray_base) {
   if (st_in->removed == 0) return;
   const unsigned total = static_cast<unsigned>(st_in->candidate_rays);
   for (unsigned q = blockIdx.x * kThreads + threadIdx.x; q < total; q += gridDim.x * kThreads) {
@@ -1043,7 +1151,7 @@ __global__ void __launch_bounds__(kThreads)
     const double dz = pz[k] - a.o[2];
     walk(a.g, a.o, px[k], py[k], [&](uint32_t c, double te, double tn, bool vertical) {
       if (cls[c] != kClsCandidate) return;
-      if (kstar[c] > static_cast<int32_t>(k)) return;
+      if (kstar[c] > static_cast<int32_t>(ray_base + k)) return;
       boundMin(L, c, rayHeight(a.o[2], dz, te, tn, vertical));
     });
   }
@@ -1187,245 +1295,284 @@ int quantizedShift(double d, double res) {
 }  // namespace
 
 // ------------------------------------------------------------------ host
-ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const double* xyz,
-                               std::size_t n, bool xyz_on_device, const Pose& pose,
-                               double stamp, double dt) {
-  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
-  if (n >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
-  cudaStream_t s = m.stream;
+namespace {
+
+// One frame's launch context. The single-call path (integrateScanDevice) and
+// the sharded path (shard*) run the same phase functions in the same order.
+struct Frame {
+  DeviceMap& m;
+  const PipelineParams& P;
+  Pose pose;
+  double stamp, dt;
+  cudaStream_t s;
+  std::size_t ncell;
+  uint32_t WH;
+  GridArgs g;
   long long launches = 0;
-  const std::size_t ncell = m.grid.cells();
-  const uint32_t N = static_cast<uint32_t>(n);
+  bool overlap = false;  // heavy cells folded on stream2 during the ray pass
+  int heavy = INT_MAX;
+  Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
+      : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
+        WH(static_cast<uint32_t>(map.grid.cells())) {}
+};
 
-  checkCuda(cudaEventRecord(m.ev[0], s), "event");
-  checkCuda(cudaMemsetAsync(m.stats, 0, sizeof(DevStats), s), "memset");
-
-  // move_to: recenter by whole cells (reference grid.cpp:87-111).
-  const int sx = quantizedShift(pose.t[0] - m.grid.center_x, m.grid.resolution);
-  const int sy = quantizedShift(pose.t[1] - m.grid.center_y, m.grid.resolution);
+// Stats reset + move_to (reference grid.cpp:87-111).
+void phaseBegin(Frame& f) {
+  DeviceMap& m = f.m;
+  checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
+  checkCuda(cudaMemsetAsync(m.stats, 0, sizeof(DevStats), f.s), "memset");
+  const int sx = quantizedShift(f.pose.t[0] - m.grid.center_x, m.grid.resolution);
+  const int sy = quantizedShift(f.pose.t[1] - m.grid.center_y, m.grid.resolution);
   if (sx != 0 || sy != 0) {
     m.grid.center_x += sx * m.grid.resolution;
     m.grid.center_y += sy * m.grid.resolution;
-    k_shift<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, m.alt, m.grid.width, m.grid.height, sx, sy);
-    ++launches;
+    k_shift<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, m.alt, m.grid.width, m.grid.height, sx, sy);
+    ++f.launches;
     std::swap(m.cur, m.alt);
   }
-  const GridArgs g = gridArgs(m.grid);
+  f.g = gridArgs(m.grid);
+}
 
-  // Input stream into HBM.
-  const double* d_xyz = xyz;
-  if (n > 0) {
-    ensurePointCapacity(m, n);
-    const std::size_t nb = gridFor(n);
-    if (m.rcap < nb || m.rslab == nullptr) {
-      cudaFree(m.rslab);
-      m.rslab = nullptr;
-      m.rcap = std::max<std::size_t>(nb, 1024);
-      checkCuda(cudaMalloc(&m.rslab, m.rcap * (sizeof(double) + sizeof(int)) + 512), "reduce scratch");
-      m.drift_sum_part = static_cast<double*>(m.rslab);
-      m.drift_n_part = reinterpret_cast<int*>(m.drift_sum_part + m.rcap);
-    }
-    if (!xyz_on_device) {
-      checkCuda(cudaMemcpyAsync(m.xyz_in, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, s),
-                "point upload");
-      d_xyz = m.xyz_in;
-    }
+// Point scratch + the input stream into HBM; returns the device points.
+const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_device) {
+  DeviceMap& m = f.m;
+  if (n == 0) return xyz;
+  ensurePointCapacity(m, n);
+  const std::size_t nb = gridFor(n);
+  if (m.rcap < nb || m.rslab == nullptr) {
+    cudaFree(m.rslab);
+    m.rslab = nullptr;
+    m.rcap = std::max<std::size_t>(nb, 1024);
+    checkCuda(cudaMalloc(&m.rslab, m.rcap * (sizeof(double) + sizeof(int) + sizeof(uint32_t)) + 1024),
+              "reduce scratch");
+    m.drift_sum_part = static_cast<double*>(m.rslab);
+    m.drift_n_part = reinterpret_cast<int*>(m.drift_sum_part + m.rcap);
+    m.blk = reinterpret_cast<uint32_t*>(m.drift_n_part + m.rcap);
+    m.drift_local = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(m.blk + m.rcap + 1) + 255) & ~static_cast<uintptr_t>(255));
   }
-  checkCuda(cudaMemsetAsync(m.count, 0, ncell * sizeof(int32_t), s), "memset");
-  // K2 geometry: 1-3 LSD passes over the bits of the cell id; tile digit
-  // counts are accumulated from K1 on, so they are zeroed here.
-  const uint32_t WH = static_cast<uint32_t>(ncell);
+  if (on_device) return xyz;
+  checkCuda(cudaMemcpyAsync(m.xyz_in, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, f.s),
+            "point upload");
+  return m.xyz_in;
+}
+
+// K2 geometry for N keys: 1-3 LSD passes over the bits of the cell id. The
+// tile digit counts are accumulated upstream, so they are zeroed here.
+SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
+  DeviceMap& m = f.m;
   SortGeom sg;
-  if (n > 0) {
-    const int bits = 32 - __builtin_clz(WH);
-    sg.passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
-    sg.dbits = (bits + sg.passes - 1) / sg.passes;
-    sg.ntiles = (N + kTile - 1) / kTile;
-    sg.pitch = (sg.ntiles + 3) & ~3u;
-    const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
-    const std::size_t need = tcn + static_cast<std::size_t>(sg.passes) * sg.buckets();
-    if (m.hist_cap < need) {
-      cudaFree(m.hist);
-      m.hist = nullptr;
-      m.hist_cap = need;
-      checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
-    }
-    sg.tc = m.hist;
-    sg.rowsum = m.hist + tcn;
-    checkCuda(cudaMemsetAsync(sg.tc, 0, tcn * sizeof(uint32_t), s), "memset");
+  if (N == 0) return sg;
+  const int bits = 32 - __builtin_clz(f.WH);
+  sg.passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
+  sg.dbits = (bits + sg.passes - 1) / sg.passes;
+  sg.ntiles = (N + kTile - 1) / kTile;
+  sg.pitch = (sg.ntiles + 3) & ~3u;
+  const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
+  const std::size_t need = tcn + static_cast<std::size_t>(sg.passes) * sg.buckets();
+  if (m.hist_cap < need) {
+    cudaFree(m.hist);
+    m.hist = nullptr;
+    m.hist_cap = need;
+    checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
   }
-  checkCuda(cudaEventRecord(m.ev[1], s), "event");  // upload done
+  sg.tc = m.hist;
+  sg.rowsum = m.hist + tcn;
+  checkCuda(cudaMemsetAsync(sg.tc, 0, tcn * sizeof(uint32_t), f.s), "memset");
+  return sg;
+}
 
-  // K1 ingest.
-  const UpdateParams& U = P.update;
-  if (n > 0) {
-    IngestArgs ia;
-    ia.g = g;
-    for (int r = 0; r < 3; ++r) {
-      for (int c = 0; c < 3; ++c) ia.R[3 * r + c] = pose.R[r][c];
-      ia.t[r] = pose.t[r];
-    }
-    ia.max_range2 = U.max_range * U.max_range;
-    ia.excl_enabled = U.exclusion.enabled;
-    ia.excl_b = U.exclusion.b;
-    ia.excl_c = U.exclusion.c;
-    ia.excl_dmax = U.exclusion.d_max;
-    ia.excl_tan = std::tan(U.exclusion.theta_a);  // host libm, as the reference
-    ia.alpha_d = U.noise.alpha_d;
-    ia.sigma_p_min2 = U.noise.sigma_p_min2;
-    ia.drift_enabled = P.drift.enabled;
-    ia.drift_thr = P.drift.traversability_threshold;
-    k_ingest<<<gridFor(n), kThreads, 0, s>>>(d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz,
-                                             m.pvar, m.key0, m.kept, m.drift_sum_part,
-                                             m.drift_n_part, sg.tc, sg.pitch,
-                                             sg.buckets() - 1, m.stats);
-    ++launches;
+// K1 (reference integration.cpp:85-140, sensing.cpp:32-41, drift.cpp:24-42).
+void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, bool count_cells) {
+  if (N == 0) return;
+  DeviceMap& m = f.m;
+  const UpdateParams& U = f.P.update;
+  IngestArgs ia;
+  ia.g = f.g;
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) ia.R[3 * r + c] = f.pose.R[r][c];
+    ia.t[r] = f.pose.t[r];
   }
-  checkCuda(cudaEventRecord(m.ev[2], s), "event");  // ingest done
+  ia.max_range2 = U.max_range * U.max_range;
+  ia.excl_enabled = U.exclusion.enabled;
+  ia.excl_b = U.exclusion.b;
+  ia.excl_c = U.exclusion.c;
+  ia.excl_dmax = U.exclusion.d_max;
+  ia.excl_tan = std::tan(U.exclusion.theta_a);  // host libm, as the reference
+  ia.alpha_d = U.noise.alpha_d;
+  ia.sigma_p_min2 = U.noise.sigma_p_min2;
+  ia.drift_enabled = f.P.drift.enabled;
+  ia.drift_thr = f.P.drift.traversability_threshold;
+  k_ingest<<<gridFor(N), kThreads, 0, f.s>>>(d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz, m.pvar,
+                                             m.key0, m.kept, m.drift_sum_part, m.drift_n_part,
+                                             sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0,
+                                             m.stats);
+  ++f.launches;
+}
 
-  // Drift compensation.
-  if (n > 0 && P.drift.enabled) {
-    k_drift_finalize<<<1, 1024, 0, s>>>(m.drift_sum_part, m.drift_n_part,
-                                        static_cast<int>(gridFor(n)), P.drift.min_points,
-                                        P.drift.max_offset_per_scan, m.drift_offset, m.stats);
-    k_apply_offset<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, m.drift_offset);
-    launches += 2;
+// K2 over N keys (cells; >= WH = not sorted) with payload (z, var) indexed
+// by key position; then K3 gated fusion. Long cells go to stream2 when the
+// ray pass can overlap them.
+void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, const double* var,
+                   const SortGeom& sg) {
+  DeviceMap& m = f.m;
+  cudaStream_t s = f.s;
+  checkCuda(cudaMemsetAsync(m.start, 0xff, f.ncell * sizeof(uint32_t), s), "memset");
+  const std::size_t sc_smem = 20 * static_cast<std::size_t>(sg.buckets());
+  const uint32_t* kin = keys;
+  uint32_t *kout = m.key1, *vin = m.val0, *vout = m.val1;
+  for (int p = 0; p < sg.passes; ++p) {
+    k_sort_rowscan<<<sg.buckets(), kThreads, 0, s>>>(sg.counts(p), sg.pitch,
+                                                     sg.rowsum + p * sg.buckets());
+    k_sort_scatter<<<sg.ntiles, kThreads, sc_smem, s>>>(kin, vin, N, p, sg, f.WH, kout, vout, z, var,
+                                                        m.spz, m.spv, m.start);
+    f.launches += 2;
+    // ping-pong between key1 and key0 (key0 is free once pass 0 has read it)
+    const uint32_t* next_in = kout;
+    kout = (kout == m.key1) ? m.key0 : m.key1;
+    kin = next_in;
+    std::swap(vin, vout);
   }
-  checkCuda(cudaEventRecord(m.ev[3], s), "event");  // drift done
+  checkCuda(cudaEventRecord(m.ev[4], s), "event");  // sort done
 
-  if (n > 0) {
-    // K2: stable sort of point indices by cell, then segment starts.
-    checkCuda(cudaMemsetAsync(m.start, 0xff, ncell * sizeof(uint32_t), s), "memset");
-    const std::size_t sc_smem = 20 * static_cast<std::size_t>(sg.buckets());
-    uint32_t *kin = m.key0, *kout = m.key1, *vin = m.val0, *vout = m.val1;
-    for (int p = 0; p < sg.passes; ++p) {
-      k_sort_rowscan<<<sg.buckets(), kThreads, 0, s>>>(sg.counts(p), sg.pitch,
-                                                       sg.rowsum + p * sg.buckets());
-      k_sort_scatter<<<sg.ntiles, kThreads, sc_smem, s>>>(kin, vin, N, p, sg, WH, kout, vout,
-                                                          m.pz, m.pvar, m.spz, m.spv, m.start);
-      launches += 2;
-      std::swap(kin, kout);
-      std::swap(vin, vout);
-    }
-    // spz / spv now hold (p_z, sigma_p^2) sorted by (cell, scan order); start[c]
-    // is the first sorted position of cell c (cells with points).
-    checkCuda(cudaEventRecord(m.ev[4], s), "event");  // sort done
+  const UpdateParams& U = f.P.update;
+  FuseArgs fa;
+  fa.now = f.stamp;
+  fa.sigma_init2 = U.sigma_init2;
+  fa.sigma_outlier2 = U.sigma_outlier2;
+  fa.sigma_max2 = U.sigma_max2;
+  fa.maha = U.mahalanobis_threshold;
+  fa.maha2 = U.mahalanobis_threshold * U.mahalanobis_threshold;
+  fa.wall = U.wall_count_threshold;
+  const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
+  f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
+  f.heavy = f.overlap ? kHeavyCell : INT_MAX;
+  k_fuse<<<gridFor(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
+                                               m.stats, f.heavy, m.heavy);
+  ++f.launches;
+  if (f.overlap) {
+    checkCuda(cudaEventRecord(m.ev[10], s), "event");
+    checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
+    k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.stats, m.start, m.spz,
+                                                      m.spv, fa, m.stats, f.P.cleanup.t_free, cleanup,
+                                                      bound);
+    ++f.launches;
+    checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
+  }
+  checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done (short cells when overlapped)
+}
 
-    // K3 gated fusion.
-    FuseArgs fa;
-    fa.now = stamp;
-    fa.sigma_init2 = U.sigma_init2;
-    fa.sigma_outlier2 = U.sigma_outlier2;
-    fa.sigma_max2 = U.sigma_max2;
-    fa.maha = U.mahalanobis_threshold;
-    fa.maha2 = U.mahalanobis_threshold * U.mahalanobis_threshold;
-    fa.wall = U.wall_count_threshold;
-    // Short cells here; cells with more than kHeavyCell points fold on the side
-    // stream while the ray pass runs (needs: a ray pass, and cells fused this
-    // scan being class "none", i.e. t_free >= 0 when cleanup is on).
-    const bool cleanup = P.cleanup.cleanup_enabled, bound = P.cleanup.upper_bound_enabled;
-    const bool overlap = (cleanup || bound) && (!cleanup || P.cleanup.t_free >= 0.0);
-    const int heavy = overlap ? kHeavyCell : INT_MAX;
-    k_fuse<<<gridFor(ncell), kThreads, 0, s>>>(m.cur, ncell, m.count, m.start, m.spz, m.spv, fa,
-                                               m.stats, heavy, m.heavy);
-    ++launches;
-    if (overlap) {
-      checkCuda(cudaEventRecord(m.ev[10], s), "event");
-      checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
-      k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.stats, m.start,
-                                                        m.spz, m.spv, fa, m.stats,
-                                                        P.cleanup.t_free, cleanup, bound);
-      ++launches;
-      checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
-    }
-    checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done (short cells when overlapped)
+RayArgs rayArgs(const Frame& f) {
+  RayArgs ra;
+  ra.g = f.g;
+  for (int i = 0; i < 3; ++i) ra.o[i] = f.pose.t[i];
+  ra.now = f.stamp;
+  ra.t_free = f.P.cleanup.t_free;
+  ra.alpha_n = f.P.cleanup.alpha_n;
+  ra.cleanup = f.P.cleanup.cleanup_enabled;
+  ra.bound = f.P.cleanup.upper_bound_enabled;
+  return ra;
+}
 
-    // K5/K6 ray casting.
-    if (cleanup || bound) {
-      RayArgs ra;
-      ra.g = g;
-      for (int i = 0; i < 3; ++i) ra.o[i] = pose.t[i];
-      ra.now = stamp;
-      ra.t_free = P.cleanup.t_free;
-      ra.alpha_n = P.cleanup.alpha_n;
-      ra.cleanup = cleanup;
-      ra.bound = bound;
-      k_classify<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, ra, m.cls, m.kstar, m.count,
-                                                        overlap ? heavy : -1, 0, m.stats);
-      k_rays_pass1<<<gridFor(n), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 0);
-      launches += 2;
-      if (overlap) {
-        // Join the long-cell fold; redo the ray pass only if a heavy cell fused
-        // nothing (both kernels return immediately otherwise).
-        checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
-        k_classify<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, ra, m.cls, m.kstar, m.count,
-                                                          -1, 1, m.stats);
-        k_rays_pass1<<<gridFor(n), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                     m.kstar, m.raylist, m.stats, 1);
-        launches += 2;
-      }
-      if (cleanup) {
-        k_remove<<<streamGrid(ncell), kThreads, 0, s>>>(m.cur, ncell, m.kstar, m.stats);
-        ++launches;
-        if (bound) {
-          k_rays_pass2<<<148 * 8, kThreads, 0, s>>>(m.raylist, m.stats, m.px, m.py, m.pz, ra,
-                                                     m.cur, m.cls, m.kstar);
-          ++launches;
-        }
-      }
+// K5 pass 1 over this process's rays (ids ray_base + k), joined with the
+// long-cell fold (and redone if a speculated class was wrong).
+void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
+  DeviceMap& m = f.m;
+  cudaStream_t s = f.s;
+  const RayArgs ra = rayArgs(f);
+  if (ra.cleanup || ra.bound) {
+    k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
+                                                        f.overlap ? f.heavy : -1, 0, m.stats);
+    ++f.launches;
+    if (N > 0) {
+      k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+                                                   m.kstar, m.raylist, m.stats, 0, ray_base);
+      ++f.launches;
     }
   }
-  if (n == 0) {
-    checkCuda(cudaEventRecord(m.ev[4], s), "event");
-    checkCuda(cudaEventRecord(m.ev[5], s), "event");
+  if (f.overlap) {
+    // Join the long-cell fold; redo the ray pass only if a heavy cell fused
+    // nothing (both kernels return immediately otherwise).
+    checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
+    k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
+                                                        -1, 1, m.stats);
+    ++f.launches;
+    if (N > 0) {
+      k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+                                                   m.kstar, m.raylist, m.stats, 1, ray_base);
+      ++f.launches;
+    }
   }
-  checkCuda(cudaEventRecord(m.ev[6], s), "event");  // rays done
+}
 
-  // K7 cell phases + update_variance.
-  {
-    CellArgs ca;
-    ca.g = g;
-    ca.rx = pose.t[0];
-    ca.ry = pose.t[1];
-    ca.rz = pose.t[2];
-    ca.overlap = P.overlap.enabled;
-    ca.ov_r2 = P.overlap.radius * P.overlap.radius;
-    ca.ov_thr = P.overlap.height_threshold;
-    const TraversabilityParams& T = P.traversability;
-    ca.geo_trav = P.use_convnet_traversability ? 0 : 1;
-    ca.radius = ca.geo_trav ? T.window / 2 : 1;
-    ca.slope_max = T.slope_max;
-    ca.step_max = T.step_max;
-    ca.rough_max = T.roughness_max;
-    ca.w_slope = T.w_slope;
-    ca.w_step = T.w_step;
-    ca.w_rough = T.w_roughness;
-    ca.time_var = (dt != 0.0 && U.sigma_t2 != 0.0) ? 1 : 0;
-    ca.growth = U.sigma_t2 * (dt / U.nominal_update_period);
-    ca.sigma_max2 = U.sigma_max2;
-    const int halo = std::max(1, ca.radius);
-    const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
-    const dim3 grid((g.W + kTileX - 1) / kTileX, (g.H + kTileY - 1) / kTileY);
-    if (sm > 48 * 1024)
-      checkCuda(cudaFuncSetAttribute(k_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(sm)),
-                "smem attribute");
-    k_cells<<<grid, dim3(kTileX, kTileY), sm, s>>>(m.cur, m.count, ca, m.stats);
-    ++launches;
+// Removal of k* < inf cells, then K6 bounds of removed cells from this
+// process's queued rays k >= k*.
+void phaseRemovePass2(Frame& f, uint32_t ray_base) {
+  DeviceMap& m = f.m;
+  const RayArgs ra = rayArgs(f);
+  if (!ra.cleanup) return;
+  k_remove<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, m.kstar, m.stats);
+  ++f.launches;
+  if (ra.bound) {
+    k_rays_pass2<<<148 * 8, kThreads, 0, f.s>>>(m.raylist, m.stats, m.px, m.py, m.pz, ra, m.cur,
+                                                m.cls, m.kstar, ray_base);
+    ++f.launches;
   }
-  checkCuda(cudaEventRecord(m.ev[7], s), "event");  // cell phases done
+}
+
+// K7 cell phases + update_variance, then the conv-net filter when selected.
+void phaseCells(Frame& f) {
+  DeviceMap& m = f.m;
+  const UpdateParams& U = f.P.update;
+  CellArgs ca;
+  ca.g = f.g;
+  ca.rx = f.pose.t[0];
+  ca.ry = f.pose.t[1];
+  ca.rz = f.pose.t[2];
+  ca.overlap = f.P.overlap.enabled;
+  ca.ov_r2 = f.P.overlap.radius * f.P.overlap.radius;
+  ca.ov_thr = f.P.overlap.height_threshold;
+  const TraversabilityParams& T = f.P.traversability;
+  ca.geo_trav = f.P.use_convnet_traversability ? 0 : 1;
+  ca.radius = ca.geo_trav ? T.window / 2 : 1;
+  ca.slope_max = T.slope_max;
+  ca.step_max = T.step_max;
+  ca.rough_max = T.roughness_max;
+  ca.w_slope = T.w_slope;
+  ca.w_step = T.w_step;
+  ca.w_rough = T.w_roughness;
+  ca.time_var = (f.dt != 0.0 && U.sigma_t2 != 0.0) ? 1 : 0;
+  ca.growth = U.sigma_t2 * (f.dt / U.nominal_update_period);
+  ca.sigma_max2 = U.sigma_max2;
+  const int halo = std::max(1, ca.radius);
+  const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
+  const dim3 grid((f.g.W + kTileX - 1) / kTileX, (f.g.H + kTileY - 1) / kTileY);
+  if (sm > 48 * 1024)
+    checkCuda(cudaFuncSetAttribute(k_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(sm)),
+              "smem attribute");
+  k_cells<<<grid, dim3(kTileX, kTileY), sm, f.s>>>(m.cur, m.count, ca, m.stats);
+  ++f.launches;
+  checkCuda(cudaEventRecord(m.ev[7], f.s), "event");  // cell phases done
   // Conv-net traversability (reference integration.cpp:242-244): reads the
   // post-overlap elevation, writes the traversability of every cell.
-  if (P.use_convnet_traversability)
-    launches += convnetEnqueue(s, m.conv, m.cur.elev, m.cur.valid, g.W, g.H, P.convnet, m.cur.trav);
-  checkCuda(cudaEventRecord(m.ev[12], s), "event");  // traversability done
-  checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, s), "stats");
-  checkCuda(cudaGetLastError(), "kernel launch");
-  checkCuda(cudaStreamSynchronize(s), "integrate");
+  if (f.P.use_convnet_traversability)
+    f.launches += convnetEnqueue(f.s, m.conv, m.cur.elev, m.cur.valid, f.g.W, f.g.H, f.P.convnet,
+                                 m.cur.trav);
+  checkCuda(cudaEventRecord(m.ev[12], f.s), "event");  // traversability done
+}
 
-  const DevStats& d = *m.h_stats;
-  if (d.error_code == 1) fail(Err::kInvalidVariance, "variances must be positive");
+// Stats to the host (one sync).
+const DevStats& phaseStats(Frame& f) {
+  DeviceMap& m = f.m;
+  checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, f.s), "stats");
+  checkCuda(cudaGetLastError(), "kernel launch");
+  checkCuda(cudaStreamSynchronize(f.s), "integrate");
+  if (m.h_stats->error_code == 1) fail(Err::kInvalidVariance, "variances must be positive");
+  return *m.h_stats;
+}
+
+ScanResult resultFrom(const DevStats& d, std::size_t n) {
   ScanResult out;
   out.points_in = static_cast<std::int64_t>(n);
   out.excluded = static_cast<std::int64_t>(d.excluded);
@@ -1440,6 +1587,46 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   out.drift_offset = d.drift_offset;
   out.drift_clamped = d.drift_clamped != 0;
   out.drift_points = d.drift_n;
+  return out;
+}
+
+}  // namespace
+
+ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const double* xyz,
+                               std::size_t n, bool xyz_on_device, const Pose& pose,
+                               double stamp, double dt) {
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (n >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
+  if (m.shard.stage != 0) fail(Err::kUsage, "a sharded frame is in progress on this map");
+  Frame f(m, P, pose, stamp, dt);
+  const uint32_t N = static_cast<uint32_t>(n);
+  phaseBegin(f);
+  const double* d_xyz = phaseUpload(f, xyz, n, xyz_on_device);
+  checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
+  const SortGeom sg = phaseSortGeometry(f, N);
+  checkCuda(cudaEventRecord(m.ev[1], f.s), "event");  // upload done
+  phaseIngest(f, d_xyz, N, sg, true);
+  checkCuda(cudaEventRecord(m.ev[2], f.s), "event");  // ingest done
+  if (n > 0 && P.drift.enabled) {
+    k_drift_finalize<<<1, 1024, 0, f.s>>>(m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
+                                          P.drift.min_points, P.drift.max_offset_per_scan,
+                                          m.drift_offset, m.stats);
+    k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, m.drift_offset);
+    f.launches += 2;
+  }
+  checkCuda(cudaEventRecord(m.ev[3], f.s), "event");  // drift done
+  if (n > 0) {
+    phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
+    phaseRaysPass1(f, N, 0);
+    phaseRemovePass2(f, 0);
+  } else {
+    checkCuda(cudaEventRecord(m.ev[4], f.s), "event");
+    checkCuda(cudaEventRecord(m.ev[5], f.s), "event");
+  }
+  checkCuda(cudaEventRecord(m.ev[6], f.s), "event");  // rays done
+  phaseCells(f);
+  const DevStats& d = phaseStats(f);
+  ScanResult out = resultFrom(d, n);
 
   float ms[7], ms_trav = 0.0f;
   for (int k = 0; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
@@ -1456,10 +1643,178 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   m.phase_seconds[5] = 0.0;
   m.phase_seconds[6] = m.kernel_seconds[7];
   out.seconds = m.phase_seconds[6];
-  m.last_launches = launches;
+  m.last_launches = f.launches;
   m.last_visits = static_cast<long long>(d.visits);
   return out;
 }
 
-}  // namespace rb200
+// ------------------------------------------------------- sharded frames
+// Phase 1: recenter, this batch's K1, and its fusion records (stable
+// compaction of the in-map kept points) plus the local drift vote and fate
+// counters for the exchange.
+void shardIngest(DeviceMap& m, const PipelineParams& P, const double* xyz, std::size_t n,
+                 bool xyz_on_device, uint64_t ray_offset, uint64_t n_total, const Pose& pose,
+                 double stamp, ShardIO& io) {
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (n_total >= 0x7fffffffULL) fail(Err::kUsage, "too many points in one scan");
+  if (ray_offset + n > n_total) fail(Err::kUsage, "shard batch outside the frame");
+  // Point scratch sized for the whole frame now: phase 2 sorts all records
+  // while this batch's points must stay resident for the ray passes.
+  if (n_total > 0) ensurePointCapacity(m, static_cast<std::size_t>(n_total));
+  ShardState& st = m.shard;
+  st = ShardState{};
+  st.params = P;
+  st.pose = pose;
+  st.stamp = stamp;
+  st.dt = m.has_last ? std::max(0.0, stamp - m.last_stamp) : 0.0;
+  st.n_local = n;
+  st.ray_base = static_cast<uint32_t>(ray_offset);
+  Frame f(m, st.params, pose, stamp, st.dt);
+  const uint32_t N = static_cast<uint32_t>(n);
+  phaseBegin(f);
+  const double* d_xyz = phaseUpload(f, xyz, n, xyz_on_device);
+  SortGeom none;
+  phaseIngest(f, d_xyz, N, none, false);
+  io = ShardIO{};
+  if (n > 0) {
+    if (P.drift.enabled) {
+      k_drift_local<<<1, 1024, 0, f.s>>>(m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
+                                         m.drift_local);
+      ++f.launches;
+    }
+    const uint32_t nblk = (N + kCompact - 1) / kCompact;
+    k_compact_count<<<nblk, kCompact, 0, f.s>>>(m.key0, N, f.WH, m.blk);
+    k_compact_scan<<<1, kThreads, 0, f.s>>>(m.blk, nblk, m.blk + m.rcap);
+    k_compact_write<<<nblk, kCompact, 0, f.s>>>(m.key0, m.pz, m.pvar, N, f.WH, m.blk, m.rec_cell,
+                                                m.rec_z, m.rec_var);
+    f.launches += 3;
+  }
+  const DevStats& d = phaseStats(f);
+  io.counters[0] = static_cast<int64_t>(d.out_of_range);
+  io.counters[1] = static_cast<int64_t>(d.excluded);
+  io.counters[2] = static_cast<int64_t>(d.out_of_map);
+  if (n > 0) {
+    uint32_t total = 0;
+    checkCuda(cudaMemcpy(&total, m.blk + m.rcap, sizeof(total), cudaMemcpyDeviceToHost), "records");
+    io.n_records = total;
+    if (P.drift.enabled)
+      checkCuda(cudaMemcpy(io.drift, m.drift_local, 2 * sizeof(double), cudaMemcpyDeviceToHost), "drift");
+  }
+  io.rec_cell = m.rec_cell;
+  io.rec_z = m.rec_z;
+  io.rec_var = m.rec_var;
+  io.kstar = m.kstar;
+  io.ub = m.cur.ub;
+  io.ubv = m.cur.ubv;
+  io.cells = f.ncell;
+  st.launches = f.launches;
+  st.stage = 1;
+}
 
+// Phase 2: drift offset from all ranks' votes (summed in rank order), sort +
+// fusion of all gathered records (every rank, identical), ray pass 1 over
+// this batch. Leaves k* / ub / ubv for the min / min / max all-reduce.
+void shardUpdate(DeviceMap& m, const double* drift_pairs, int n_ranks, const uint32_t* d_cells,
+                 const double* d_z, const double* d_var, std::size_t n_records, ShardIO& io) {
+  ShardState& st = m.shard;
+  if (st.stage != 1) fail(Err::kUsage, "shard phases out of order (expected update after ingest)");
+  if (n_records >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  Frame f(m, st.params, st.pose, st.stamp, st.dt);
+  f.g = gridArgs(m.grid);
+  const PipelineParams& P = st.params;
+  if (P.drift.enabled && n_ranks > 0 && drift_pairs != nullptr) {
+    // Same arithmetic as k_drift_finalize (drift.cpp:44-55, integration.cpp:119-128).
+    double total = 0.0;
+    long long cnt = 0;
+    for (int r = 0; r < n_ranks; ++r) {
+      total += drift_pairs[2 * r];
+      cnt += static_cast<long long>(drift_pairs[2 * r + 1]);
+    }
+    const int nvote = static_cast<int>(cnt);
+    if (nvote >= P.drift.min_points) {
+      const double mean = total / nvote;
+      const double off = std::clamp(mean, -P.drift.max_offset_per_scan, P.drift.max_offset_per_scan);
+      st.drift_offset = off;
+      st.drift_clamped = off != mean;
+      st.drift_n = nvote;
+      if (off != 0.0) {
+        k_apply_offset_value<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, off);
+        ++f.launches;
+      }
+    }
+  }
+  const uint32_t M = static_cast<uint32_t>(n_records);
+  if (M > 0 && M > m.cap) fail(Err::kUsage, "more fusion records than points in the frame");
+  checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
+  if (M > 0) {
+    const SortGeom sg = phaseSortGeometry(f, M);
+    k_records_count<<<gridFor(M), kThreads, 0, f.s>>>(d_cells, M, m.count, sg.tc, sg.pitch,
+                                                      sg.buckets() - 1);
+    ++f.launches;
+    phaseSortFuse(f, d_cells, M, d_z, d_var, sg);
+  } else {
+    f.overlap = false;
+  }
+  phaseRaysPass1(f, static_cast<uint32_t>(st.n_local), st.ray_base);
+  checkCuda(cudaGetLastError(), "kernel launch");
+  checkCuda(cudaStreamSynchronize(f.s), "shard update");
+  st.overlap = f.overlap;
+  st.launches += f.launches;
+  io.kstar = m.kstar;
+  io.ub = m.cur.ub;
+  io.ubv = m.cur.ubv;
+  io.cells = f.ncell;
+  st.stage = 2;
+}
+
+// Phase 3 (after k* / ub / ubv hold the all-reduced values): removal and ray
+// pass 2 over this batch. Returns the cells removed (identical on every rank);
+// when > 0, ub / ubv need another min / max all-reduce.
+int64_t shardRemove(DeviceMap& m, ShardIO& io) {
+  ShardState& st = m.shard;
+  if (st.stage != 2) fail(Err::kUsage, "shard phases out of order (expected remove after update)");
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  Frame f(m, st.params, st.pose, st.stamp, st.dt);
+  f.g = gridArgs(m.grid);
+  phaseRemovePass2(f, st.ray_base);
+  unsigned long long removed = 0;
+  checkCuda(cudaMemcpyAsync(&m.h_stats->removed, &m.stats->removed, sizeof(removed),
+                            cudaMemcpyDeviceToHost, f.s),
+            "stats");
+  checkCuda(cudaGetLastError(), "kernel launch");
+  checkCuda(cudaStreamSynchronize(f.s), "shard remove");
+  removed = m.h_stats->removed;
+  st.launches += f.launches;
+  io.ub = m.cur.ub;
+  io.ubv = m.cur.ubv;
+  st.stage = 3;
+  return static_cast<int64_t>(removed);
+}
+
+// Phase 4: cell phases (every rank, identical) and the frame's stats with the
+// fate counters summed over the ranks.
+ScanResult shardFinish(DeviceMap& m, const int64_t counters_total[3], uint64_t points_total) {
+  ShardState& st = m.shard;
+  if (st.stage != 3) fail(Err::kUsage, "shard phases out of order (expected finish after remove)");
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  Frame f(m, st.params, st.pose, st.stamp, st.dt);
+  f.g = gridArgs(m.grid);
+  phaseCells(f);
+  const DevStats& d = phaseStats(f);
+  ScanResult out = resultFrom(d, points_total);
+  out.out_of_range = counters_total[0];
+  out.excluded = counters_total[1];
+  out.out_of_map = counters_total[2];
+  out.drift_offset = st.drift_offset;
+  out.drift_clamped = st.drift_clamped;
+  out.drift_points = st.drift_n;
+  m.last_launches = st.launches + f.launches;
+  m.last_visits = static_cast<long long>(d.visits);
+  m.last_stamp = st.stamp;
+  m.has_last = true;
+  st.stage = 0;
+  return out;
+}
+
+}  // namespace rb200
