@@ -638,9 +638,11 @@ __device__ __forceinline__ bool foldCell(const Layers& L, size_t i, int cnt,
           }
           continue;
         }
+        // The two quotients share one reciprocal as straight-line code
+        // (div2_rn == IEEE a/b for all inputs), instead of two division
+        // subroutines one after the other on the fold's dependent chain.
         const double denom = cv + sp;
-        h = (sp * ch + cv * z) / denom;
-        v = cv * sp / denom;
+        div2_rn(sp * ch + cv * z, cv * sp, denom, h, v);
         valid = true;
         fused_any = true;
         ++nf;

@@ -46,3 +46,15 @@ def test_double_to_int_like_x86(fp):
     assert fp.rb_to_int(1e10) == -2**31
     assert fp.rb_to_int(-1e10) == -2**31
     assert fp.rb_to_int(-3.7) == -3 and fp.rb_to_int(2147483647.5) == 2147483647
+
+
+@pytest.mark.gpu
+def test_device_div2_equals_ieee_division(tmp_path):
+    """div2_rn (two quotients over one shared reciprocal, used by the fold) must return exactly
+    the IEEE quotients: 10^9 random pairs over the whole double range on the device."""
+    exe = tmp_path / "div2_check"
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                    "--fmad=false", "-std=c++17", "-I", str(ROOT / "paper_2204_12876_b200" / "csrc"),
+                    str(ROOT / "tests" / "native" / "div2_check.cu"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), str(500_000_000), "7"], capture_output=True, text=True, check=True)
+    assert int(out.stdout.strip()) == 0
