@@ -1058,29 +1058,31 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   const uint8_t* __restrict__ cls = c.cls;
   uint8_t cl = cls[idx];
   double t_enter = t0;
+  // The axis step is written without branches around it (both sides predicate
+  // cleanly: the exit tests are hoisted), and the step counters double as the
+  // visit count: iterations = steps taken + 1.
+  const int xl0 = xl, yl0 = yl;
   while (true) {
-    ++visits;  // DDA steps (accounting)
     const bool sx = tmx < tmy;
     const double m = sx ? tmx : tmy;
     const bool more = m < t1;
     const double t_next = more ? m : t1;
     if (cl != 0 && idx != end_idx && t_next > t_enter)
       pass1Visit(c, cl, idx, c.oz + (0.5 * (t_enter + t_next)) * c.dz, touched);
-    if (!more) break;
+    const int lim = sx ? xl : yl;
+    if (!more || lim == 0) break;
     if (sx) {
-      if (xl == 0) break;
       --xl;
       tmx += tdx;
-      idx += step_col;
     } else {
-      if (yl == 0) break;
       --yl;
       tmy += tdy;
-      idx += step_idx_row;
     }
+    idx += sx ? step_col : step_idx_row;
     cl = cls[idx];
     t_enter = t_next;
   }
+  visits += static_cast<unsigned>((xl0 - xl) + (yl0 - yl) + 1);
 }
 
 #ifndef RB_PASS1_MIN_BLOCKS
