@@ -1062,6 +1062,15 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   // cleanly: the exit tests are hoisted), and the step counters double as the
   // visit count: iterations = steps taken + 1.
   const int xl0 = xl, yl0 = yl;
+// Unrolled by 2: the compiler renames t_enter / t_next across the two copies
+// and interleaves them (pass 1 224 -> 194 us on C4).
+#ifndef RB_P1_UNROLL
+#define RB_P1_UNROLL 2
+#endif
+#define RB_PRAGMA_(x) _Pragma(#x)
+#define RB_UNROLL_(n) RB_PRAGMA_(unroll n)
+#define RB_UNROLL(n) RB_UNROLL_(n)
+  RB_UNROLL(RB_P1_UNROLL)
   while (true) {
     const bool sx = tmx < tmy;
     const double m = sx ? tmx : tmy;
@@ -1078,7 +1087,8 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
       --yl;
       tmy += tdy;
     }
-    idx += sx ? step_col : step_idx_row;
+    const int inc = sx ? step_col : step_idx_row;
+    idx += inc;
     cl = cls[idx];
     t_enter = t_next;
   }
