@@ -189,9 +189,15 @@ __global__ void __launch_bounds__(kThreads)
       const int row = x86_to_int(floor((my - a.g.oy) / a.g.res));
       if (col >= 0 && col < a.g.W && row >= 0 && row < a.g.H) {
         cell = static_cast<uint32_t>(row) * a.g.W + col;
-        if (a.drift_enabled && L.valid[cell] && !(L.trav[cell] <= a.drift_thr)) {
-          ds = mz - L.elev[cell];
-          dn = 1;
+        if (a.drift_enabled) {
+          // The three gathers are issued together (one memory round trip
+          // instead of a dependent chain of three).
+          const uint8_t vld = L.valid[cell];
+          const double tr = L.trav[cell], el = L.elev[cell];
+          if (vld && !(tr <= a.drift_thr)) {
+            ds = mz - el;
+            dn = 1;
+          }
         }
       } else {
         oom = 1;
