@@ -49,7 +49,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "points/sec integrated and per-frame map-update ms (1/2/4/8 B200) vs CPU ref"
 REF_LIB = ROOT / "oracle" / "_ref" / "librelief_ref.so"
 L2_FLUSH_BYTES = 256 << 20
-DEVSTATS_BYTES = 120  # DevStats read back per scan (device_map.hpp)
+DEVSTATS_BYTES = 128  # DevStats read back per scan (device_map.hpp)
 
 
 def log(*a):

@@ -126,15 +126,15 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     const std::size_t n = grid.cells();
-    const std::size_t bytes = 2 * layerBytes(n) + 3 * alignUp(n * 4) + alignUp((n + 1) * 4) +
-                              alignUp(n) + 5 * kAlign;
+    const std::size_t bytes = 2 * layerBytes(n) + 4 * alignUp(n * 4) + alignUp((n + 1) * 4) +
+                              alignUp(n) + 6 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
     Carver c{static_cast<char*>(m->slab)};
     carveLayers(c, m->cur, n);
     carveLayers(c, m->alt, n);
     m->count = c.take<int32_t>(n);
     m->kstar = c.take<int32_t>(n);
-    m->heavy = c.take<uint32_t>(n);
+    m->heavy = c.take<uint32_t>(2 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");

@@ -46,7 +46,8 @@ struct DevStats {
   unsigned long long overlap_cleared;
   unsigned long long candidate_rays;  // rays queued for the k* pass
   unsigned long long visits;          // DDA cells emitted by pass 1
-  unsigned long long heavy_cells;     // cells folded by k_fuse_heavy
+  unsigned long long heavy_cells;     // cells folded by k_fuse_heavy, one per lane
+  unsigned long long vheavy_cells;    // cells folded by k_fuse_heavy, one per warp
   double drift_offset;                // applied offset (0 when not applied)
   int drift_n;
   int drift_clamped;
@@ -119,7 +120,7 @@ struct DeviceMap {
   uint32_t* start = nullptr;
   uint8_t* cls = nullptr;
   int32_t* kstar = nullptr;
-  uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold
+  uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
   // per-point scratch (grown on demand)
   std::size_t cap = 0;
   void* pslab = nullptr;

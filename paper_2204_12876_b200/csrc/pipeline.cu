@@ -584,90 +584,105 @@ struct FoldCounts {
   unsigned long long nf = 0, no = 0, ni = 0, upd = 0;
 };
 
+// Running state of one cell's gated Kalman fold.
+struct FoldState {
+  bool valid, var_changed, bad, fused_any;
+  double h, v;
+};
+
+__device__ __forceinline__ FoldState foldBegin(const Layers& L, size_t i) {
+  return FoldState{L.valid[i] != 0, false, false, false, L.elev[i], L.var[i]};
+}
+
+// One point of the fold (reference integration.cpp:40-55, 142-203). Returns
+// false when a non-positive variance stops the fold.
+__device__ __forceinline__ bool foldPoint(FoldState& s, double z, double sp, bool wall,
+                                          const FuseArgs& a, FoldCounts& k) {
+  const double ch = s.valid ? s.h : z;
+  const double cv = s.valid ? s.v : a.sigma_init2;
+  if (cv <= 0.0 || sp <= 0.0) {
+    s.bad = true;
+    return false;
+  }
+  if (wall && z < ch) {
+    ++k.ni;
+    return true;
+  }
+  if (gateOutlier(fabs(z - ch), cv, a)) {
+    ++k.no;
+    if (s.valid) {
+      s.v = smin(cv + a.sigma_outlier2, a.sigma_max2);
+      s.var_changed = true;
+    }
+    return true;
+  }
+  // The two quotients share one reciprocal as straight-line code (div2_rn ==
+  // IEEE a/b for all inputs), instead of two division subroutines one after
+  // the other on the fold's dependent chain.
+  const double denom = cv + sp;
+  div2_rn(sp * ch + cv * z, cv * sp, denom, s.h, s.v);
+  s.valid = true;
+  s.fused_any = true;
+  ++k.nf;
+  return true;
+}
+
+// setEstimate (grid.cpp:139-147) for a cell that fused, else the outlier
+// variance; flags a non-positive variance.
+__device__ __forceinline__ bool foldEnd(const Layers& L, size_t i, const FoldState& s,
+                                        const FuseArgs& a, DevStats* st, FoldCounts& k) {
+  if (s.bad) atomicExch(&st->error_code, 1);
+  if (s.fused_any) {
+    L.elev[i] = s.h;
+    L.var[i] = s.v;
+    L.last[i] = a.now;
+    L.valid[i] = 1;
+    L.ub[i] = s.h;
+    L.ubv[i] = 1;
+    k.upd = k.upd + 1;
+  } else if (s.var_changed) {
+    L.var[i] = s.v;
+  }
+  return s.fused_any;
+}
+
 // Gated Kalman fold of one cell (reference integration.cpp:40-55,142-203,
 // grid.cpp:139-147): the cell's points in scan order. The payload is
 // contiguous per cell (written by the last radix pass), loaded in batches of 8
-// with the next batch in flight while the current one is folded, so the
-// dependent fp64 chain does not wait on memory. Returns whether any point fused.
+// with the next batch in flight while the current one is folded. Returns
+// whether any point fused.
 __device__ __forceinline__ bool foldCell(const Layers& L, size_t i, int cnt,
                                          const uint32_t* __restrict__ start,
                                          const double* __restrict__ spz,
                                          const double* __restrict__ spv, const FuseArgs& a,
                                          DevStats* st, FoldCounts& k) {
-  unsigned long long& nf = k.nf;
-  unsigned long long& no = k.no;
-  unsigned long long& ni = k.ni;
-  unsigned long long& upd = k.upd;
-  bool fused_any = false;
-  {
-    bool valid = L.valid[i] != 0;
-    double h = L.elev[i], v = L.var[i];
-    bool var_changed = false, bad = false;
-    const double* zp = spz + start[i];
-    const double* vp = spv + start[i];
-    const bool wall = cnt > a.wall;
-    double zn[kFoldBatch], vn[kFoldBatch];
+  FoldState s = foldBegin(L, i);
+  const double* zp = spz + start[i];
+  const double* vp = spv + start[i];
+  const bool wall = cnt > a.wall;
+  double zn[kFoldBatch], vn[kFoldBatch];
+#pragma unroll
+  for (int b = 0; b < kFoldBatch; ++b) {
+    zn[b] = b < cnt ? zp[b] : 0.0;
+    vn[b] = b < cnt ? vp[b] : 0.0;
+  }
+  for (int base = 0; base < cnt && !s.bad; base += kFoldBatch) {
+    double zc[kFoldBatch], vc[kFoldBatch];
 #pragma unroll
     for (int b = 0; b < kFoldBatch; ++b) {
-      zn[b] = b < cnt ? zp[b] : 0.0;
-      vn[b] = b < cnt ? vp[b] : 0.0;
+      zc[b] = zn[b];
+      vc[b] = vn[b];
+      const int j = base + kFoldBatch + b;
+      zn[b] = j < cnt ? zp[j] : 0.0;
+      vn[b] = j < cnt ? vp[j] : 0.0;
     }
-    for (int base = 0; base < cnt && !bad; base += kFoldBatch) {
-      double zc[kFoldBatch], vc[kFoldBatch];
 #pragma unroll
-      for (int b = 0; b < kFoldBatch; ++b) {
-        zc[b] = zn[b];
-        vc[b] = vn[b];
-        const int j = base + kFoldBatch + b;
-        zn[b] = j < cnt ? zp[j] : 0.0;
-        vn[b] = j < cnt ? vp[j] : 0.0;
-      }
-#pragma unroll
-      for (int b = 0; b < kFoldBatch; ++b) {
-        if (base + b >= cnt || bad) break;
-        const double z = zc[b], sp = vc[b];
-        const double ch = valid ? h : z;
-        const double cv = valid ? v : a.sigma_init2;
-        if (cv <= 0.0 || sp <= 0.0) {
-          bad = true;
-          break;
-        }
-        if (wall && z < ch) {
-          ++ni;
-          continue;
-        }
-        if (gateOutlier(fabs(z - ch), cv, a)) {
-          ++no;
-          if (valid) {
-            v = smin(cv + a.sigma_outlier2, a.sigma_max2);
-            var_changed = true;
-          }
-          continue;
-        }
-        // The two quotients share one reciprocal as straight-line code
-        // (div2_rn == IEEE a/b for all inputs), instead of two division
-        // subroutines one after the other on the fold's dependent chain.
-        const double denom = cv + sp;
-        div2_rn(sp * ch + cv * z, cv * sp, denom, h, v);
-        valid = true;
-        fused_any = true;
-        ++nf;
-      }
-    }
-    if (bad) atomicExch(&st->error_code, 1);
-    if (fused_any) {
-      L.elev[i] = h;
-      L.var[i] = v;
-      L.last[i] = a.now;
-      L.valid[i] = 1;
-      L.ub[i] = h;
-      L.ubv[i] = 1;
-      upd = 1;
-    } else if (var_changed) {
-      L.var[i] = v;
+    for (int b = 0; b < kFoldBatch; ++b) {
+      if (base + b >= cnt) break;
+      if (!foldPoint(s, zc[b], vc[b], wall, a, k)) break;
     }
   }
-  return fused_any;
+  return foldEnd(L, i, s, a, st, k);
 }
 
 __device__ __forceinline__ void flushCounts(FoldCounts k, DevStats* st) {
@@ -685,47 +700,122 @@ __device__ __forceinline__ void flushCounts(FoldCounts k, DevStats* st) {
 
 // Cells with at most `heavy` points are folded here, one thread per cell;
 // longer cells are queued for k_fuse_heavy, which runs on a second stream
-// concurrently with the ray pass.
+// concurrently with the ray pass: cells
+// with more than kVeryHeavyCell points on their own list (one warp each there).
+constexpr int kVeryHeavyCell = 256;
 __global__ void __launch_bounds__(kThreads)
     k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
            const uint32_t* __restrict__ start, const double* __restrict__ spz,
            const double* __restrict__ spv, FuseArgs a, DevStats* st, int heavy,
-           uint32_t* heavy_list) {
+           uint32_t* heavy_list, uint32_t* vheavy_list) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const int cnt = i < ncell ? count[i] : 0;
   const bool is_heavy = cnt > heavy;
-  const unsigned hv = __ballot_sync(0xffffffffu, is_heavy);
+  const bool is_vheavy = is_heavy && cnt > kVeryHeavyCell;
+  const int lane = threadIdx.x & 31;
+  const unsigned hv = __ballot_sync(0xffffffffu, is_heavy && !is_vheavy);
   if (hv) {
-    const int lane = threadIdx.x & 31;
     unsigned base = 0;
     if (lane == __ffs(hv) - 1)
       base = static_cast<unsigned>(atomicAdd(&st->heavy_cells, static_cast<unsigned long long>(__popc(hv))));
     base = __shfl_sync(0xffffffffu, base, __ffs(hv) - 1);
-    if (is_heavy) heavy_list[base + __popc(hv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+    if (is_heavy && !is_vheavy) heavy_list[base + __popc(hv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+  }
+  const unsigned vv = __ballot_sync(0xffffffffu, is_vheavy);
+  if (vv) {
+    unsigned base = 0;
+    if (lane == __ffs(vv) - 1)
+      base = static_cast<unsigned>(atomicAdd(&st->vheavy_cells, static_cast<unsigned long long>(__popc(vv))));
+    base = __shfl_sync(0xffffffffu, base, __ffs(vv) - 1);
+    if (is_vheavy) vheavy_list[base + __popc(vv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
   }
   FoldCounts k;
   if (cnt > 0 && !is_heavy) foldCell(L, i, cnt, start, spz, spv, a, st, k);
   flushCounts(k, st);
 }
 
-// Long cells (queued by k_fuse). The concurrent ray pass treated them as ray
-// class "none"; if a cell's post-fusion class is anything else (it fused
-// nothing and is invalid, or stale with a normal) that is flagged and the ray
-// pass is re-run after the join.
+// Post-fusion ray class of a cell the concurrent ray pass treated as "none";
+// flags a wrong speculation.
+__device__ __forceinline__ void checkSpeculation(const Layers& L, size_t i, const FuseArgs& a,
+                                                 double t_free, int cleanup, int bound, DevStats* st) {
+  const bool none = L.valid[i] ? !(cleanup && !(a.now - L.last[i] <= t_free) &&
+                                   (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0))
+                               : !bound;
+  if (!none) atomicExch(&st->respeculate, 1);
+}
+
+// Long cells (queued by k_fuse), concurrently with the ray pass. The very
+// long ones first, one warp each: the warp stages the cell's payload into
+// shared memory (coalesced, all loads in flight at once) and lane 0 folds it
+// from there -- one thread folding from global memory waits an L2 round trip
+// per prefetch batch (~250 cycles per point, scripts/fold_bench.cu), which made
+// the longest cell (1,230 points) the critical path. Then the rest, one cell
+// per lane from global memory.
+constexpr int kHeavyStage = 2048;  // points staged per round (32 KB)
 __global__ void __launch_bounds__(32)
     k_fuse_heavy(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
-                 const DevStats* st_in, const uint32_t* __restrict__ start,
-                 const double* __restrict__ spz, const double* __restrict__ spv, FuseArgs a,
-                 DevStats* st, double t_free, int cleanup, int bound) {
-  const unsigned total = static_cast<unsigned>(st_in->heavy_cells);
+                 const uint32_t* __restrict__ vlist, const DevStats* st_in,
+                 const uint32_t* __restrict__ start, const double* __restrict__ spz,
+                 const double* __restrict__ spv, FuseArgs a, DevStats* st, double t_free,
+                 int cleanup, int bound) {
+  __shared__ double sz[kHeavyStage];
+  __shared__ double sv[kHeavyStage];
+  const int lane = threadIdx.x;
   FoldCounts k;
-  for (unsigned q = blockIdx.x * 32 + threadIdx.x; q < total; q += gridDim.x * 32) {
+  const unsigned nv = static_cast<unsigned>(st_in->vheavy_cells);
+  for (unsigned q = blockIdx.x; q < nv; q += gridDim.x) {
+    const uint32_t i = vlist[q];
+    const int cnt = count[i];
+    const uint32_t s0 = start[i];
+    const bool wall = cnt > a.wall;
+    FoldState s{};
+    if (lane == 0) s = foldBegin(L, i);
+    bool go = true;
+    for (int base = 0; base < cnt && go; base += kHeavyStage) {
+      const int n = min(kHeavyStage, cnt - base);
+      __syncwarp();
+      for (int j = lane; j < n; j += 32) {
+        sz[j] = spz[s0 + base + j];
+        sv[j] = spv[s0 + base + j];
+      }
+      __syncwarp();
+      // Warp-cooperative fold: points the wall rule ignores leave (h, v)
+      // unchanged, so the lanes test the next 32 points against the current
+      // state at once and the whole leading run of ignored points is skipped
+      // in one step (counted, in order); lane 0 then folds the first point
+      // that is not ignored. Same decisions in the same order as the
+      // sequential fold.
+      int j = 0;
+      while (j < n) {
+        const bool valid = __shfl_sync(0xffffffffu, s.valid, 0);
+        const double h = __shfl_sync(0xffffffffu, s.h, 0);
+        const double v = __shfl_sync(0xffffffffu, s.v, 0);
+        const int jj = j + lane;
+        // ignored <=> no variance error (cv, sp > 0) and the wall rule fires;
+        // an invalid cell compares z < z (false) -- never ignored.
+        const bool ign = wall && valid && v > 0.0 && jj < n && sv[jj] > 0.0 && sz[jj] < h;
+        const unsigned run_mask = ~__ballot_sync(0xffffffffu, ign);
+        const int run = run_mask ? __ffs(run_mask) - 1 : 32;
+        if (lane == 0) k.ni += static_cast<unsigned>(run);
+        j += run;
+        if (run == 32 || j >= n) continue;
+        int ok = 1;
+        if (lane == 0) ok = foldPoint(s, sz[j], sv[j], wall, a, k) ? 1 : 0;
+        ++j;
+        if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+      }
+      go = __shfl_sync(0xffffffffu, lane == 0 ? !s.bad : 1, 0) != 0;
+    }
+    if (lane == 0) {
+      foldEnd(L, i, s, a, st, k);
+      checkSpeculation(L, i, a, t_free, cleanup, bound, st);
+    }
+  }
+  const unsigned total = static_cast<unsigned>(st_in->heavy_cells);
+  for (unsigned q = blockIdx.x * 32 + lane; q < total; q += gridDim.x * 32) {
     const uint32_t i = list[q];
     foldCell(L, i, count[i], start, spz, spv, a, st, k);
-    const bool none = L.valid[i] ? !(cleanup && !(a.now - L.last[i] <= t_free) &&
-                                     (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0))
-                                 : !bound;
-    if (!none) atomicExch(&st->respeculate, 1);
+    checkSpeculation(L, i, a, t_free, cleanup, bound, st);
   }
   flushCounts(k, st);
 }
@@ -1468,12 +1558,13 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
   f.heavy = f.overlap ? kHeavyCell : INT_MAX;
   k_fuse<<<gridFor(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
-                                               m.stats, f.heavy, m.heavy);
+                                               m.stats, f.heavy, m.heavy, m.heavy + f.ncell);
   ++f.launches;
   if (f.overlap) {
     checkCuda(cudaEventRecord(m.ev[10], s), "event");
     checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
-    k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.stats, m.start, m.spz,
+    k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.heavy + f.ncell, m.stats,
+                                                      m.start, m.spz,
                                                       m.spv, fa, m.stats, f.P.cleanup.t_free, cleanup,
                                                       bound);
     ++f.launches;
