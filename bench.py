@@ -357,9 +357,15 @@ def roofline(dom, kmean, m, w, pts, frames):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(dom)
+    ceiling = None
+    cf = ROOT / "profiles" / "l2_visit_ceiling.json"
+    if cf.exists():
+        ceiling = json.loads(cf.read_text()).get("u8_1MB_probes_per_s")
     return {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
             "frac": ach / peak, "traffic": traffic, "algorithmic_bytes": int(by[dom]),
             "duration_us": dur * 1e6, "dda_visits_per_frame": int(visits),
+            "visits_per_s": visits / dur if dom == "rays" else None,
+            "l2_random_probe_ceiling_per_s": ceiling,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6.65 TB/s"}
 
 
