@@ -21,6 +21,27 @@ __global__ void k_bench(Layers L, const uint32_t* start, const double* spz, cons
   cycles[2] = static_cast<long long>(k.ni);
   cycles[3] = static_cast<long long>(k.no);
 }
+__global__ void k_bench_smem(Layers L, const double* spz, const double* spv, int cnt, FuseArgs a,
+                             long long* cycles) {
+  __shared__ double sz[2048], sv[2048];
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    sz[j] = spz[j];
+    sv[j] = spv[j];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  FoldCounts k;
+  FoldState s = foldBegin(L, 0);
+  const bool wall = cnt > a.wall;
+  const long long t0 = clock64();
+  for (int j = 0; j < cnt; ++j)
+    if (!foldPoint(s, sz[j], sv[j], wall, a, k)) break;
+  const long long t1 = clock64();
+  cycles[0] = t1 - t0 + (s.h > 1e300 ? 1 : 0);
+  cycles[1] = static_cast<long long>(k.nf);
+  cycles[2] = static_cast<long long>(k.ni);
+  cycles[3] = static_cast<long long>(k.no);
+}
 }  // namespace
 }  // namespace rb200
 
@@ -54,6 +75,11 @@ int main() {
       cudaMemcpy(c, dc, 32, cudaMemcpyDeviceToHost);
     }
     printf("mode %d: %lld cycles, %.1f cycles/point (fused %lld ignored %lld outlier %lld)\n", mode, c[0],
+           double(c[0]) / n, c[1], c[2], c[3]);
+    fillFresh(*m);
+    k_bench_smem<<<1, 256>>>(m->cur, dz, dv, n, a, dc);
+    cudaMemcpy(c, dc, 32, cudaMemcpyDeviceToHost);
+    printf("  smem single-thread: %.1f cycles/point (fused %lld ignored %lld outlier %lld)\n",
            double(c[0]) / n, c[1], c[2], c[3]);
   }
   return 0;
