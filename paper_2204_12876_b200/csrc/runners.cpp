@@ -354,14 +354,13 @@ void runExport(const std::string& snapshot_path, const std::string& layer, bool 
   }
 }
 
+// Reference capi.cpp:320-332 + runner.cpp:349-362: parameters from the config
+// first (if any), then the snapshot.
 std::size_t runSegment(const std::string& snapshot_path, const char* config_path,
                        const std::string& out_path) {
-  (void)readSnapshotFile(snapshot_path);
-  if (config_path != nullptr) (void)loadRunConfigFile(config_path);
-  (void)out_path;
-  fail(Err::kUsage,
-       "plane segmentation is not part of the B200 update path (reference postprocess.cpp:"
-       "389-545 runs on demand on the CPU); see DESIGN.md");
+  PlaneSegParams params;
+  if (config_path != nullptr) params = loadRunConfigFile(config_path).segmentation;
+  return segmentSnapshot(snapshot_path, params, out_path);
 }
 
 }  // namespace rb200

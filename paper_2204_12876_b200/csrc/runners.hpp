@@ -23,6 +23,9 @@ void runExport(const std::string& snapshot_path, const std::string& layer, bool 
                const std::string& out_path);
 std::size_t runSegment(const std::string& snapshot_path, const char* config_path,
                        const std::string& out_path);
+// Plane segmentation of a snapshot on the host (segment.cpp); returns the regions written.
+std::size_t segmentSnapshot(const std::string& snapshot_path, const PlaneSegParams& params,
+                            const std::string& out_path);
 
 void runMapChain(DeviceMap& m, const std::string& layer, const int* kinds, const int* radii,
                  const double* sigmas, int n_steps, double* values_out, uint8_t* valid_out);

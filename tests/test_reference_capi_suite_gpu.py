@@ -1,8 +1,8 @@
 """Drop-in check: the reference's own C API suite (proj/tests/test_capi.cpp, unmodified) built
 against librelief_b200.so (oracle/Makefile target capi-on-b200) and run on the GPU.
 
-Expected: every check passes except the plane-segmentation runner (relief_run_segment), which
-is outside the B200 path and returns RELIEF_ERROR_USAGE."""
+Expected: every check passes, the plane-segmentation runner included (host code,
+csrc/segment.cpp)."""
 from __future__ import annotations
 
 import re
@@ -25,7 +25,6 @@ def test_reference_capi_suite_against_b200(gpu, tmp_path):
     summary = proc.stdout.strip().splitlines()[-1]
     m = re.search(r"checks: (\d+) \| failed checks: (\d+)", summary)
     assert m, summary
-    # only the segmentation runner may fail
-    assert all("relief_run_segment" in l for l in failures), failures
-    assert len(failures) <= 1, failures
+    assert not failures, failures
+    assert int(m.group(2)) == 0, summary
     assert int(m.group(1)) > 11000, summary  # the layer round-trip checks ran
