@@ -267,3 +267,22 @@ def test_overlapped_fold_retry_path(gpu, reference, tmp_path):
     assert_stats_match(got, want)
     assert got.points_ignored_low == 100 and got.cells_removed_by_cleanup >= 1
     assert_layers_match(maps[0].layers(), maps[1].layers())
+
+
+@pytest.mark.parametrize("W,H", [(3, 3), (45, 46), (64, 32), (2100, 2100)])
+def test_sort_pass_count_paths(gpu, reference, tmp_path, W, H):
+    """The stable radix sort by cell runs 1 pass (<= 2^11 cells), 2 passes (<= 2^22) or 3 passes
+    (more cells); every geometry must keep scan order within cells (fold parity)."""
+    res = 0.04 if W * H > 10_000 else 0.05
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\nupdate.sigma_outlier2 = 0.02\n",
+                res, W, H)
+    rng = np.random.default_rng(W)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    half_x, half_y = 0.5 * W * res, 0.5 * H * res
+    n = 200_000 if W * H > 1_000_000 else 20_000
+    for scan in range(2):
+        xy = np.column_stack([rng.uniform(-half_x, half_x, n), rng.uniform(-half_y, half_y, n)])
+        xy = xy * np.where(rng.random((n, 1)) < 0.5, 0.02, 1.0)  # dense centre: long cells too
+        z = -1.0 + 0.05 * rng.standard_normal(n)
+        pair.integrate(np.column_stack([xy, z]), pose, 0.1 * scan, context=f"{W}x{H} scan {scan}")
+        pair.compare(context=f"{W}x{H} scan {scan}")
