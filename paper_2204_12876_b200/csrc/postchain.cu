@@ -95,10 +95,11 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
   out[i] = (n % 2 == 1) ? win[n / 2] : 0.5 * (win[n / 2 - 1] + win[n / 2]);
 }
 
-// ---- min inpaint: connected components of invalid cells (4-neighbour),
-// ECL-CC style: every parent index is smaller than its child, the initial
-// forest links each cell to its left / upper invalid neighbour, finds use
-// intermediate pointer jumping, and a flatten pass makes parent[i] the root.
+// ---- min inpaint: connected components of invalid cells (4-neighbour).
+// Tile-local labels in shared memory (k_cc_tile), then a lock-free
+// union-find over tile roots across tile edges (ECL-CC style hooks: every
+// parent index is smaller than its child, finds use intermediate pointer
+// jumping), and a flatten pass makes parent[i] the root.
 __device__ __forceinline__ int representative(int* p, int x) {
   int cur = p[x];
   if (cur != x) {
@@ -145,43 +146,92 @@ __device__ __forceinline__ double fromKey(unsigned long long k) {
 }
 constexpr unsigned long long kKeyInf = 0xfff0000000000000ULL;  // orderKey(+inf)
 
-__global__ void __launch_bounds__(kT) k_cc_init(const uint8_t* ok, int W, int H, int* parent,
-                                                unsigned long long* key, uint8_t* border,
-                                                int* any_valid) {
-  const int i = blockIdx.x * kT + threadIdx.x;
-  if (i >= W * H) return;
-  key[i] = kKeyInf;
-  border[i] = 0;
-  if (ok[i]) {
-    *any_valid = 1;
+
+// Two-level labelling: each 32x32 tile labels its invalid cells in shared
+// memory, writing the tile-local root (smallest index) as a global index;
+// k_cc_merge then only unions across tile edges, so the global forest's
+// chains are tile-root chains instead of whole rows.
+constexpr int kTileCC = 32;
+
+__global__ void __launch_bounds__(kTileCC* kTileCC)
+    k_cc_tile(const uint8_t* ok, int W, int H, int* parent, unsigned long long* key,
+              uint8_t* border, int* any_valid) {
+  __shared__ int lab[kTileCC * kTileCC];
+  const int tx = threadIdx.x % kTileCC, ty = threadIdx.x / kTileCC;
+  const int c = blockIdx.x * kTileCC + tx, r = blockIdx.y * kTileCC + ty;
+  const bool in = c < W && r < H;
+  const int i = r * W + c;
+  const int t = threadIdx.x;
+  bool fg = false;
+  if (in) {
+    key[i] = kKeyInf;
+    border[i] = 0;
+    if (ok[i]) *any_valid = 1;
+    else fg = true;
+  }
+  // Tile-local labels by min-propagation with pointer jumping: every cell
+  // takes the smallest label among itself, its 4-neighbours in the tile and
+  // the label its label points at, until no label changes (labels only
+  // decrease and always name a cell of the same component, so the in-place
+  // races are benign). The fixed point is the component's smallest index.
+  constexpr int kNone = 1 << 30;
+  lab[t] = fg ? t : kNone;
+  __syncthreads();
+  while (true) {
+    int changed = 0;
+    if (fg) {
+      int m = lab[t];
+      if (tx > 0) m = min(m, lab[t - 1]);
+      if (tx < kTileCC - 1) m = min(m, lab[t + 1]);
+      if (ty > 0) m = min(m, lab[t - kTileCC]);
+      if (ty < kTileCC - 1) m = min(m, lab[t + kTileCC]);
+      m = min(m, lab[m]);
+      if (m < lab[t]) {
+        lab[t] = m;
+        changed = 1;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  if (!in) return;
+  if (!fg) {
     parent[i] = i;
     return;
   }
-  const int c = i % W;
-  int p = i;
-  if (c > 0 && !ok[i - 1]) p = i - 1;
-  else if (i >= W && !ok[i - W]) p = i - W;
-  parent[i] = p;
+  const int root = lab[t];
+  parent[i] = (blockIdx.y * kTileCC + root / kTileCC) * W + blockIdx.x * kTileCC + root % kTileCC;
 }
 
-__global__ void __launch_bounds__(kT) k_cc_union(const uint8_t* ok, int W, int H, int* parent) {
-  const int i = blockIdx.x * kT + threadIdx.x;
-  if (i >= W * H || ok[i]) return;
-  // The initial forest already joined i to its left neighbour when both are
-  // invalid; the upper neighbour still needs an explicit union then.
-  const int c = i % W;
-  if (c > 0 && !ok[i - 1] && i >= W && !ok[i - W]) hook(parent, i, i - W);
+// Unions across tile edges, one thread per edge cell, consecutive threads
+// walking along one boundary (the first H * (tiles_x - 1) threads the
+// vertical boundaries, the rest the horizontal ones). Neighbouring edge cells
+// usually join the same pair of tile roots, so each warp hooks every distinct
+// (root, root) pair once.
+__global__ void __launch_bounds__(kT) k_cc_merge(const uint8_t* ok, int W, int H, int* parent) {
+  const int q = blockIdx.x * kT + threadIdx.x;
+  const int vx = (W - 1) / kTileCC;  // vertical boundaries
+  const int hy = (H - 1) / kTileCC;  // horizontal boundaries
+  int i = -1, j = -1;
+  if (q < H * vx) {
+    const int r = q % H, c = (q / H + 1) * kTileCC;
+    i = r * W + c;
+    j = i - 1;
+  } else if (q < H * vx + W * hy) {
+    const int e = q - H * vx;
+    const int r = (e / W + 1) * kTileCC, c = e % W;
+    i = r * W + c;
+    j = i - W;
+  }
+  const bool pair = i >= 0 && !ok[i] && !ok[j];
+  const int a = pair ? parent[i] : -1, b = pair ? parent[j] : -1;
+  const unsigned long long key =
+      (static_cast<unsigned long long>(static_cast<unsigned>(a)) << 32) | static_cast<unsigned>(b);
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  if (pair && (threadIdx.x & 31) == __ffs(peers) - 1) hook(parent, a, b);
 }
 
-__global__ void __launch_bounds__(kT) k_cc_flatten(const uint8_t* ok, int n, int* parent) {
-  const int i = blockIdx.x * kT + threadIdx.x;
-  if (i >= n || ok[i]) return;
-  parent[i] = representative(parent, i);
-}
-
-// Second flatten without path writes: the compressing pass above can leave an
-// entry pointing at a non-root ancestor when another thread's compression
-// overwrote it; now every chain is short and only own entries are written.
+// Flatten without path writes: chains are tile-root chains (short); only each
+// cell's own entry is written, so concurrent walks never see a torn path.
 __global__ void __launch_bounds__(kT) k_cc_flatten2(const uint8_t* ok, int n, int* parent) {
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= n || ok[i]) return;
@@ -319,10 +369,11 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
       k_median<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, nv, no);
       ++launches;
     } else {
-      k_cc_init<<<grid, kT, 0, s>>>(co, W, H, sc.parent, sc.key, sc.border, sc.flag);
+      const dim3 tiles((W + kTileCC - 1) / kTileCC, (H + kTileCC - 1) / kTileCC);
+      k_cc_tile<<<tiles, kTileCC * kTileCC, 0, s>>>(co, W, H, sc.parent, sc.key, sc.border, sc.flag);
       k_check_any<<<1, 1, 0, s>>>(sc.flag);
-      k_cc_union<<<grid, kT, 0, s>>>(co, W, H, sc.parent);
-      k_cc_flatten<<<grid, kT, 0, s>>>(co, n, sc.parent);
+      const int edges = H * ((W - 1) / kTileCC) + W * ((H - 1) / kTileCC);
+      if (edges > 0) k_cc_merge<<<(edges + kT - 1) / kT, kT, 0, s>>>(co, W, H, sc.parent);
       k_cc_flatten2<<<grid, kT, 0, s>>>(co, n, sc.parent);
       k_cc_border<<<grid, kT, 0, s>>>(cv, co, W, H, sc.parent, sc.key, sc.border);
       k_cc_fill<<<grid, kT, 0, s>>>(cv, co, n, sc.parent, sc.key, sc.border, nv, no);
