@@ -61,6 +61,39 @@ __global__ void __launch_bounds__(kT) k_linear(const double* __restrict__ v,
   out[i] = acc / ws;
 }
 
+// Fixed-radius linear filter: same sums in the same order, loops unrolled.
+template <int R>
+__global__ void __launch_bounds__(kT) k_linear_r(const double* __restrict__ v,
+                                                 const uint8_t* __restrict__ ok, int W, int H,
+                                                 Weights wt, double* __restrict__ out,
+                                                 uint8_t* __restrict__ ok_out) {
+  constexpr int k = 2 * R + 1;
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= W * H) return;
+  ok_out[i] = ok[i];
+  if (!ok[i]) {
+    out[i] = v[i];
+    return;
+  }
+  const int r = i / W, c = i - (i / W) * W;
+  double acc = 0.0, ws = 0.0;
+#pragma unroll
+  for (int dr = -R; dr <= R; ++dr) {
+    const int rr = r + dr;
+#pragma unroll
+    for (int dc = -R; dc <= R; ++dc) {
+      const int cc = c + dc;
+      if (rr < 0 || rr >= H || cc < 0 || cc >= W) continue;
+      const int j = rr * W + cc;
+      if (!ok[j]) continue;
+      const double w = wt.w[(dr + R) * k + (dc + R)];
+      acc += w * v[j];
+      ws += w;
+    }
+  }
+  out[i] = acc / ws;
+}
+
 __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
                                                const uint8_t* __restrict__ ok, int W, int H,
                                                int R, double* __restrict__ out,
@@ -363,7 +396,9 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
         for (int dc = -st.radius; dc <= st.radius; ++dc)
           wt.w[(dr + st.radius) * kk + (dc + st.radius)] =
               st.kind == 1 ? 1.0 : std::exp(-(dr * dr + dc * dc) / (2.0 * st.sigma * st.sigma));
-      k_linear<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, wt, nv, no);
+      if (st.radius == 1) k_linear_r<1><<<grid, kT, 0, s>>>(cv, co, W, H, wt, nv, no);
+      else if (st.radius == 2) k_linear_r<2><<<grid, kT, 0, s>>>(cv, co, W, H, wt, nv, no);
+      else k_linear<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, wt, nv, no);
       ++launches;
     } else if (st.kind == 2) {
       k_median<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, nv, no);
