@@ -91,6 +91,21 @@ RELIEF_API relief_status relief_gpu_smooth_chain(const double* values, const uin
                                                  int n_steps, double* values_out,
                                                  uint8_t* valid_out);
 
+/* Streaming integrate for sensor pipelines: enqueues the frame (xyz in host
+ * memory -- pinned memory lets the copy run asynchronously) and returns. Frames
+ * are processed in call order; the PCIe copy of frame k+1 overlaps the kernels
+ * of frame k. At most three frames may be in flight: relief_gpu_map_wait blocks
+ * until the oldest one completes and returns its stats (same values as
+ * relief_map_integrate). The caller keeps xyz unchanged until that frame's
+ * wait returns. relief_map_integrate and the shard calls refuse while frames
+ * are in flight (RELIEF_ERROR_USAGE). */
+RELIEF_API relief_status relief_gpu_map_integrate_async(relief_map* map,
+                                                        const relief_config* config,
+                                                        const double* xyz, size_t n_points,
+                                                        const double pose[12], double stamp);
+RELIEF_API relief_status relief_gpu_map_wait(relief_map* map, relief_scan_stats* stats_out);
+RELIEF_API int relief_gpu_map_in_flight(const relief_map* map);
+
 /* Conv-net traversability (reference analysis.cpp:138-290). Loads the weight
  * file into the config and switches the pipeline to the learned filter, so
  * relief_map_integrate runs it (the reference reaches it only through its

@@ -129,6 +129,9 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_map_chain_seconds": (_D, [_P]),
     "relief_gpu_smooth_chain": (_I, [_DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, ctypes.POINTER(_I),
                                      ctypes.POINTER(_I), _DP, _I, _DP, ctypes.POINTER(ctypes.c_uint8)]),
+    "relief_gpu_map_integrate_async": (_I, [_P, _P, ctypes.c_void_p, _SZ, _DP, _D]),
+    "relief_gpu_map_wait": (_I, [_P, ctypes.POINTER(ScanStats)]),
+    "relief_gpu_map_in_flight": (_I, [_P]),
     "relief_gpu_config_load_convnet": (_I, [_P, _CS]),
     "relief_gpu_convnet_infer": (_I, [_P, _DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, _DP]),
     "relief_gpu_shard_ingest": (_I, [_P, _P, ctypes.c_void_p, _SZ, _I, ctypes.c_uint64, ctypes.c_uint64, _DP, _D,
@@ -299,6 +302,20 @@ class ReliefMap:
             self.handle, config.handle if config is not None else None,
             _dptr(xyz) if xyz.size else None, xyz.size // 3, _dptr(pose), stamp, ctypes.byref(st))
         _check(self.lib, status)
+        return st
+
+    def integrate_async(self, xyz, pose, stamp: float, config: Optional[Config] = None) -> None:
+        """relief_gpu_map_integrate_async: enqueue a frame (keep xyz alive until its wait())."""
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1)
+        pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+        _check(self.lib, self.lib.relief_gpu_map_integrate_async(
+            self.handle, config.handle if config else None, xyz.ctypes.data_as(ctypes.c_void_p),
+            xyz.size // 3, _dptr(pose), stamp))
+
+    def wait(self) -> ScanStats:
+        """relief_gpu_map_wait: stats of the oldest frame in flight."""
+        st = ScanStats()
+        _check(self.lib, self.lib.relief_gpu_map_wait(self.handle, ctypes.byref(st)))
         return st
 
     def integrate_device(self, d_xyz_ptr: int, n: int, pose, stamp: float,

@@ -418,6 +418,31 @@ relief_status relief_gpu_smooth_chain(const double* values, const uint8_t* valid
   });
 }
 
+relief_status relief_gpu_map_integrate_async(relief_map* map, const relief_config* config,
+                                            const double* xyz, size_t n_points,
+                                            const double pose[12], double stamp) {
+  if (map == nullptr || pose == nullptr || (xyz == nullptr && n_points > 0))
+    return usage("null argument");
+  return guard([&] {
+    const rb200::Pose p = rb200::Pose::fromRowMajor34(pose);
+    const rb200::PipelineParams params =
+        config ? config->config.pipeline : rb200::PipelineParams{};
+    validateScan(params, p);
+    rb200::DeviceMap& m = *map->dev;
+    const double dt = m.has_last ? std::max(0.0, stamp - m.last_stamp) : 0.0;
+    rb200::integrateScanAsync(m, params, xyz, n_points, p, stamp, dt);
+    m.last_stamp = stamp;
+    m.has_last = true;
+  });
+}
+
+relief_status relief_gpu_map_wait(relief_map* map, relief_scan_stats* stats_out) {
+  if (map == nullptr) return usage("null argument");
+  return guard([&] { fillStats(rb200::waitScan(*map->dev), stats_out); });
+}
+
+int relief_gpu_map_in_flight(const relief_map* map) { return map ? map->dev->async_count : 0; }
+
 relief_status relief_gpu_config_load_convnet(relief_config* config, const char* model_path) {
   if (config == nullptr || model_path == nullptr) return usage("null argument");
   return guard([&] {

@@ -125,6 +125,15 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
     checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
+    checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
+    for (int k = 0; k < DeviceMap::kSlots; ++k) {
+      checkCuda(cudaEventCreate(&m->ev_copied[k]), "event create");
+      checkCuda(cudaEventCreateWithFlags(&m->ev_consumed[k], cudaEventDisableTiming), "event create");
+      checkCuda(cudaEventCreate(&m->ev_done[k]), "event create");
+      checkCuda(cudaEventCreate(&m->ev_copy0[k]), "event create");
+      checkCuda(cudaEventCreate(&m->ev_start[k]), "event create");
+      checkCuda(cudaMallocHost(&m->h_slot[k], sizeof(DevStats)), "pinned stats");
+    }
     const std::size_t n = grid.cells();
     const std::size_t bytes = 2 * layerBytes(n) + 4 * alignUp(n * 4) + alignUp((n + 1) * 4) +
                               alignUp(n) + 6 * kAlign;
@@ -166,6 +175,18 @@ void destroyDeviceMap(DeviceMap* m) {
   cudaFree(m->stats);
   cudaFree(m->drift_offset);
   if (m->h_stats) cudaFreeHost(m->h_stats);
+  for (int k = 0; k < DeviceMap::kSlots; ++k) {
+    if (m->h_slot[k]) cudaFreeHost(m->h_slot[k]);
+    if (m->ev_copied[k]) cudaEventDestroy(m->ev_copied[k]);
+    if (m->ev_consumed[k]) cudaEventDestroy(m->ev_consumed[k]);
+    if (m->ev_done[k]) cudaEventDestroy(m->ev_done[k]);
+    if (m->ev_copy0[k]) cudaEventDestroy(m->ev_copy0[k]);
+    if (m->ev_start[k]) cudaEventDestroy(m->ev_start[k]);
+  }
+  if (m->copy_stream) {
+    cudaStreamSynchronize(m->copy_stream);
+    cudaStreamDestroy(m->copy_stream);
+  }
   for (auto& e : m->ev)
     if (e) cudaEventDestroy(e);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -185,11 +206,12 @@ void ensurePointCapacity(DeviceMap& m, std::size_t n) {
   while (cap < n) cap <<= 1;
   cudaFree(m.pslab);
   m.pslab = nullptr;
-  const std::size_t bytes = alignUp(cap * 24) + 8 * alignUp(cap * 8) + 6 * alignUp(cap * 4) +
-                            alignUp(cap) + 16 * kAlign;
+  const std::size_t bytes = DeviceMap::kSlots * alignUp(cap * 24) + 8 * alignUp(cap * 8) +
+                            6 * alignUp(cap * 4) + alignUp(cap) + 16 * kAlign;
   checkCuda(cudaMalloc(&m.pslab, bytes), "point scratch allocation");
   Carver c{static_cast<char*>(m.pslab)};
-  m.xyz_in = c.take<double>(cap * 3);
+  for (int k = 0; k < DeviceMap::kSlots; ++k) m.xyz_slot[k] = c.take<double>(cap * 3);
+  m.xyz_in = m.xyz_slot[0];
   m.px = c.take<double>(cap);
   m.py = c.take<double>(cap);
   m.pz = c.take<double>(cap);

@@ -160,6 +160,16 @@ struct DeviceMap {
   ChainScratch chain;            // post-processing chain scratch
   ConvScratch conv;              // conv-net traversability scratch
   ShardState shard;              // sharded-frame bookkeeping
+  // Streaming frames (relief_gpu_map_integrate_async / _wait): the input of
+  // frame k+1 is copied on copy_stream while frame k computes; two slots.
+  static constexpr int kSlots = 3;  // frames in flight
+  cudaStream_t copy_stream = nullptr;
+  DevStats* h_slot[kSlots] = {};    // pinned stats of the frames in flight
+  double* xyz_slot[kSlots] = {};    // device input of each slot
+  cudaEvent_t ev_copied[kSlots] = {}, ev_consumed[kSlots] = {}, ev_done[kSlots] = {};
+  cudaEvent_t ev_copy0[kSlots] = {}, ev_start[kSlots] = {};  // timing: copy start, compute start
+  int async_head = 0, async_count = 0;
+  std::size_t async_n[kSlots] = {};
   double* chain_in = nullptr;    // masked input layer of the chain
   double* chain_out = nullptr;   // chain output staging for host callers
   uint8_t* chain_out_ok = nullptr;
@@ -202,6 +212,11 @@ struct ScanResult {
 ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& params, const double* xyz,
                                std::size_t n, bool xyz_on_device, const Pose& pose,
                                double stamp, double dt);
+// Streaming variant: enqueue the frame (host points, ideally pinned) and
+// return; at most two frames in flight, completed in order by waitScan.
+void integrateScanAsync(DeviceMap& m, const PipelineParams& params, const double* xyz,
+                        std::size_t n, const Pose& pose, double stamp, double dt);
+ScanResult waitScan(DeviceMap& m);
 
 // Exact point-batch sharding of one frame: every rank holds a
 // full replica and runs its contiguous batch of the frame's points; the host

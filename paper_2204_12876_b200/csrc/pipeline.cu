@@ -1443,10 +1443,10 @@ void phaseBegin(Frame& f) {
   f.g = gridArgs(m.grid);
 }
 
-// Point scratch + the input stream into HBM; returns the device points.
-const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_device) {
+// Point + reduction scratch for n points.
+void phaseScratch(Frame& f, std::size_t n) {
   DeviceMap& m = f.m;
-  if (n == 0) return xyz;
+  if (n == 0) return;
   ensurePointCapacity(m, n);
   const std::size_t nb = gridFor(n);
   if (m.rcap < nb || m.rslab == nullptr) {
@@ -1461,6 +1461,13 @@ const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_de
     m.drift_local = reinterpret_cast<double*>(
         (reinterpret_cast<uintptr_t>(m.blk + m.rcap + 1) + 255) & ~static_cast<uintptr_t>(255));
   }
+}
+
+// Point scratch + the input stream into HBM; returns the device points.
+const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_device) {
+  DeviceMap& m = f.m;
+  if (n == 0) return xyz;
+  phaseScratch(f, n);
   if (on_device) return xyz;
   checkCuda(cudaMemcpyAsync(m.xyz_in, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, f.s),
             "point upload");
@@ -1709,6 +1716,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
   if (n >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
   if (m.shard.stage != 0) fail(Err::kUsage, "a sharded frame is in progress on this map");
+  if (m.async_count != 0) fail(Err::kUsage, "streaming frames in flight: call relief_gpu_map_wait");
   Frame f(m, P, pose, stamp, dt);
   const uint32_t N = static_cast<uint32_t>(n);
   phaseBegin(f);
@@ -1759,6 +1767,95 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   return out;
 }
 
+// ------------------------------------------------------- streaming frames
+// Same launch sequence as integrateScanDevice, but the points are copied on
+// copy_stream into one of two input slots (waiting until the frame that last
+// used the slot has ingested it), the stats go to that slot's pinned buffer,
+// and nothing waits: frame k+1's PCIe transfer overlaps frame k's kernels.
+void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz, std::size_t n,
+                        const Pose& pose, double stamp, double dt) {
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (n >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
+  if (m.shard.stage != 0) fail(Err::kUsage, "a sharded frame is in progress on this map");
+  if (m.async_count == DeviceMap::kSlots)
+    fail(Err::kUsage, "too many frames in flight: call relief_gpu_map_wait");
+  const int slot = (m.async_head + m.async_count) % DeviceMap::kSlots;
+  // Growing the scratch frees buffers a frame in flight may still use.
+  const bool grows = n > 0 && (n > m.cap || m.pslab == nullptr || gridFor(n) > m.rcap);
+  if (grows && m.async_count > 0) {
+    checkCuda(cudaStreamSynchronize(m.stream), "stream sync");
+    checkCuda(cudaStreamSynchronize(m.copy_stream), "stream sync");
+  }
+  Frame f(m, P, pose, stamp, dt);
+  const uint32_t N = static_cast<uint32_t>(n);
+  phaseBegin(f);
+  phaseScratch(f, n);
+  double* d_xyz = m.xyz_slot[slot];
+  if (n > 0) {
+    checkCuda(cudaStreamWaitEvent(m.copy_stream, m.ev_consumed[slot], 0), "stream wait");
+    checkCuda(cudaEventRecord(m.ev_copy0[slot], m.copy_stream), "event");
+    checkCuda(cudaMemcpyAsync(d_xyz, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, m.copy_stream),
+              "point upload");
+    checkCuda(cudaEventRecord(m.ev_copied[slot], m.copy_stream), "event");
+  }
+  checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
+  const SortGeom sg = phaseSortGeometry(f, N);
+  if (n > 0) checkCuda(cudaStreamWaitEvent(f.s, m.ev_copied[slot], 0), "stream wait");
+  checkCuda(cudaEventRecord(m.ev_start[slot], f.s), "event");
+  checkCuda(cudaEventRecord(m.ev[1], f.s), "event");
+  phaseIngest(f, d_xyz, N, sg, true);
+  checkCuda(cudaEventRecord(m.ev_consumed[slot], f.s), "event");
+  checkCuda(cudaEventRecord(m.ev[2], f.s), "event");
+  if (n > 0 && P.drift.enabled) {
+    k_drift_finalize<<<1, 1024, 0, f.s>>>(m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
+                                          P.drift.min_points, P.drift.max_offset_per_scan,
+                                          m.drift_offset, m.stats);
+    k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, m.drift_offset);
+    f.launches += 2;
+  }
+  checkCuda(cudaEventRecord(m.ev[3], f.s), "event");
+  if (n > 0) {
+    phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
+    phaseRaysPass1(f, N, 0);
+    phaseRemovePass2(f, 0);
+  } else {
+    checkCuda(cudaEventRecord(m.ev[4], f.s), "event");
+    checkCuda(cudaEventRecord(m.ev[5], f.s), "event");
+  }
+  checkCuda(cudaEventRecord(m.ev[6], f.s), "event");
+  phaseCells(f);
+  checkCuda(cudaMemcpyAsync(m.h_slot[slot], m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, f.s),
+            "stats");
+  checkCuda(cudaEventRecord(m.ev_done[slot], f.s), "event");
+  checkCuda(cudaGetLastError(), "kernel launch");
+  m.async_n[slot] = n;
+  ++m.async_count;
+  m.last_launches = f.launches;
+}
+
+ScanResult waitScan(DeviceMap& m) {
+  if (m.async_count == 0) fail(Err::kUsage, "no frame in flight");
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  const int slot = m.async_head;
+  checkCuda(cudaEventSynchronize(m.ev_done[slot]), "integrate");
+  const DevStats d = *m.h_slot[slot];
+  // Device timing of this frame: its copy, and its kernels from the moment
+  // the copy had landed (kernel_seconds[0] / [7]; the other phases are not
+  // separated in streaming mode).
+  float ms_copy = 0.0f, ms_run = 0.0f;
+  if (m.async_n[slot] > 0)
+    checkCuda(cudaEventElapsedTime(&ms_copy, m.ev_copy0[slot], m.ev_copied[slot]), "timing");
+  checkCuda(cudaEventElapsedTime(&ms_run, m.ev_start[slot], m.ev_done[slot]), "timing");
+  for (double& v : m.kernel_seconds) v = 0.0;
+  m.kernel_seconds[0] = ms_copy * 1e-3;
+  m.kernel_seconds[7] = ms_run * 1e-3;
+  m.async_head = (m.async_head + 1) % DeviceMap::kSlots;
+  --m.async_count;
+  if (d.error_code == 1) fail(Err::kInvalidVariance, "variances must be positive");
+  m.last_visits = static_cast<long long>(d.visits);
+  return resultFrom(d, m.async_n[slot]);
+}
+
 // ------------------------------------------------------- sharded frames
 // Phase 1: recenter, this batch's K1, and its fusion records (stable
 // compaction of the in-map kept points) plus the local drift vote and fate
@@ -1767,6 +1864,7 @@ void shardIngest(DeviceMap& m, const PipelineParams& P, const double* xyz, std::
                  bool xyz_on_device, uint64_t ray_offset, uint64_t n_total, const Pose& pose,
                  double stamp, ShardIO& io) {
   checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (m.async_count != 0) fail(Err::kUsage, "streaming frames in flight: call relief_gpu_map_wait");
   if (n_total >= 0x7fffffffULL) fail(Err::kUsage, "too many points in one scan");
   if (ray_offset + n > n_total) fail(Err::kUsage, "shard batch outside the frame");
   // Point scratch sized for the whole frame now: phase 2 sorts all records
