@@ -175,7 +175,7 @@ struct DeviceMap {
   uint8_t* chain_out_ok = nullptr;
   double last_chain_seconds = 0.0;
   int last_chain_launches = 0;
-  cudaEvent_t ev[13] = {};
+  cudaEvent_t ev[14] = {};
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
   long long last_launches = 0;

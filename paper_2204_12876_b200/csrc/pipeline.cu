@@ -1427,9 +1427,9 @@ struct Frame {
 };
 
 // Stats reset + move_to (reference grid.cpp:87-111).
-void phaseBegin(Frame& f) {
+void phaseBegin(Frame& f, bool record_start = true) {
   DeviceMap& m = f.m;
-  checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
+  if (record_start) checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
   checkCuda(cudaMemsetAsync(m.stats, 0, sizeof(DevStats), f.s), "memset");
   const int sx = quantizedShift(f.pose.t[0] - m.grid.center_x, m.grid.resolution);
   const int sy = quantizedShift(f.pose.t[1] - m.grid.center_y, m.grid.resolution);
@@ -1719,11 +1719,15 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   if (m.async_count != 0) fail(Err::kUsage, "streaming frames in flight: call relief_gpu_map_wait");
   Frame f(m, P, pose, stamp, dt);
   const uint32_t N = static_cast<uint32_t>(n);
-  phaseBegin(f);
+  // ev0 -> ev13: the input copy (host input only); everything after it is the
+  // frame's device time (stats / count / tile-count resets, recenter, kernels).
+  checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
   const double* d_xyz = phaseUpload(f, xyz, n, xyz_on_device);
+  checkCuda(cudaEventRecord(m.ev[13], f.s), "event");  // copy done
+  phaseBegin(f, false);
   checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
   const SortGeom sg = phaseSortGeometry(f, N);
-  checkCuda(cudaEventRecord(m.ev[1], f.s), "event");  // upload done
+  checkCuda(cudaEventRecord(m.ev[1], f.s), "event");  // resets done
   phaseIngest(f, d_xyz, N, sg, true);
   checkCuda(cudaEventRecord(m.ev[2], f.s), "event");  // ingest done
   if (n > 0 && P.drift.enabled) {
@@ -1747,14 +1751,19 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   const DevStats& d = phaseStats(f);
   ScanResult out = resultFrom(d, n);
 
-  float ms[7], ms_trav = 0.0f;
-  for (int k = 0; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
+  float ms[7], ms_trav = 0.0f, ms_copy = 0.0f, ms_reset = 0.0f;
+  for (int k = 1; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
   checkCuda(cudaEventElapsedTime(&ms_trav, m.ev[7], m.ev[12]), "timing");
-  // ms: upload, ingest(+shift), drift, sort, fusion, rays, cell phases
+  checkCuda(cudaEventElapsedTime(&ms_copy, m.ev[0], m.ev[13]), "timing");
+  checkCuda(cudaEventElapsedTime(&ms_reset, m.ev[13], m.ev[1]), "timing");
+  // kernel_seconds: upload (input copy), ingest (+ resets / recenter), drift,
+  // sort, fusion, rays, cell phases, total device time after the copy
+  ms[0] = ms_copy;
+  ms[1] += ms_reset;
   for (int k = 0; k < 6; ++k) m.kernel_seconds[k] = ms[k] * 1e-3;
   m.kernel_seconds[6] = (ms[6] + ms_trav) * 1e-3;
   m.kernel_seconds[7] = (ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6] + ms_trav) * 1e-3;
-  m.phase_seconds[0] = ms[1] * 1e-3;                    // point transform & z error count
+  m.phase_seconds[0] = ms[1] * 1e-3;                    // point transform & z error count (+ move_to)
   m.phase_seconds[1] = ms[2] * 1e-3;                    // drift compensation
   m.phase_seconds[2] = (ms[3] + ms[4] + ms[5]) * 1e-3;  // height update & ray casting
   m.phase_seconds[3] = ms[6] * 1e-3;                    // overlap + normals (+ geometric traversability, fused)
