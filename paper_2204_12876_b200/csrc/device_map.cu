@@ -150,6 +150,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
     fillFresh(*m);
+    checkCuda(cudaMemsetAsync(m->count, 0, n * sizeof(int32_t), m->stream), "map init");
     checkCuda(cudaStreamSynchronize(m->stream), "map init");
   } catch (...) {
     destroyDeviceMap(m);

@@ -1288,7 +1288,7 @@ constexpr int kTileX = 32, kTileY = 8;
 // memory tile with a (radius)-cell halo. Overlap is evaluated for halo cells
 // too, so every thread sees the post-clearance validity of its window.
 __global__ void __launch_bounds__(kTileX* kTileY)
-    k_cells(Layers L, const int32_t* __restrict__ count, CellArgs a, DevStats* st) {
+    k_cells(Layers L, int32_t* __restrict__ count, CellArgs a, DevStats* st) {
   extern __shared__ unsigned char smem[];
   const int halo = a.radius > 1 ? a.radius : 1;
   const int tw = kTileX + 2 * halo, th = kTileY + 2 * halo;
@@ -1322,6 +1322,8 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   unsigned long long cleared = 0;
   if (r < H && c < W) {
     const size_t i = static_cast<size_t>(r) * W + c;
+    const int32_t cnt_i = count[i];
+    if (cnt_i != 0) count[i] = 0;  // last reader this scan: ready for the next one
     const int lr = threadIdx.y + halo, lc = threadIdx.x + halo;
     const bool was_valid = L.valid[i] != 0;
     const bool ok = sv[lr * tw + lc] != 0;
@@ -1383,7 +1385,7 @@ __global__ void __launch_bounds__(kTileX* kTileY)
         trav = a.w_slope * s_slope + a.w_step * s_step + a.w_rough * s_rough;
       }
       if (a.geo_trav) L.trav[i] = trav;
-      if (a.time_var && count[i] == 0) L.var[i] = smin(L.var[i] + a.growth, a.sigma_max2);
+      if (a.time_var && cnt_i == 0) L.var[i] = smin(L.var[i] + a.growth, a.sigma_max2);
     }
   }
   cleared = warpSum(cleared);
@@ -1725,7 +1727,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   const double* d_xyz = phaseUpload(f, xyz, n, xyz_on_device);
   checkCuda(cudaEventRecord(m.ev[13], f.s), "event");  // copy done
   phaseBegin(f, false);
-  checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
+  // count[] is all zero here: k_cells clears it after its last use each scan.
   const SortGeom sg = phaseSortGeometry(f, N);
   checkCuda(cudaEventRecord(m.ev[1], f.s), "event");  // resets done
   phaseIngest(f, d_xyz, N, sg, true);
@@ -1807,8 +1809,7 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
               "point upload");
     checkCuda(cudaEventRecord(m.ev_copied[slot], m.copy_stream), "event");
   }
-  checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
-  const SortGeom sg = phaseSortGeometry(f, N);
+  const SortGeom sg = phaseSortGeometry(f, N);  // count[] is zero (cleared by k_cells)
   if (n > 0) checkCuda(cudaStreamWaitEvent(f.s, m.ev_copied[slot], 0), "stream wait");
   checkCuda(cudaEventRecord(m.ev_start[slot], f.s), "event");
   checkCuda(cudaEventRecord(m.ev[1], f.s), "event");
