@@ -286,3 +286,17 @@ def test_sort_pass_count_paths(gpu, reference, tmp_path, W, H):
         z = -1.0 + 0.05 * rng.standard_normal(n)
         pair.integrate(np.column_stack([xy, z]), pose, 0.1 * scan, context=f"{W}x{H} scan {scan}")
         pair.compare(context=f"{W}x{H} scan {scan}")
+
+
+def test_frame_sizes_changing_between_scans(gpu, reference, tmp_path):
+    """Scratch sized by the largest frame, sort tile counts reused across scans of different
+    sizes (tile-count layout changes with N), empty scans in between."""
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\nupdate.sigma_outlier2 = 0.02\n",
+                0.04, 150, 150)
+    rng = np.random.default_rng(21)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    for scan, n in enumerate([20000, 3, 0, 70000, 5000, 2048, 2049, 150000, 1]):
+        xy = rng.normal(0.0, 1.2, (n, 2))
+        z = -1.0 + 0.05 * rng.standard_normal(n)
+        pair.integrate(np.column_stack([xy, z]), pose, 0.1 * scan, context=f"n={n}")
+        pair.compare(context=f"n={n}")
