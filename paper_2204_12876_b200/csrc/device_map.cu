@@ -135,8 +135,8 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
       checkCuda(cudaMallocHost(&m->h_slot[k], sizeof(DevStats)), "pinned stats");
     }
     const std::size_t n = grid.cells();
-    const std::size_t bytes = 2 * layerBytes(n) + 4 * alignUp(n * 4) + alignUp((n + 1) * 4) +
-                              alignUp(n) + 6 * kAlign;
+    const std::size_t bytes = 2 * layerBytes(n) + 5 * alignUp(n * 4) + alignUp((n + 1) * 4) +
+                              alignUp(n) + 7 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
     Carver c{static_cast<char*>(m->slab)};
     carveLayers(c, m->cur, n);
@@ -146,6 +146,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     m->heavy = c.take<uint32_t>(2 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
+    m->probe = c.take<uint32_t>(n);
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");

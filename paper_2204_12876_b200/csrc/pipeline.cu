@@ -852,10 +852,26 @@ struct RayArgs {
 // those cells are classified "none" up front; k_fuse_heavy flags any heavy
 // cell that fused nothing and the ray pass is then redone (retry = 1: this
 // kernel and pass 1 run only if the flag is set).
+// Pass-1 probe word of a cell: the ray class in the low 2 bits and, above it,
+// an f32 bound F >= T of the cell's gate threshold T (T = upper_bound for a
+// bound cell, elevation - sqrt(variance) for a removal candidate), so that a
+// visit with ray height h >= F is rejected without loading the cell state:
+// the reference's own test (h < ub, resp. !(h >= elev - sqrt(var))) rejects it
+// too. F is T rounded up to f32 and then up again to a multiple of 4 ulps
+// (for negative values: towards zero), NaN thresholds become +inf.
+__device__ __forceinline__ uint32_t probeWord(uint8_t cls, double t) {
+  if (cls == kClsNone) return 0u;
+  const float f = (t == t) ? __double2float_ru(t) : __int_as_float(0x7f800000);
+  uint32_t b = __float_as_uint(f);
+  b = (b >> 31) ? (b & ~3u) : ((b + 3u) & ~3u);
+  return b | cls;
+}
+
 __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayArgs a, uint8_t* cls,
                                                        int32_t* kstar,
                                                        const int32_t* __restrict__ count,
-                                                       int heavy, int retry, DevStats* st) {
+                                                       int heavy, int retry, DevStats* st,
+                                                       uint32_t* probe) {
   if (retry) {
     if (!st->respeculate) return;
     __syncthreads();
@@ -867,15 +883,19 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     uint8_t c = kClsNone;
+    double t = 0.0;
     if (heavy >= 0 && count[i] > heavy) {
       c = kClsNone;
     } else if (!L.valid[i]) {
       c = a.bound ? kClsBound : kClsNone;
+      if (c) t = L.ub[i];
     } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
                (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
       c = kClsCandidate;
+      t = L.elev[i] - sqrt(L.var[i]);
     }
     cls[i] = c;
+    probe[i] = probeWord(c, t);
     kstar[i] = INT_MAX;
   }
 }
@@ -1097,6 +1117,7 @@ __device__ __forceinline__ void candidateVisit(const Layers& L, uint32_t c, doub
 
 struct Pass1Ctx {
   const uint8_t* cls;
+  const uint32_t* probe;
   Layers L;
   int32_t* kstar;
   double oz, dz, vx, vy, alpha_n;
@@ -1164,8 +1185,8 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   // reference's bounds test after a step, raycast.cpp:121,125).
   int xl = step_col > 0 ? g.W - 1 - col : (step_col < 0 ? col : 0);
   int yl = step_row > 0 ? g.H - 1 - row : (step_row < 0 ? row : 0);
-  const uint8_t* __restrict__ cls = c.cls;
-  uint8_t cl = cls[idx];
+  const uint32_t* __restrict__ probe = c.probe;
+  uint32_t wd = probe[idx];
   double t_enter = t0;
   // The axis step is written without branches around it (both sides predicate
   // cleanly: the exit tests are hoisted), and the step counters double as the
@@ -1185,8 +1206,13 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     const double m = sx ? tmx : tmy;
     const bool more = m < t1;
     const double t_next = more ? m : t1;
-    if (cl != 0 && idx != end_idx && t_next > t_enter)
-      pass1Visit(c, cl, idx, c.oz + (0.5 * (t_enter + t_next)) * c.dz, touched);
+    if ((wd & 3u) != 0 && idx != end_idx && t_next > t_enter) {
+      const double h = c.oz + (0.5 * (t_enter + t_next)) * c.dz;
+      const uint8_t tag = static_cast<uint8_t>(wd & 3u);
+      if (tag == kClsCandidate) touched = true;
+      // probe filter: h >= F implies the exact gate rejects (see probeWord)
+      if (!(h >= static_cast<double>(__uint_as_float(wd & ~3u)))) pass1Visit(c, tag, idx, h, touched);
+    }
     const int lim = sx ? xl : yl;
     if (!more || lim == 0) break;
     if (sx) {
@@ -1198,7 +1224,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     }
     const int inc = sx ? step_col : step_idx_row;
     idx += inc;
-    cl = cls[idx];
+    wd = probe[idx];
     t_enter = t_next;
   }
   visits += static_cast<unsigned>((xl0 - xl) + (yl0 - yl) + 1);
@@ -1211,14 +1237,14 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
-                 DevStats* st, int retry, uint32_t ray_base) {
+                 DevStats* st, int retry, uint32_t ray_base, const uint32_t* __restrict__ probe) {
   if (retry && !st->respeculate) return;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   bool touched = false;
   unsigned visits = 0;
   if (k < n && kept[k]) {
     const double ex = px[k], ey = py[k], ez = pz[k];
-    Pass1Ctx c{cls, L, kstar, a.o[2], ez - a.o[2], ex - a.o[0], ey - a.o[1], a.alpha_n,
+    Pass1Ctx c{cls, probe, L, kstar, a.o[2], ez - a.o[2], ex - a.o[0], ey - a.o[1], a.alpha_n,
                static_cast<int32_t>(ray_base + k)};  // global ray id (sharded frames)
     if (isfinite(c.vx) && isfinite(c.vy)) {
       pass1Finite(a.g, a.o, ex, ey, c, touched, visits);
@@ -1618,11 +1644,11 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
   const RayArgs ra = rayArgs(f);
   if (ra.cleanup || ra.bound) {
     k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
-                                                        f.overlap ? f.heavy : -1, 0, m.stats);
+                                                        f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
       k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 0, ray_base);
+                                                   m.kstar, m.raylist, m.stats, 0, ray_base, m.probe);
       ++f.launches;
     }
   }
@@ -1631,11 +1657,11 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
     // nothing (both kernels return immediately otherwise).
     checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
     k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
-                                                        -1, 1, m.stats);
+                                                        -1, 1, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
       k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 1, ray_base);
+                                                   m.kstar, m.raylist, m.stats, 1, ray_base, m.probe);
       ++f.launches;
     }
   }
