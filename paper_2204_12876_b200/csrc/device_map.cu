@@ -146,7 +146,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     m->heavy = c.take<uint32_t>(2 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
-    m->probe = c.take<uint32_t>(n);
+    m->probe = c.take<uint16_t>(n);
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");

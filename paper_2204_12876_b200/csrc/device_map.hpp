@@ -119,7 +119,7 @@ struct DeviceMap {
   int32_t* count = nullptr;
   uint32_t* start = nullptr;
   uint8_t* cls = nullptr;
-  uint32_t* probe = nullptr;  // pass-1 probe words (class + conservative gate bound)
+  uint16_t* probe = nullptr;  // pass-1 probe words (class + conservative gate bound)
   int32_t* kstar = nullptr;
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
   // per-point scratch (grown on demand)

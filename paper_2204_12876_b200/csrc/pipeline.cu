@@ -18,6 +18,7 @@
 //   K6  k_rays_pass2     bounds of removed cells from rays k >= k*
 //   K7  k_cells          overlap clearance + normals + traversability + time
 //                        variance, one shared-memory tile with a halo
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -852,26 +853,33 @@ struct RayArgs {
 // those cells are classified "none" up front; k_fuse_heavy flags any heavy
 // cell that fused nothing and the ray pass is then redone (retry = 1: this
 // kernel and pass 1 run only if the flag is set).
-// Pass-1 probe word of a cell: the ray class in the low 2 bits and, above it,
-// an f32 bound F >= T of the cell's gate threshold T (T = upper_bound for a
-// bound cell, elevation - sqrt(variance) for a removal candidate), so that a
-// visit with ray height h >= F is rejected without loading the cell state:
-// the reference's own test (h < ub, resp. !(h >= elev - sqrt(var))) rejects it
-// too. F is T rounded up to f32 and then up again to a multiple of 4 ulps
-// (for negative values: towards zero), NaN thresholds become +inf.
-__device__ __forceinline__ uint32_t probeWord(uint8_t cls, double t) {
+// Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
+// above it, an f16 bound F >= T of the cell's gate threshold T (T =
+// upper_bound for a bound cell, elevation - sqrt(variance) for a removal
+// candidate), so that a visit with ray height h >= F is rejected without
+// loading the cell state: the reference's own test (h < ub, resp.
+// !(h >= elev - sqrt(var))) rejects it too. F is T rounded up (double -> f32
+// -> f16) and then up again to a multiple of 4 ulps (for negative values:
+// towards zero); NaN thresholds become +inf, values beyond the f16 range +inf
+// or -65504 (both still >= T).
+typedef uint16_t ProbeT;
+__device__ __forceinline__ ProbeT probeWord(uint8_t cls, double t) {
   if (cls == kClsNone) return 0u;
-  const float f = (t == t) ? __double2float_ru(t) : __int_as_float(0x7f800000);
-  uint32_t b = __float_as_uint(f);
-  b = (b >> 31) ? (b & ~3u) : ((b + 3u) & ~3u);
-  return b | cls;
+  // up-rounded twice (double -> f32 -> f16) stays >= t
+  const __half hf = (t == t) ? __float2half_ru(__double2float_ru(t)) : __ushort_as_half(0x7c00);
+  uint32_t b = __half_as_ushort(hf);
+  b = (b >> 15) ? (b & ~3u) : ((b + 3u) & ~3u);
+  return static_cast<ProbeT>(b | cls);
+}
+__device__ __forceinline__ double probeBound(uint32_t w) {
+  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & ~3u))));
 }
 
 __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayArgs a, uint8_t* cls,
                                                        int32_t* kstar,
                                                        const int32_t* __restrict__ count,
                                                        int heavy, int retry, DevStats* st,
-                                                       uint32_t* probe) {
+                                                       ProbeT* probe) {
   if (retry) {
     if (!st->respeculate) return;
     __syncthreads();
@@ -1117,7 +1125,7 @@ __device__ __forceinline__ void candidateVisit(const Layers& L, uint32_t c, doub
 
 struct Pass1Ctx {
   const uint8_t* cls;
-  const uint32_t* probe;
+  const ProbeT* probe;
   Layers L;
   int32_t* kstar;
   double oz, dz, vx, vy, alpha_n;
@@ -1185,7 +1193,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   // reference's bounds test after a step, raycast.cpp:121,125).
   int xl = step_col > 0 ? g.W - 1 - col : (step_col < 0 ? col : 0);
   int yl = step_row > 0 ? g.H - 1 - row : (step_row < 0 ? row : 0);
-  const uint32_t* __restrict__ probe = c.probe;
+  const ProbeT* __restrict__ probe = c.probe;
   uint32_t wd = probe[idx];
   double t_enter = t0;
   // The axis step is written without branches around it (both sides predicate
@@ -1211,7 +1219,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
       const uint8_t tag = static_cast<uint8_t>(wd & 3u);
       if (tag == kClsCandidate) touched = true;
       // probe filter: h >= F implies the exact gate rejects (see probeWord)
-      if (!(h >= static_cast<double>(__uint_as_float(wd & ~3u)))) pass1Visit(c, tag, idx, h, touched);
+      if (!(h >= probeBound(wd))) pass1Visit(c, tag, idx, h, touched);
     }
     const int lim = sx ? xl : yl;
     if (!more || lim == 0) break;
@@ -1237,7 +1245,7 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
-                 DevStats* st, int retry, uint32_t ray_base, const uint32_t* __restrict__ probe) {
+                 DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe) {
   if (retry && !st->respeculate) return;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   bool touched = false;
