@@ -123,11 +123,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
   m->grid = grid;
   try {
     checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
-    // The long-cell fold outranks the concurrently launched ray pass: its few
-    // blocks must be resident first, they carry the fusion tail.
-    int prio_lo = 0, prio_hi = 0;
-    checkCuda(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
-    checkCuda(cudaStreamCreateWithPriority(&m->stream2, cudaStreamNonBlocking, prio_hi), "stream create");
+    checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
     for (int k = 0; k < DeviceMap::kSlots; ++k) {

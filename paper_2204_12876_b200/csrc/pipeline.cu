@@ -568,60 +568,6 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ------------------------------------------------------------- K3 fusion
-// Ray classes of a cell for the ray pass (reference raycast.cpp:132-183 gates
-// that do not depend on the ray).
-enum : uint8_t { kClsNone = 0, kClsBound = 1, kClsCandidate = 2 };
-
-// Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
-// above it, an f16 bound F >= T of the cell's gate threshold T (T =
-// upper_bound for a bound cell, elevation - sqrt(variance) for a removal
-// candidate), so that a visit with ray height h >= F is rejected without
-// loading the cell state: the reference's own test (h < ub, resp.
-// !(h >= elev - sqrt(var))) rejects it too. F is T rounded up (double -> f32
-// -> f16) and then up again to a multiple of 4 ulps (for negative values:
-// towards zero); NaN thresholds become +inf, values beyond the f16 range +inf
-// or -65504 (both still >= T).
-typedef uint16_t ProbeT;
-__device__ __forceinline__ ProbeT probeWord(uint8_t cls, double t) {
-  if (cls == kClsNone) return 0u;
-  // up-rounded twice (double -> f32 -> f16) stays >= t
-  const __half hf = (t == t) ? __float2half_ru(__double2float_ru(t)) : __ushort_as_half(0x7c00);
-  uint32_t b = __half_as_ushort(hf);
-  b = (b >> 15) ? (b & ~3u) : ((b + 3u) & ~3u);
-  return static_cast<ProbeT>(b | cls);
-}
-__device__ __forceinline__ double probeBound(uint32_t w) {
-  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & ~3u))));
-}
-
-struct ClassArgs {
-  double now, t_free;
-  int cleanup, bound;
-};
-
-// Class, probe word and k* reset of cell i from its post-fusion state; a
-// cell still being folded on the side stream (spec_none) is speculatively
-// "none".
-__device__ __forceinline__ void writeClass(const Layers& L, size_t i, bool spec_none,
-                                           const ClassArgs& a, uint8_t* cls, ProbeT* probe,
-                                           int32_t* kstar) {
-  uint8_t c = kClsNone;
-  double t = 0.0;
-  if (spec_none) {
-    c = kClsNone;
-  } else if (!L.valid[i]) {
-    c = a.bound ? kClsBound : kClsNone;
-    if (c) t = L.ub[i];
-  } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
-             (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
-    c = kClsCandidate;
-    t = L.elev[i] - sqrt(L.var[i]);
-  }
-  cls[i] = c;
-  probe[i] = probeWord(c, t);
-  kstar[i] = INT_MAX;
-}
-
 struct FuseArgs {
   double now;
   double sigma_init2, sigma_outlier2, sigma_max2, maha, maha2;
@@ -775,8 +721,7 @@ __global__ void __launch_bounds__(kThreads)
     k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
            const uint32_t* __restrict__ start, const double* __restrict__ spz,
            const double* __restrict__ spv, FuseArgs a, DevStats* st, int heavy,
-           uint32_t* heavy_list, uint32_t* vheavy_list, int classify, ClassArgs ca,
-           uint8_t* cls, ProbeT* probe, int32_t* kstar) {
+           uint32_t* heavy_list, uint32_t* vheavy_list) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const int cnt = i < ncell ? count[i] : 0;
   const bool is_heavy = cnt > heavy;
@@ -800,9 +745,6 @@ __global__ void __launch_bounds__(kThreads)
   }
   FoldCounts k;
   if (cnt > 0 && !is_heavy) foldCell(L, i, cnt, start, spz, spv, a, st, k);
-  // The ray classes follow from the post-fusion state, so they are written
-  // here, after the cell's own fold (no separate classification pass).
-  if (classify && i < ncell) writeClass(L, i, is_heavy, ca, cls, probe, kstar);
   flushCounts(k, st);
 }
 
@@ -893,6 +835,7 @@ __global__ void __launch_bounds__(32)
 }
 
 // ------------------------------------------------------------- K5/K6 rays
+enum : uint8_t { kClsNone = 0, kClsBound = 1, kClsCandidate = 2 };
 
 struct RayArgs {
   GridArgs g;
@@ -910,6 +853,28 @@ struct RayArgs {
 // those cells are classified "none" up front; k_fuse_heavy flags any heavy
 // cell that fused nothing and the ray pass is then redone (retry = 1: this
 // kernel and pass 1 run only if the flag is set).
+// Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
+// above it, an f16 bound F >= T of the cell's gate threshold T (T =
+// upper_bound for a bound cell, elevation - sqrt(variance) for a removal
+// candidate), so that a visit with ray height h >= F is rejected without
+// loading the cell state: the reference's own test (h < ub, resp.
+// !(h >= elev - sqrt(var))) rejects it too. F is T rounded up (double -> f32
+// -> f16) and then up again to a multiple of 4 ulps (for negative values:
+// towards zero); NaN thresholds become +inf, values beyond the f16 range +inf
+// or -65504 (both still >= T).
+typedef uint16_t ProbeT;
+__device__ __forceinline__ ProbeT probeWord(uint8_t cls, double t) {
+  if (cls == kClsNone) return 0u;
+  // up-rounded twice (double -> f32 -> f16) stays >= t
+  const __half hf = (t == t) ? __float2half_ru(__double2float_ru(t)) : __ushort_as_half(0x7c00);
+  uint32_t b = __half_as_ushort(hf);
+  b = (b >> 15) ? (b & ~3u) : ((b + 3u) & ~3u);
+  return static_cast<ProbeT>(b | cls);
+}
+__device__ __forceinline__ double probeBound(uint32_t w) {
+  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & ~3u))));
+}
+
 __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayArgs a, uint8_t* cls,
                                                        int32_t* kstar,
                                                        const int32_t* __restrict__ count,
@@ -923,10 +888,24 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
       st->visits = 0;
     }
   }
-  const ClassArgs ca{a.now, a.t_free, a.cleanup, a.bound};
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x)
-    writeClass(L, i, heavy >= 0 && count[i] > heavy, ca, cls, probe, kstar);
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    uint8_t c = kClsNone;
+    double t = 0.0;
+    if (heavy >= 0 && count[i] > heavy) {
+      c = kClsNone;
+    } else if (!L.valid[i]) {
+      c = a.bound ? kClsBound : kClsNone;
+      if (c) t = L.ub[i];
+    } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
+               (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
+      c = kClsCandidate;
+      t = L.elev[i] - sqrt(L.var[i]);
+    }
+    cls[i] = c;
+    probe[i] = probeWord(c, t);
+    kstar[i] = INT_MAX;
+  }
 }
 
 // Liang-Barsky slab clip (reference raycast.cpp:30-42).
@@ -1490,7 +1469,6 @@ struct Frame {
   GridArgs g;
   long long launches = 0;
   bool overlap = false;  // heavy cells folded on stream2 during the ray pass
-  bool classified = false;  // k_fuse wrote the ray classes
   int heavy = INT_MAX;
   Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
       : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
@@ -1638,11 +1616,8 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
   f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
   f.heavy = f.overlap ? kHeavyCell : INT_MAX;
-  const ClassArgs ca{f.stamp, f.P.cleanup.t_free, cleanup, bound};
-  f.classified = cleanup || bound;
   k_fuse<<<gridFor(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
-                                               m.stats, f.heavy, m.heavy, m.heavy + f.ncell,
-                                               f.classified ? 1 : 0, ca, m.cls, m.probe, m.kstar);
+                                               m.stats, f.heavy, m.heavy, m.heavy + f.ncell);
   ++f.launches;
   if (f.overlap) {
     checkCuda(cudaEventRecord(m.ev[10], s), "event");
@@ -1676,11 +1651,9 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
   cudaStream_t s = f.s;
   const RayArgs ra = rayArgs(f);
   if (ra.cleanup || ra.bound) {
-    if (!f.classified) {  // fusion did not run (no points): classify here
-      k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
-                                                          f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
-      ++f.launches;
-    }
+    k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
+                                                        f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
+    ++f.launches;
     if (N > 0) {
       k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
                                                    m.kstar, m.raylist, m.stats, 0, ray_base, m.probe);
