@@ -498,19 +498,6 @@ __global__ void __launch_bounds__(kThreads)
   }
   const uint32_t n = pass == 0 ? n_in : nkeys;
   __syncthreads();
-  if (last) {
-    // Every pass's counts for this tile have been consumed (this block read
-    // its own column above; earlier passes are complete): zero them for the
-    // next scan.
-    for (int q = threadIdx.x; q < sg.passes * buckets; q += kThreads)
-      sg.tc[static_cast<size_t>(q) * sg.pitch + tile] = 0;
-    // The row scan also wrote the padding columns [ntiles, pitch): the last
-    // tile's block clears them.
-    if (tile == sg.ntiles - 1)
-      for (uint32_t pad = sg.ntiles; pad < sg.pitch; ++pad)
-        for (int q = threadIdx.x; q < sg.passes * buckets; q += kThreads)
-          sg.tc[static_cast<size_t>(q) * sg.pitch + pad] = 0;
-  }
   uint16_t* my = wcnt + warp * buckets;
   const unsigned lt = (1u << lane) - 1u;
   const uint32_t wbase = tile * kTile + warp * (kTile / 8);
@@ -1536,18 +1523,15 @@ SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
   sg.pitch = (sg.ntiles + 3) & ~3u;
   const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
   const std::size_t need = tcn + static_cast<std::size_t>(sg.passes) * sg.buckets();
-  // Layout: row totals first (a fixed size per map), then the tile counts.
-  // The tile counts are zero between scans -- zeroed at allocation, then by
-  // the last scatter pass for every tile it used -- so no per-scan memset.
   if (m.hist_cap < need) {
     cudaFree(m.hist);
     m.hist = nullptr;
     m.hist_cap = need;
     checkCuda(cudaMalloc(&m.hist, m.hist_cap * sizeof(uint32_t)), "sort scratch");
-    checkCuda(cudaMemsetAsync(m.hist, 0, m.hist_cap * sizeof(uint32_t), f.s), "memset");
   }
-  sg.rowsum = m.hist;
-  sg.tc = m.hist + static_cast<std::size_t>(sg.passes) * sg.buckets();
+  sg.tc = m.hist;
+  sg.rowsum = m.hist + tcn;
+  checkCuda(cudaMemsetAsync(sg.tc, 0, tcn * sizeof(uint32_t), f.s), "memset");
   return sg;
 }
 
