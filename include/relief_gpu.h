@@ -91,6 +91,12 @@ RELIEF_API relief_status relief_gpu_smooth_chain(const double* values, const uin
                                                  int n_steps, double* values_out,
                                                  uint8_t* valid_out);
 
+/* Page-locked host buffer for point clouds (cudaHostAlloc, portable): the
+ * H2D copy inside relief_map_integrate / _async then runs at full PCIe speed.
+ * NULL on failure. */
+RELIEF_API void* relief_gpu_host_alloc(size_t bytes);
+RELIEF_API void relief_gpu_host_free(void* ptr);
+
 /* Streaming integrate for sensor pipelines: enqueues the frame (xyz in host
  * memory -- pinned memory lets the copy run asynchronously) and returns. Frames
  * are processed in call order; the PCIe copy of frame k+1 overlaps the kernels

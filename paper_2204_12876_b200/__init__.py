@@ -129,6 +129,8 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_map_chain_seconds": (_D, [_P]),
     "relief_gpu_smooth_chain": (_I, [_DP, ctypes.POINTER(ctypes.c_uint8), _I, _I, ctypes.POINTER(_I),
                                      ctypes.POINTER(_I), _DP, _I, _DP, ctypes.POINTER(ctypes.c_uint8)]),
+    "relief_gpu_host_alloc": (ctypes.c_void_p, [_SZ]),
+    "relief_gpu_host_free": (None, [ctypes.c_void_p]),
     "relief_gpu_map_integrate_async": (_I, [_P, _P, ctypes.c_void_p, _SZ, _DP, _D]),
     "relief_gpu_map_wait": (_I, [_P, ctypes.POINTER(ScanStats)]),
     "relief_gpu_map_in_flight": (_I, [_P]),
@@ -407,6 +409,28 @@ def convnet_infer(lib, config: "Config", layer: np.ndarray, valid: np.ndarray) -
                                              valid.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), W, H,
                                              _dptr(out)))
     return out
+
+
+class PinnedArray:
+    """(n, 3) float64 points in page-locked memory from relief_gpu_host_alloc."""
+
+    def __init__(self, lib, src: np.ndarray):
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        self.lib = lib
+        self.ptr = lib.relief_gpu_host_alloc(max(src.nbytes, 8))
+        if not self.ptr:
+            raise ReliefError(2, lib.relief_last_error().decode())
+        buf = (ctypes.c_double * max(src.size, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=np.float64, count=src.size).reshape(src.shape)
+        self.array[...] = src
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.lib.relief_gpu_host_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
 
 
 def sim_render(lib, config_path, pose, time: float, seed: int, scan_index: int,

@@ -418,6 +418,20 @@ relief_status relief_gpu_smooth_chain(const double* values, const uint8_t* valid
   });
 }
 
+void* relief_gpu_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    t_last_error = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void relief_gpu_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 relief_status relief_gpu_map_integrate_async(relief_map* map, const relief_config* config,
                                             const double* xyz, size_t n_points,
                                             const double pose[12], double stamp) {

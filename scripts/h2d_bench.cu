@@ -2,6 +2,7 @@
 // memory (1, 2, 4 streams) vs a kernel reading mapped pinned memory directly.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 scripts/h2d_bench.cu -o /tmp/h2d
 #include <cstdio>
+#include <cstring>
 #include <cuda_runtime.h>
 
 __global__ void k_read(const double* __restrict__ src, double* __restrict__ dst, size_t n) {
@@ -62,6 +63,25 @@ int main() {
       printf("zero-copy kernel %s blocks=%d: %.1f us  %.1f GB/s\n", v ? "f64x2" : "f64", blocks, best * 1e3,
              bytes / (best * 1e-3) / 1e9);
     }
+  }
+  // 8 distinct pinned frames copied in turn (what bench.py's e2e leg does)
+  {
+    double* hs[8];
+    for (auto& b : hs) {
+      cudaHostAlloc(&b, bytes, cudaHostAllocDefault);
+      memset(b, 1, bytes);
+    }
+    float tot = 0;
+    for (int it = 0; it < 16; ++it) {
+      cudaEventRecord(a, s[0]);
+      cudaMemcpyAsync(d, hs[it % 8], bytes, cudaMemcpyHostToDevice, s[0]);
+      cudaEventRecord(b, s[0]);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (it >= 8) tot += ms;
+    }
+    printf("memcpy cycling 8 pinned buffers: %.1f us  %.1f GB/s\n", tot / 8 * 1e3, bytes / (tot / 8 * 1e-3) / 1e9);
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
