@@ -829,6 +829,9 @@ struct RayArgs {
   double o[3];  // sensor origin = pose translation
   double now, t_free, alpha_n;
   int cleanup, bound;
+  // Per-frame ray constants: the origin lies in the closed map extent, and its
+  // cell (the start cell of every ray that is not clipped at its start).
+  int origin_in, ocol, orow;
 };
 
 // Post-fusion ray class per cell; also resets k* (reference raycast.cpp:
@@ -1133,13 +1136,24 @@ __device__ __forceinline__ void pass1Visit(const Pass1Ctx& c, uint8_t cl, uint32
 // with the class probe software-pipelined -- the next cell's class byte is
 // loaded before the current cell is handled, so the L1 latency overlaps the
 // current visit. Visit side effects (bound min, k* min) are order independent.
+//
+// Setup shortcuts, each equal to the reference's arithmetic:
+// * |dx| or |dy| >= 2e-12 implies hypot(dx, dy) >= 1e-12 (hypot is within an
+//   ulp of a value >= max(|dx|, |dy|)), so the vertical test needs no hypot;
+// * origin and endpoint both in the map: the four Liang-Barsky clips leave
+//   t0 = 0, t1 = 1 (every q >= 0, and q >= |p| on the side the ray moves
+//   towards because fl(xmax - o) >= fl(px - o) when px < xmax), so the start
+//   cell is the origin's (RayArgs::ocol/orow);
+// * the endpoint's cell is the point's cell from k_ingest (same expression
+//   floor((p - origin) / res), in range so the clamp is the identity) when
+//   that is known (pcell < W*H).
 __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3], double px,
                                             double py, const Pass1Ctx& c, bool& touched,
-                                            unsigned& visits) {
+                                            unsigned& visits, const RayArgs& a, uint32_t pcell) {
   const double dx = px - o[0];
   const double dy = py - o[1];
   const double res = g.res;
-  if (libm_hypot(dx, dy) < 1e-12) {
+  if (!(fabs(dx) >= 2e-12 || fabs(dy) >= 2e-12) && libm_hypot(dx, dy) < 1e-12) {
     if (o[0] >= g.ox && o[0] < g.xmax && o[1] >= g.oy && o[1] < g.ymax) {
       const uint32_t idx =
           static_cast<uint32_t>(clampCell(x86_to_int(floor((o[1] - g.oy) / res)), g.H)) * g.W +
@@ -1151,28 +1165,40 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     return;
   }
   double t0 = 0.0, t1 = 1.0;
-  if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return;
-  if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return;
-  if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return;
-  if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
-  if (t0 >= t1) return;
   const bool end_in = px >= g.ox && px < g.xmax && py >= g.oy && py < g.ymax;
+  if (!(a.origin_in && end_in)) {
+    if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return;
+    if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return;
+    if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return;
+    if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
+    if (t0 >= t1) return;
+  }
   uint32_t end_idx = 0xffffffffu;
-  if (end_in)
-    end_idx = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H)) * g.W +
-              clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
-  int col = clampCell(x86_to_int(floor(((o[0] + t0 * dx) - g.ox) / res)), g.W);
-  int row = clampCell(x86_to_int(floor(((o[1] + t0 * dy) - g.oy) / res)), g.H);
+  if (end_in) {
+    if (pcell < static_cast<uint32_t>(g.W) * static_cast<uint32_t>(g.H))
+      end_idx = pcell;
+    else
+      end_idx = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H)) * g.W +
+                clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
+  }
+  int col = a.ocol, row = a.orow;
+  if (t0 != 0.0) {
+    col = clampCell(x86_to_int(floor(((o[0] + t0 * dx) - g.ox) / res)), g.W);
+    row = clampCell(x86_to_int(floor(((o[1] + t0 * dy) - g.oy) / res)), g.H);
+  }
   const int step_col = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
   const int step_row = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
   double tmx = kInf, tmy = kInf, tdx = kInf, tdy = kInf;
+  // t_max and t_delta share the divisor |d| (a / -b == -(a / b) exactly).
   if (step_col != 0) {
-    tmx = ((g.ox + (col + (step_col > 0 ? 1 : 0)) * res) - o[0]) / dx;
-    tdx = res / fabs(dx);
+    double q;
+    div2_rn(res, (g.ox + (col + (step_col > 0 ? 1 : 0)) * res) - o[0], fabs(dx), tdx, q);
+    tmx = dx < 0.0 ? -q : q;
   }
   if (step_row != 0) {
-    tmy = ((g.oy + (row + (step_row > 0 ? 1 : 0)) * res) - o[1]) / dy;
-    tdy = res / fabs(dy);
+    double q;
+    div2_rn(res, (g.oy + (row + (step_row > 0 ? 1 : 0)) * res) - o[1], fabs(dy), tdy, q);
+    tmy = dy < 0.0 ? -q : q;
   }
   uint32_t idx = static_cast<uint32_t>(row) * g.W + col;
   const int step_idx_row = step_row * g.W;
@@ -1232,7 +1258,8 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
-                 DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe) {
+                 DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
+                 const uint32_t* __restrict__ pcell) {
   if (retry && !st->respeculate) return;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   bool touched = false;
@@ -1242,7 +1269,7 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
     Pass1Ctx c{cls, probe, L, kstar, a.o[2], ez - a.o[2], ex - a.o[0], ey - a.o[1], a.alpha_n,
                static_cast<int32_t>(ray_base + k)};  // global ray id (sharded frames)
     if (isfinite(c.vx) && isfinite(c.vy)) {
-      pass1Finite(a.g, a.o, ex, ey, c, touched, visits);
+      pass1Finite(a.g, a.o, ex, ey, c, touched, visits, a, pcell ? pcell[k] : 0xffffffffu);
     } else {
       walkRay(a.g, a.o, ex, ey, [&](uint32_t cell, double te, double tn, bool vertical) {
         ++visits;
@@ -1456,6 +1483,9 @@ struct Frame {
   GridArgs g;
   long long launches = 0;
   bool overlap = false;  // heavy cells folded on stream2 during the ray pass
+  // Per-ray endpoint cell from k_ingest (indexed like the rays), or null when
+  // the sort has overwritten it (3 passes) or the rays are a shard's.
+  const uint32_t* point_cells = nullptr;
   int heavy = INT_MAX;
   Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
       : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
@@ -1625,6 +1655,11 @@ RayArgs rayArgs(const Frame& f) {
   ra.alpha_n = f.P.cleanup.alpha_n;
   ra.cleanup = f.P.cleanup.cleanup_enabled;
   ra.bound = f.P.cleanup.upper_bound_enabled;
+  const GridArgs& g = f.g;
+  ra.origin_in = ra.o[0] >= g.ox && ra.o[0] <= g.xmax && ra.o[1] >= g.oy && ra.o[1] <= g.ymax;
+  auto clampc = [](int v, int n) { return v < 0 ? 0 : (v > n - 1 ? n - 1 : v); };
+  ra.ocol = clampc(x86_to_int(std::floor((ra.o[0] - g.ox) / g.res)), g.W);
+  ra.orow = clampc(x86_to_int(std::floor((ra.o[1] - g.oy) / g.res)), g.H);
   return ra;
 }
 
@@ -1640,7 +1675,8 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
     ++f.launches;
     if (N > 0) {
       k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 0, ray_base, m.probe);
+                                                   m.kstar, m.raylist, m.stats, 0, ray_base, m.probe,
+                                                   f.point_cells);
       ++f.launches;
     }
   }
@@ -1653,7 +1689,8 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
     ++f.launches;
     if (N > 0) {
       k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 1, ray_base, m.probe);
+                                                   m.kstar, m.raylist, m.stats, 1, ray_base, m.probe,
+                                                   f.point_cells);
       ++f.launches;
     }
   }
@@ -1776,6 +1813,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   checkCuda(cudaEventRecord(m.ev[3], f.s), "event");  // drift done
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
+    f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
     phaseRaysPass1(f, N, 0);
     phaseRemovePass2(f, 0);
   } else {
@@ -1860,6 +1898,7 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   checkCuda(cudaEventRecord(m.ev[3], f.s), "event");
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
+    f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
     phaseRaysPass1(f, N, 0);
     phaseRemovePass2(f, 0);
   } else {
