@@ -1251,17 +1251,29 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   visits += static_cast<unsigned>((xl0 - xl) + (yl0 - yl) + 1);
 }
 
+// 128-thread blocks, 9 per SM: 56 registers (no spills in the DDA loop) at 36
+// resident warps (256 x 5 at 48 registers spilled the step increments).
 #ifndef RB_PASS1_MIN_BLOCKS
-#define RB_PASS1_MIN_BLOCKS 5
+#define RB_PASS1_MIN_BLOCKS 9
 #endif
-__global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
+#ifndef RB_P1_THREADS
+#define RB_P1_THREADS 128
+#endif
+constexpr int kP1Threads = RB_P1_THREADS;
+template <bool kStride>
+__global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
     k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
                  const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
                  DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
                  const uint32_t* __restrict__ pcell) {
   if (retry && !st->respeculate) return;
-  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  // kStride (the retry launch): grid-stride over ray tiles with a one-wave
+  // grid, so its common no-op case costs one wave of returning blocks. The
+  // main launch has one block per tile (the loop runs once).
+  for (uint32_t k0 = blockIdx.x * kP1Threads; k0 < n;
+       k0 = kStride ? k0 + gridDim.x * kP1Threads : n) {
+  const uint32_t k = k0 + threadIdx.x;
   bool touched = false;
   unsigned visits = 0;
   if (k < n && kept[k]) {
@@ -1290,6 +1302,7 @@ __global__ void __launch_bounds__(kThreads, RB_PASS1_MIN_BLOCKS)
   }
   unsigned long long v = warpSum(static_cast<unsigned long long>(visits));
   if (lane == 0 && v) atomicAdd(&st->visits, v);
+  }
 }
 
 // Invalidate every cell some ray removed (set is order independent).
@@ -1674,7 +1687,7 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
                                                         f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
-      k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+      k_rays_pass1<false><<<gridFor(N, kP1Threads), kP1Threads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
                                                    m.kstar, m.raylist, m.stats, 0, ray_base, m.probe,
                                                    f.point_cells);
       ++f.launches;
@@ -1688,7 +1701,8 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
                                                         -1, 1, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
-      k_rays_pass1<<<gridFor(N), kThreads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+      k_rays_pass1<true><<<std::min(gridFor(N, kP1Threads), 148u * RB_PASS1_MIN_BLOCKS),
+                     kP1Threads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
                                                    m.kstar, m.raylist, m.stats, 1, ray_base, m.probe,
                                                    f.point_cells);
       ++f.launches;
