@@ -170,9 +170,10 @@ __global__ void __launch_bounds__(kThreads)
     bool keep = false;
     if (sq > a.max_range2) {
       oor = 1;
-    } else if (a.excl_enabled &&
+    } else if (a.excl_enabled && !(a.excl_tan >= 0.0 && z <= smin(a.excl_dmax, a.excl_b)) &&
                z > smin(a.excl_dmax,
                         a.excl_b + smax(0.0, libm_hypot(x, y) - a.excl_c) * a.excl_tan)) {
+      // (the pre-test skips the hypot: with tan >= 0 the bound is >= min(d_max, b))
       exc = 1;
     } else {
       keep = true;
@@ -186,8 +187,10 @@ __global__ void __launch_bounds__(kThreads)
       py[k] = my;
       pz[k] = mz;
       pvar[k] = smax(a.alpha_d * d * d, a.sigma_p_min2);
-      const int col = x86_to_int(floor((mx - a.g.ox) / a.g.res));
-      const int row = x86_to_int(floor((my - a.g.oy) / a.g.res));
+      double qx, qy;  // (m - origin) / res, both quotients from one reciprocal
+      div2_rn(mx - a.g.ox, my - a.g.oy, a.g.res, qx, qy);
+      const int col = x86_to_int(floor(qx));
+      const int row = x86_to_int(floor(qy));
       if (col >= 0 && col < a.g.W && row >= 0 && row < a.g.H) {
         cell = static_cast<uint32_t>(row) * a.g.W + col;
         if (a.drift_enabled) {
@@ -578,7 +581,10 @@ __device__ __forceinline__ bool gateOutlier(double d, double cv, const FuseArgs&
 constexpr int kFoldBatch = 8;
 
 // Cells with more points than this fold on the side stream (k_fuse_heavy).
-constexpr int kHeavyCell = 64;
+#ifndef RB_HEAVY_CELL
+#define RB_HEAVY_CELL 64
+#endif
+constexpr int kHeavyCell = RB_HEAVY_CELL;
 constexpr int kHeavyBlocks = 256;  // one warp each
 
 struct FoldCounts {

@@ -12,7 +12,7 @@ import paper_2204_12876_b200 as pk
 from paper_2204_12876_b200 import workloads as wl
 
 lib = pk.load_library()
-w = wl.headline()
+w = wl.ALL[os.environ.get("AB_WORKLOAD", "headline")]()
 names = ["upload", "ingest", "drift", "sort", "fuse", "rays", "cells", "total"]
 print("lib", os.environ.get("RELIEF_B200_LIB", "default"))
 for extra in ["", "cleanup.upper_bound_enabled = false\n"]:
