@@ -63,8 +63,9 @@ def main(rep, launches, tag):
         bw = (rd + wr) * 1e6 / (dur * 1e-6) / 1e9 if dur and rd is not None else None
         lines.append(f"| {k} | {dur:.1f} | {rd:.2f} | {wr:.2f} | {bw:.0f} | {occ:.1f} | {ipc:.2f} | {regs:.0f} | "
                      + ", ".join(f"{n} {v:.0f}" for v, n in stalls) + " |")
-        if k in GROUP:
-            traffic[GROUP[k]].append((rd + wr) * 1e6)
+        base = k.split("<")[0]  # template instances (k_rays_pass1<0>/<1>)
+        if base in GROUP:
+            traffic[GROUP[base]].append((rd + wr) * 1e6)
     (prof / f"{tag}_kernels.md").write_text("\n".join(lines) + "\n")
     # per frame: every captured frame launches k_ingest exactly once
     frames = max(1, len(traffic.get("ingest", [])))
