@@ -126,6 +126,8 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
+    for (auto& e : m->ev_chunk)
+      checkCuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
     for (int k = 0; k < DeviceMap::kSlots; ++k) {
       checkCuda(cudaEventCreate(&m->ev_copied[k]), "event create");
       checkCuda(cudaEventCreateWithFlags(&m->ev_consumed[k], cudaEventDisableTiming), "event create");
@@ -190,6 +192,8 @@ void destroyDeviceMap(DeviceMap* m) {
     cudaStreamDestroy(m->copy_stream);
   }
   for (auto& e : m->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : m->ev_chunk)
     if (e) cudaEventDestroy(e);
   if (m->stream) cudaStreamDestroy(m->stream);
   if (m->stream2) cudaStreamDestroy(m->stream2);

@@ -177,6 +177,10 @@ struct DeviceMap {
   double last_chain_seconds = 0.0;
   int last_chain_launches = 0;
   cudaEvent_t ev[14] = {};
+  // Synchronous host-input frames: the upload is split into kChunks copies on
+  // copy_stream and each chunk is ingested as soon as it lands.
+  static constexpr int kChunks = 2;  // 2 and 4 measured alike; 8 slower
+  cudaEvent_t ev_chunk[kChunks] = {};
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
   long long last_launches = 0;

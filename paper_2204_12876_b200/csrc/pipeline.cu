@@ -156,9 +156,11 @@ __global__ void __launch_bounds__(kThreads)
              double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
              uint8_t* __restrict__ kept, double* __restrict__ drift_part,
              int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
-             uint32_t dmask, int count_cells, DevStats* st) {
+             uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base) {
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
-  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  // k_base: first point of this launch (a chunk of a frame whose upload is
+  // split); block partials are indexed by the frame-wide block k / kThreads.
+  const uint32_t k = k_base + blockIdx.x * kThreads + threadIdx.x;
   int oor = 0, exc = 0, oom = 0, dn = 0;
   double ds = 0.0;
   uint32_t cell = WH;
@@ -246,8 +248,8 @@ __global__ void __launch_bounds__(kThreads)
       c2 += s_cnt[2][w];
       c3 += s_cnt[3][w];
     }
-    drift_part[blockIdx.x] = bs;
-    drift_npart[blockIdx.x] = c0;
+    drift_part[k_base / kThreads + blockIdx.x] = bs;
+    drift_npart[k_base / kThreads + blockIdx.x] = c0;
     if (c1) atomicAdd(&st->out_of_range, static_cast<unsigned long long>(c1));
     if (c2) atomicAdd(&st->excluded, static_cast<unsigned long long>(c2));
     if (c3) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c3));
@@ -1549,6 +1551,13 @@ void phaseScratch(Frame& f, std::size_t n) {
 }
 
 // Point scratch + the input stream into HBM; returns the device points.
+// Chunks of an uploaded frame: multiples of the radix tile (and so of the
+// block), so tile digit counts and drift block partials are those of one launch.
+inline uint32_t chunkPoints(uint32_t N) {
+  const uint32_t c = (N + DeviceMap::kChunks - 1) / DeviceMap::kChunks;
+  return (c + kTile - 1) / kTile * kTile;
+}
+
 const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_device) {
   DeviceMap& m = f.m;
   if (n == 0) return xyz;
@@ -1556,6 +1565,26 @@ const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_de
   if (on_device) return xyz;
   checkCuda(cudaMemcpyAsync(m.xyz_in, xyz, n * 3 * sizeof(double), cudaMemcpyHostToDevice, f.s),
             "point upload");
+  return m.xyz_in;
+}
+
+// Host input of a synchronous frame: kChunks copies on copy_stream (after
+// ev[0] on the frame stream), one event per chunk; phaseIngest(chunked) runs
+// each chunk's k_ingest when it lands, and the per-scan resets / recenter
+// run under the copy. ev[13] marks the end of the upload.
+const double* phaseUploadChunked(Frame& f, const double* xyz, uint32_t N) {
+  DeviceMap& m = f.m;
+  phaseScratch(f, N);
+  checkCuda(cudaStreamWaitEvent(m.copy_stream, m.ev[0], 0), "stream wait");
+  const uint32_t chunk = chunkPoints(N);
+  for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
+    const std::size_t len = std::min(chunk, N - base);
+    checkCuda(cudaMemcpyAsync(m.xyz_in + 3 * static_cast<std::size_t>(base), xyz + 3 * static_cast<std::size_t>(base),
+                              len * 3 * sizeof(double), cudaMemcpyHostToDevice, m.copy_stream),
+              "point upload");
+    checkCuda(cudaEventRecord(m.ev_chunk[c], m.copy_stream), "event");
+  }
+  checkCuda(cudaEventRecord(m.ev[13], m.copy_stream), "event");  // upload done
   return m.xyz_in;
 }
 
@@ -1585,7 +1614,8 @@ SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
 }
 
 // K1 (reference integration.cpp:85-140, sensing.cpp:32-41, drift.cpp:24-42).
-void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, bool count_cells) {
+void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, bool count_cells,
+                 bool chunked = false) {
   if (N == 0) return;
   DeviceMap& m = f.m;
   const UpdateParams& U = f.P.update;
@@ -1605,11 +1635,14 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   ia.sigma_p_min2 = U.noise.sigma_p_min2;
   ia.drift_enabled = f.P.drift.enabled;
   ia.drift_thr = f.P.drift.traversability_threshold;
-  k_ingest<<<gridFor(N), kThreads, 0, f.s>>>(d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz, m.pvar,
-                                             m.key0, m.kept, m.drift_sum_part, m.drift_n_part,
-                                             sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0,
-                                             m.stats);
-  ++f.launches;
+  const uint32_t chunk = chunked ? chunkPoints(N) : N;
+  for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
+    if (chunked) checkCuda(cudaStreamWaitEvent(f.s, m.ev_chunk[c], 0), "stream wait");
+    k_ingest<<<gridFor(std::min(chunk, N - base)), kThreads, 0, f.s>>>(
+        d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz, m.pvar, m.key0, m.kept, m.drift_sum_part,
+        m.drift_n_part, sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0, m.stats, base);
+    ++f.launches;
+  }
 }
 
 // K2 over N keys (cells; >= WH = not sorted) with payload (z, var) indexed
@@ -1815,13 +1848,14 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // ev0 -> ev13: the input copy (host input only); everything after it is the
   // frame's device time (stats / count / tile-count resets, recenter, kernels).
   checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
-  const double* d_xyz = phaseUpload(f, xyz, n, xyz_on_device);
-  checkCuda(cudaEventRecord(m.ev[13], f.s), "event");  // copy done
+  const bool chunked = !xyz_on_device && N >= 2 * kTile;
+  const double* d_xyz = chunked ? phaseUploadChunked(f, xyz, N) : phaseUpload(f, xyz, n, xyz_on_device);
+  if (!chunked) checkCuda(cudaEventRecord(m.ev[13], f.s), "event");  // copy done
   phaseBegin(f, false);
   // count[] is all zero here: k_cells clears it after its last use each scan.
   const SortGeom sg = phaseSortGeometry(f, N);
   checkCuda(cudaEventRecord(m.ev[1], f.s), "event");  // resets done
-  phaseIngest(f, d_xyz, N, sg, true);
+  phaseIngest(f, d_xyz, N, sg, true, chunked);
   checkCuda(cudaEventRecord(m.ev[2], f.s), "event");  // ingest done
   if (n > 0 && P.drift.enabled) {
     k_drift_finalize<<<1, 1024, 0, f.s>>>(m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
@@ -1851,9 +1885,17 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   checkCuda(cudaEventElapsedTime(&ms_copy, m.ev[0], m.ev[13]), "timing");
   checkCuda(cudaEventElapsedTime(&ms_reset, m.ev[13], m.ev[1]), "timing");
   // kernel_seconds: upload (input copy), ingest (+ resets / recenter), drift,
-  // sort, fusion, rays, cell phases, total device time after the copy
+  // sort, fusion, rays, cell phases, total device time after the copy. With a
+  // chunked upload the resets and all but the last chunk's ingest run under
+  // the copy: "ingest" is then the part after the upload ended.
   ms[0] = ms_copy;
-  ms[1] += ms_reset;
+  if (chunked) {
+    float after = 0.0f;
+    checkCuda(cudaEventElapsedTime(&after, m.ev[13], m.ev[2]), "timing");
+    ms[1] = std::max(0.0f, after);
+  } else {
+    ms[1] += ms_reset;
+  }
   for (int k = 0; k < 6; ++k) m.kernel_seconds[k] = ms[k] * 1e-3;
   m.kernel_seconds[6] = (ms[6] + ms_trav) * 1e-3;
   m.kernel_seconds[7] = (ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6] + ms_trav) * 1e-3;
