@@ -61,39 +61,6 @@ __global__ void __launch_bounds__(kT) k_linear(const double* __restrict__ v,
   out[i] = acc / ws;
 }
 
-// Fixed-radius linear filter: same sums in the same order, loops unrolled.
-template <int R>
-__global__ void __launch_bounds__(kT) k_linear_r(const double* __restrict__ v,
-                                                 const uint8_t* __restrict__ ok, int W, int H,
-                                                 Weights wt, double* __restrict__ out,
-                                                 uint8_t* __restrict__ ok_out) {
-  constexpr int k = 2 * R + 1;
-  const int i = blockIdx.x * kT + threadIdx.x;
-  if (i >= W * H) return;
-  ok_out[i] = ok[i];
-  if (!ok[i]) {
-    out[i] = v[i];
-    return;
-  }
-  const int r = i / W, c = i - (i / W) * W;
-  double acc = 0.0, ws = 0.0;
-#pragma unroll
-  for (int dr = -R; dr <= R; ++dr) {
-    const int rr = r + dr;
-#pragma unroll
-    for (int dc = -R; dc <= R; ++dc) {
-      const int cc = c + dc;
-      if (rr < 0 || rr >= H || cc < 0 || cc >= W) continue;
-      const int j = rr * W + cc;
-      if (!ok[j]) continue;
-      const double w = wt.w[(dr + R) * k + (dc + R)];
-      acc += w * v[j];
-      ws += w;
-    }
-  }
-  out[i] = acc / ws;
-}
-
 __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
                                                const uint8_t* __restrict__ ok, int W, int H,
                                                int R, double* __restrict__ out,
@@ -126,6 +93,73 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
     }
   }
   out[i] = (n % 2 == 1) ? win[n / 2] : 0.5 * (win[n / 2 - 1] + win[n / 2]);
+}
+
+// Tiled linear filter (32 x 8 cells per block, the window halo staged in
+// shared memory with coalesced loads): the same row-major window order and
+// skips (outside the grid or invalid) as k_linear. (A tiled median was not
+// faster: its cost is the per-cell insertion sort, not the loads.)
+constexpr int kSX = 32, kSY = 8;
+template <int R, int KIND>
+__global__ void __launch_bounds__(kSX* kSY) k_stencil_tile(const double* __restrict__ v,
+                                                           const uint8_t* __restrict__ ok, int W,
+                                                           int H, Weights wt,
+                                                           double* __restrict__ out,
+                                                           uint8_t* __restrict__ ok_out) {
+  static_assert(KIND == 0, "linear filter only");
+  constexpr int TW = kSX + 2 * R, TH = kSY + 2 * R, k = 2 * R + 1;
+  __shared__ double sv[TH * TW];
+  __shared__ uint8_t so[TH * TW];
+  const int c0 = blockIdx.x * kSX - R, r0 = blockIdx.y * kSY - R;
+  const int tid = threadIdx.y * kSX + threadIdx.x;
+  for (int q = tid; q < TW * TH; q += kSX * kSY) {
+    const int rr = r0 + q / TW, cc = c0 + q % TW;
+    uint8_t o = 0;
+    double x = 0.0;
+    if (rr >= 0 && rr < H && cc >= 0 && cc < W) {
+      const int j = rr * W + cc;
+      o = ok[j];
+      if (o) x = v[j];
+    }
+    so[q] = o;
+    sv[q] = x;
+  }
+  __syncthreads();
+  const int r = blockIdx.y * kSY + threadIdx.y, c = blockIdx.x * kSX + threadIdx.x;
+  if (r >= H || c >= W) return;
+  const int i = r * W + c;
+  const int lc = threadIdx.x + R, lr = threadIdx.y + R;
+  const uint8_t oi = so[lr * TW + lc];
+  ok_out[i] = oi;
+  if (!oi) {
+    out[i] = v[i];
+    return;
+  }
+  double acc = 0.0, ws = 0.0;
+#pragma unroll
+  for (int dr = -R; dr <= R; ++dr) {
+#pragma unroll
+    for (int dc = -R; dc <= R; ++dc) {
+      const int q = (lr + dr) * TW + (lc + dc);
+      if (!so[q]) continue;
+      const double w = wt.w[(dr + R) * k + (dc + R)];
+      acc += w * sv[q];
+      ws += w;
+    }
+  }
+  out[i] = acc / ws;
+}
+
+template <int KIND>
+bool launchStencilTile(int R, const double* v, const uint8_t* ok, int W, int H, const Weights& wt,
+                       double* out, uint8_t* ok_out, cudaStream_t s) {
+  const dim3 grid((W + kSX - 1) / kSX, (H + kSY - 1) / kSY), block(kSX, kSY);
+  switch (R) {
+    case 1: k_stencil_tile<1, KIND><<<grid, block, 0, s>>>(v, ok, W, H, wt, out, ok_out); return true;
+    case 2: k_stencil_tile<2, KIND><<<grid, block, 0, s>>>(v, ok, W, H, wt, out, ok_out); return true;
+    case 3: k_stencil_tile<3, KIND><<<grid, block, 0, s>>>(v, ok, W, H, wt, out, ok_out); return true;
+    default: return false;
+  }
 }
 
 // ---- min inpaint: connected components of invalid cells (4-neighbour).
@@ -396,9 +430,8 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
         for (int dc = -st.radius; dc <= st.radius; ++dc)
           wt.w[(dr + st.radius) * kk + (dc + st.radius)] =
               st.kind == 1 ? 1.0 : std::exp(-(dr * dr + dc * dc) / (2.0 * st.sigma * st.sigma));
-      if (st.radius == 1) k_linear_r<1><<<grid, kT, 0, s>>>(cv, co, W, H, wt, nv, no);
-      else if (st.radius == 2) k_linear_r<2><<<grid, kT, 0, s>>>(cv, co, W, H, wt, nv, no);
-      else k_linear<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, wt, nv, no);
+      if (!launchStencilTile<0>(st.radius, cv, co, W, H, wt, nv, no, s))
+        k_linear<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, wt, nv, no);
       ++launches;
     } else if (st.kind == 2) {
       k_median<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, nv, no);
