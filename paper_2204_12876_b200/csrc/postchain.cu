@@ -299,20 +299,20 @@ __global__ void __launch_bounds__(kT) k_cc_merge(const uint8_t* ok, int W, int H
 
 // Flatten without path writes: chains are tile-root chains (short); only each
 // cell's own entry is written, so concurrent walks never see a torn path.
-__global__ void __launch_bounds__(kT) k_cc_flatten2(const uint8_t* ok, int n, int* parent) {
-  const int i = blockIdx.x * kT + threadIdx.x;
-  if (i >= n || ok[i]) return;
-  int r = parent[i];
-  while (parent[r] != r) r = parent[r];
-  parent[i] = r;
-}
-
+// Also flattens (parent[i] = root, for k_cc_fill) and, in thread 0, folds
+// the step's "any valid cell" flag (see k_cc_tile) into flag[1].
 __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t* ok, int W, int H,
-                                                  const int* parent, unsigned long long* key,
-                                                  uint8_t* border) {
+                                                  int* parent, unsigned long long* key,
+                                                  uint8_t* border, int* flag) {
   const int i = blockIdx.x * kT + threadIdx.x;
+  if (i == 0) {
+    if (flag[0] == 0) flag[1] = 1;
+    flag[0] = 0;
+  }
   if (i >= W * H || ok[i]) return;
-  const int root = parent[i];
+  int root = parent[i];
+  while (parent[root] != root) root = parent[root];
+  parent[i] = root;
   const int r = i / W, c = i - (i / W) * W;
   bool any = false;
   unsigned long long best = kKeyInf;
@@ -356,13 +356,6 @@ __global__ void __launch_bounds__(kT) k_cc_fill(const double* v, const uint8_t* 
     out[i] = v[i];
     ok_out[i] = 0;
   }
-}
-
-// flag[0] = any valid cell seen at an inpaint step (per step, OR-ed into
-// flag[1] = "some inpaint step had nothing to inpaint").
-__global__ void k_check_any(int* flag) {
-  if (flag[0] == 0) flag[1] = 1;
-  flag[0] = 0;
 }
 
 }  // namespace
@@ -423,6 +416,11 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
     const ChainStep& st = steps[k];
     double* nv = bufs[which];
     uint8_t* no = oks[which];
+    const bool direct = k == n_steps - 1 && d_values_out != cv && d_valid_out != co;
+    if (direct) {  // the last step writes the caller's buffers (no trailing copy)
+      nv = d_values_out;
+      no = d_valid_out;
+    }
     if (st.kind == 0 || st.kind == 1) {
       Weights wt{};
       const int kk = 2 * st.radius + 1;
@@ -439,20 +437,20 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
     } else {
       const dim3 tiles((W + kTileCC - 1) / kTileCC, (H + kTileCC - 1) / kTileCC);
       k_cc_tile<<<tiles, kTileCC * kTileCC, 0, s>>>(co, W, H, sc.parent, sc.key, sc.border, sc.flag);
-      k_check_any<<<1, 1, 0, s>>>(sc.flag);
       const int edges = H * ((W - 1) / kTileCC) + W * ((H - 1) / kTileCC);
       if (edges > 0) k_cc_merge<<<(edges + kT - 1) / kT, kT, 0, s>>>(co, W, H, sc.parent);
-      k_cc_flatten2<<<grid, kT, 0, s>>>(co, n, sc.parent);
-      k_cc_border<<<grid, kT, 0, s>>>(cv, co, W, H, sc.parent, sc.key, sc.border);
+      k_cc_border<<<grid, kT, 0, s>>>(cv, co, W, H, sc.parent, sc.key, sc.border, sc.flag);
       k_cc_fill<<<grid, kT, 0, s>>>(cv, co, n, sc.parent, sc.key, sc.border, nv, no);
-      launches += 6;
+      launches += 3 + (edges > 0 ? 1 : 0);
     }
     cv = nv;
     co = no;
     which ^= 1;
   }
-  checkCuda(cudaMemcpyAsync(d_values_out, cv, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
-  checkCuda(cudaMemcpyAsync(d_valid_out, co, n, cudaMemcpyDeviceToDevice, s), "copy");
+  if (cv != d_values_out)
+    checkCuda(cudaMemcpyAsync(d_values_out, cv, n * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+  if (co != d_valid_out)
+    checkCuda(cudaMemcpyAsync(d_valid_out, co, n, cudaMemcpyDeviceToDevice, s), "copy");
   checkCuda(cudaGetLastError(), "chain launch");
   return launches;
 }
