@@ -154,6 +154,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
     fillFresh(*m);
     checkCuda(cudaMemsetAsync(m->count, 0, n * sizeof(int32_t), m->stream), "map init");
+    checkCuda(cudaMemsetAsync(m->start, 0xff, (n + 1) * sizeof(uint32_t), m->stream), "map init");
     checkCuda(cudaStreamSynchronize(m->stream), "map init");
   } catch (...) {
     destroyDeviceMap(m);

@@ -1370,7 +1370,8 @@ constexpr int kTileX = 32, kTileY = 8;
 // memory tile with a (radius)-cell halo. Overlap is evaluated for halo cells
 // too, so every thread sees the post-clearance validity of its window.
 __global__ void __launch_bounds__(kTileX* kTileY)
-    k_cells(Layers L, int32_t* __restrict__ count, CellArgs a, DevStats* st) {
+    k_cells(Layers L, int32_t* __restrict__ count, uint32_t* __restrict__ seg_start, CellArgs a,
+            DevStats* st) {
   extern __shared__ unsigned char smem[];
   const int halo = a.radius > 1 ? a.radius : 1;
   const int tw = kTileX + 2 * halo, th = kTileY + 2 * halo;
@@ -1405,7 +1406,10 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   if (r < H && c < W) {
     const size_t i = static_cast<size_t>(r) * W + c;
     const int32_t cnt_i = count[i];
-    if (cnt_i != 0) count[i] = 0;  // last reader this scan: ready for the next one
+    if (cnt_i != 0) {  // last reader this scan: ready for the next one (the sort's
+      count[i] = 0;     // atomicMin segment starts need 0xffffffff)
+      seg_start[i] = 0xffffffffu;
+    }
     const int lr = threadIdx.y + halo, lc = threadIdx.x + halo;
     const bool was_valid = L.valid[i] != 0;
     const bool ok = sv[lr * tw + lc] != 0;
@@ -1652,7 +1656,8 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
                    const SortGeom& sg) {
   DeviceMap& m = f.m;
   cudaStream_t s = f.s;
-  checkCuda(cudaMemsetAsync(m.start, 0xff, f.ncell * sizeof(uint32_t), s), "memset");
+  // start[] is all 0xffffffff here: set at map creation, and k_cells resets
+  // the entries of cells that had points after each scan.
   const std::size_t sc_smem = 20 * static_cast<std::size_t>(sg.buckets());
   const uint32_t* kin = keys;
   uint32_t *kout = m.key1, *vin = m.val0, *vout = m.val1;
@@ -1795,7 +1800,7 @@ void phaseCells(Frame& f) {
     checkCuda(cudaFuncSetAttribute(k_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sm)),
               "smem attribute");
-  k_cells<<<grid, dim3(kTileX, kTileY), sm, f.s>>>(m.cur, m.count, ca, m.stats);
+  k_cells<<<grid, dim3(kTileX, kTileY), sm, f.s>>>(m.cur, m.count, m.start, ca, m.stats);
   ++f.launches;
   checkCuda(cudaEventRecord(m.ev[7], f.s), "event");  // cell phases done
   // Conv-net traversability (reference integration.cpp:242-244): reads the
@@ -2101,6 +2106,7 @@ void shardUpdate(DeviceMap& m, const double* drift_pairs, int n_ranks, const uin
   const uint32_t M = static_cast<uint32_t>(n_records);
   if (M > 0 && M > m.cap) fail(Err::kUsage, "more fusion records than points in the frame");
   checkCuda(cudaMemsetAsync(m.count, 0, f.ncell * sizeof(int32_t), f.s), "memset");
+  checkCuda(cudaMemsetAsync(m.start, 0xff, f.ncell * sizeof(uint32_t), f.s), "memset");
   if (M > 0) {
     const SortGeom sg = phaseSortGeometry(f, M);
     k_records_count<<<gridFor(M), kThreads, 0, f.s>>>(d_cells, M, m.count, sg.tc, sg.pitch,
