@@ -345,14 +345,18 @@ relief_status relief_gpu_map_integrate_device(relief_map* map, const relief_conf
 
 relief_status relief_gpu_map_phase_seconds(const relief_map* map, double out[7]) {
   if (map == nullptr || out == nullptr) return usage("null argument");
-  for (int k = 0; k < 7; ++k) out[k] = map->dev->phase_seconds[k];
-  return RELIEF_OK;
+  return guard([&] {
+    rb200::resolveTiming(*map->dev);
+    for (int k = 0; k < 7; ++k) out[k] = map->dev->phase_seconds[k];
+  });
 }
 
 relief_status relief_gpu_map_kernel_seconds(const relief_map* map, double out[8]) {
   if (map == nullptr || out == nullptr) return usage("null argument");
-  for (int k = 0; k < 8; ++k) out[k] = map->dev->kernel_seconds[k];
-  return RELIEF_OK;
+  return guard([&] {
+    rb200::resolveTiming(*map->dev);
+    for (int k = 0; k < 8; ++k) out[k] = map->dev->kernel_seconds[k];
+  });
 }
 
 int64_t relief_gpu_map_last_visits(const relief_map* map) {

@@ -183,6 +183,8 @@ struct DeviceMap {
   cudaEvent_t ev_chunk[kChunks] = {};
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
+  bool timing_pending = false;  // the arrays above still to be read from the events (resolveTiming)
+  bool timing_chunked = false;
   long long last_launches = 0;
   long long last_visits = 0;
 };
@@ -214,6 +216,8 @@ struct ScanResult {
   int drift_points = 0;
   double seconds = 0.0;
 };
+// Fills DeviceMap::kernel_seconds / phase_seconds of the last synchronous frame.
+void resolveTiming(DeviceMap& m);
 ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& params, const double* xyz,
                                std::size_t n, bool xyz_on_device, const Pose& pose,
                                double stamp, double dt);

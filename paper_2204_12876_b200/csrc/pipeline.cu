@@ -1844,6 +1844,7 @@ ScanResult resultFrom(const DevStats& d, std::size_t n) {
 ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const double* xyz,
                                std::size_t n, bool xyz_on_device, const Pose& pose,
                                double stamp, double dt) {
+  const auto t_call = std::chrono::steady_clock::now();
   checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
   if (n >= 0xffffffffULL) fail(Err::kUsage, "too many points in one scan");
   if (m.shard.stage != 0) fail(Err::kUsage, "a sharded frame is in progress on this map");
@@ -1884,6 +1885,23 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   const DevStats& d = phaseStats(f);
   ScanResult out = resultFrom(d, n);
 
+  // Per-phase device times are read from the events only when asked for
+  // (resolveTiming): nine event queries cost ~30 us of host time per call.
+  m.timing_pending = true;
+  m.timing_chunked = chunked;
+  out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call).count();
+  m.last_launches = f.launches;
+  m.last_visits = static_cast<long long>(d.visits);
+  return out;
+}
+
+// Per-phase device times of the last synchronous frame (kernel_seconds:
+// upload, ingest (+ resets / recenter), drift, sort, fusion, rays, cell
+// phases, total device time after the copy; phase_seconds: the reference's
+// Table I labels), from its events, on first request.
+void resolveTiming(DeviceMap& m) {
+  if (!m.timing_pending) return;
+  m.timing_pending = false;
   float ms[7], ms_trav = 0.0f, ms_copy = 0.0f, ms_reset = 0.0f;
   for (int k = 1; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
   checkCuda(cudaEventElapsedTime(&ms_trav, m.ev[7], m.ev[12]), "timing");
@@ -1894,7 +1912,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // chunked upload the resets and all but the last chunk's ingest run under
   // the copy: "ingest" is then the part after the upload ended.
   ms[0] = ms_copy;
-  if (chunked) {
+  if (m.timing_chunked) {
     float after = 0.0f;
     checkCuda(cudaEventElapsedTime(&after, m.ev[13], m.ev[2]), "timing");
     ms[1] = std::max(0.0f, after);
@@ -1911,10 +1929,6 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   m.phase_seconds[4] = ms_trav * 1e-3;                  // conv-net traversability
   m.phase_seconds[5] = 0.0;
   m.phase_seconds[6] = m.kernel_seconds[7];
-  out.seconds = m.phase_seconds[6];
-  m.last_launches = f.launches;
-  m.last_visits = static_cast<long long>(d.visits);
-  return out;
 }
 
 // ------------------------------------------------------- streaming frames
@@ -1996,6 +2010,7 @@ ScanResult waitScan(DeviceMap& m) {
   if (m.async_n[slot] > 0)
     checkCuda(cudaEventElapsedTime(&ms_copy, m.ev_copy0[slot], m.ev_copied[slot]), "timing");
   checkCuda(cudaEventElapsedTime(&ms_run, m.ev_start[slot], m.ev_done[slot]), "timing");
+  m.timing_pending = false;
   for (double& v : m.kernel_seconds) v = 0.0;
   m.kernel_seconds[0] = ms_copy * 1e-3;
   m.kernel_seconds[7] = ms_run * 1e-3;

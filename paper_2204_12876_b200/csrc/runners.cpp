@@ -54,6 +54,7 @@ class Pipeline {
   DeviceMap& map() { return *map_; }
   std::array<double, 7> phases() const {
     std::array<double, 7> a{};
+    resolveTiming(*map_);
     for (int k = 0; k < 7; ++k) a[k] = map_->phase_seconds[k];
     return a;
   }
