@@ -107,3 +107,77 @@ def test_randomised_scenarios_match_reference(gpu, reference, tmp_path, seed):
         assert_stats_match(got, want, drift_tol=1e-12 if drift else 0.0, context=ctx)
         assert_layers_match(maps[0].layers(), maps[1].layers(), height_tol=1e-9 if drift else 0.0,
                             context=ctx)
+
+
+def _frames(rng, res, cell_aligned, n_frames):
+    pos, stamp, out = np.zeros(3), 0.0, []
+    for _ in range(n_frames):
+        if cell_aligned:
+            R = np.eye(3)
+            step = rng.integers(-3, 4, 2) * res
+            pos = np.array([pos[0] + step[0], pos[1] + step[1], 1.0])
+        else:
+            R = wl.rot_z(rng.uniform(-math.pi, math.pi)) @ wl.rot_y(rng.uniform(-0.3, 0.3))
+            pos = pos + np.array([rng.normal(0, 3 * res), rng.normal(0, 3 * res), 0.0])
+            pos[2] = rng.uniform(0.4, 1.8)
+        stamp += float(rng.choice([0.0, 0.1, 0.4, 1.5]))
+        out.append((_cloud(rng, res, cell_aligned, int(rng.integers(200, 6000))),
+                    wl.pose34(R, tuple(pos)), stamp))
+    return out
+
+
+@pytest.mark.parametrize("seed", SEEDS[: max(1, len(SEEDS) // 4)])
+def test_randomised_sharded_frames_match_single_call(gpu, tmp_path, seed):
+    """G replicas integrating one frame as exact point-batch shards (multigpu.
+    integrate_sharded_lockstep) equal the single relief_map_integrate call, which the scenarios
+    above tie to the reference."""
+    from paper_2204_12876_b200 import multigpu as mg
+    rng = np.random.default_rng(5000 + seed)
+    res = float(rng.choice([0.02, 0.04, 0.05, 0.1]))
+    W, H = int(rng.integers(20, 300)), int(rng.integers(20, 300))
+    cell_aligned = bool(rng.random() < 0.4)
+    text, drift = _config(rng)
+    G = int(rng.integers(2, 5))
+    cfg_path = tmp_path / "shard_soak.config"
+    cfg_path.write_text(wl._map(res, W, H) + text)
+    cfg = pk.Config.load(gpu, cfg_path)
+    single = pk.ReliefMap.create(gpu, res, W, H)
+    reps = [pk.ReliefMap.create(gpu, res, W, H) for _ in range(G)]
+    apis = [mg.CudaShardAPI(gpu, m, cfg) for m in reps]
+    for f, (xyz, pose, stamp) in enumerate(_frames(rng, res, cell_aligned, 5)):
+        want = single.integrate(xyz, pose, stamp, cfg)
+        got = mg.integrate_sharded_lockstep(apis, xyz, pose, stamp)
+        ctx = f"seed {seed} frame {f} G={G} ({W}x{H}@{res}, drift={drift})"
+        for g, (st, m) in enumerate(zip(got, reps)):
+            assert_stats_match(st, want, drift_tol=1e-12 if drift else 0.0, context=f"{ctx} rank {g}")
+            assert_layers_match(m.layers(), single.layers(), height_tol=1e-9 if drift else 0.0,
+                                context=f"{ctx} rank {g}")
+
+
+@pytest.mark.parametrize("seed", SEEDS[: max(1, len(SEEDS) // 4)])
+def test_randomised_streaming_matches_sync(gpu, tmp_path, seed):
+    """Up to three frames in flight (relief_gpu_map_integrate_async / wait) from pinned memory
+    equal the synchronous sequence bit for bit."""
+    import torch
+    rng = np.random.default_rng(9000 + seed)
+    res = float(rng.choice([0.02, 0.04, 0.05, 0.1]))
+    W, H = int(rng.integers(20, 300)), int(rng.integers(20, 300))
+    text, _ = _config(rng)
+    cfg_path = tmp_path / "stream_soak.config"
+    cfg_path.write_text(wl._map(res, W, H) + text)
+    cfg = pk.Config.load(gpu, cfg_path)
+    sync = pk.ReliefMap.create(gpu, res, W, H)
+    stream = pk.ReliefMap.create(gpu, res, W, H)
+    frames = _frames(rng, res, bool(rng.random() < 0.4), 7)
+    want = [sync.integrate(x, p, t, cfg) for x, p, t in frames]
+    pinned = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy() for x, _, _ in frames]
+    got = []
+    for x, (_, p, t) in zip(pinned, frames):
+        stream.integrate_async(x, p, t, cfg)
+        if gpu.relief_gpu_map_in_flight(stream.handle) == 3:
+            got.append(stream.wait())
+    while gpu.relief_gpu_map_in_flight(stream.handle):
+        got.append(stream.wait())
+    for k, (g, w) in enumerate(zip(got, want)):
+        assert_stats_match(g, w, context=f"seed {seed} frame {k}")
+    assert_layers_match(stream.layers(), sync.layers(), context=f"seed {seed} final map")
