@@ -35,6 +35,22 @@ namespace rb200 {
 namespace {
 
 constexpr int kThreads = 256;
+
+// Programmatic dependent launch (sm_90+): consecutive frame kernels on the
+// library stream are launched with programmatic stream serialisation, and
+// every such kernel lets its dependent launch as soon as all of its blocks
+// are resident, then waits for its predecessor's completion (and memory)
+// before touching any data. The dependent's launch and block scheduling thus
+// overlap the predecessor's tail; the data order is unchanged.
+#ifndef RB_PDL
+#define RB_PDL 1
+#endif
+__device__ __forceinline__ void pdlEnter() {
+#if RB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 constexpr double kInf = __builtin_huge_val();
 
 __device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
@@ -157,6 +173,7 @@ __global__ void __launch_bounds__(kThreads)
              uint8_t* __restrict__ kept, double* __restrict__ drift_part,
              int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
              uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base) {
+  pdlEnter();
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
   // k_base: first point of this launch (a chunk of a frame whose upload is
   // split); block partials are indexed by the frame-wide block k / kThreads.
@@ -264,6 +281,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(1024)
     k_drift_finalize(const double* part, const int* npart, int nblocks, int min_points,
                      double max_off, double* offset_out, DevStats* st) {
+  pdlEnter();
   __shared__ double s_sum[32];
   __shared__ long long s_cnt[32];
   double s = 0.0;
@@ -301,6 +319,7 @@ __global__ void __launch_bounds__(1024)
 
 // Reference drift.cpp:44-55.
 __global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, const double* off_p) {
+  pdlEnter();
   const double off = *off_p;
   if (off == 0.0) return;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
@@ -443,6 +462,7 @@ struct SortGeom {
 // Row d of tc -> exclusive offsets within the digit; rowsum[d] = row total.
 __global__ void __launch_bounds__(kThreads)
     k_sort_rowscan(uint32_t* __restrict__ tc, uint32_t pitch, uint32_t* __restrict__ rowsum) {
+  pdlEnter();
   uint4* row = reinterpret_cast<uint4*>(tc + static_cast<size_t>(blockIdx.x) * pitch);
   const uint32_t nq = pitch / 4;
   uint32_t carry = 0;
@@ -470,6 +490,7 @@ __global__ void __launch_bounds__(kThreads)
                    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                    const double* __restrict__ pz, const double* __restrict__ pvar,
                    double* __restrict__ spz, double* __restrict__ spv, uint32_t* start) {
+  pdlEnter();
   extern __shared__ unsigned char smem[];
   const int dbits = sg.dbits, shift = pass * dbits;
   const int buckets = 1 << dbits;
@@ -717,6 +738,7 @@ __global__ void __launch_bounds__(kThreads)
            const uint32_t* __restrict__ start, const double* __restrict__ spz,
            const double* __restrict__ spv, FuseArgs a, DevStats* st, int heavy,
            uint32_t* heavy_list, uint32_t* vheavy_list) {
+  pdlEnter();
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const int cnt = i < ncell ? count[i] : 0;
   const bool is_heavy = cnt > heavy;
@@ -878,6 +900,7 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
                                                        const int32_t* __restrict__ count,
                                                        int heavy, int retry, DevStats* st,
                                                        ProbeT* probe) {
+  pdlEnter();
   if (retry) {
     if (!st->respeculate) return;
     __syncthreads();
@@ -1275,6 +1298,7 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
                  DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
                  const uint32_t* __restrict__ pcell) {
+  pdlEnter();
   if (retry && !st->respeculate) return;
   // kStride (the retry launch): grid-stride over ray tiles with a one-wave
   // grid, so its common no-op case costs one wave of returning blocks. The
@@ -1316,6 +1340,7 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
 // Invalidate every cell some ray removed (set is order independent).
 __global__ void __launch_bounds__(kThreads) k_remove(Layers L, size_t n, const int32_t* kstar,
                                                      DevStats* st) {
+  pdlEnter();
   unsigned long long cnt = 0;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -1336,6 +1361,7 @@ __global__ void __launch_bounds__(kThreads)
                  const double* __restrict__ pz, RayArgs a, Layers L,
                  const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar,
                  uint32_t ray_base) {
+  pdlEnter();
   if (st_in->removed == 0) return;
   const unsigned total = static_cast<unsigned>(st_in->candidate_rays);
   for (unsigned q = blockIdx.x * kThreads + threadIdx.x; q < total; q += gridDim.x * kThreads) {
@@ -1372,6 +1398,7 @@ constexpr int kTileX = 32, kTileY = 8;
 __global__ void __launch_bounds__(kTileX* kTileY)
     k_cells(Layers L, int32_t* __restrict__ count, uint32_t* __restrict__ seg_start, CellArgs a,
             DevStats* st) {
+  pdlEnter();
   extern __shared__ unsigned char smem[];
   const int halo = a.radius > 1 ? a.radius : 1;
   const int tw = kTileX + 2 * halo, th = kTileY + 2 * halo;
@@ -1476,6 +1503,27 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   }
   cleared = warpSum(cleared);
   if (((threadIdx.y * kTileX + threadIdx.x) & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
+}
+
+
+template <typename... KArgs, typename... Args>
+void launchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+               Args&&... args) {
+#if RB_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  checkCuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+#else
+  kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+#endif
 }
 
 inline unsigned gridFor(size_t n, int threads = kThreads) {
@@ -1642,7 +1690,7 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   const uint32_t chunk = chunked ? chunkPoints(N) : N;
   for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
     if (chunked) checkCuda(cudaStreamWaitEvent(f.s, m.ev_chunk[c], 0), "stream wait");
-    k_ingest<<<gridFor(std::min(chunk, N - base)), kThreads, 0, f.s>>>(
+    launchPdl(k_ingest, gridFor(std::min(chunk, N - base)), kThreads, 0, f.s, 
         d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz, m.pvar, m.key0, m.kept, m.drift_sum_part,
         m.drift_n_part, sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0, m.stats, base);
     ++f.launches;
@@ -1662,9 +1710,9 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   const uint32_t* kin = keys;
   uint32_t *kout = m.key1, *vin = m.val0, *vout = m.val1;
   for (int p = 0; p < sg.passes; ++p) {
-    k_sort_rowscan<<<sg.buckets(), kThreads, 0, s>>>(sg.counts(p), sg.pitch,
+    launchPdl(k_sort_rowscan, sg.buckets(), kThreads, 0, s, sg.counts(p), sg.pitch,
                                                      sg.rowsum + p * sg.buckets());
-    k_sort_scatter<<<sg.ntiles, kThreads, sc_smem, s>>>(kin, vin, N, p, sg, f.WH, kout, vout, z, var,
+    launchPdl(k_sort_scatter, sg.ntiles, kThreads, sc_smem, s, kin, vin, N, p, sg, f.WH, kout, vout, z, var,
                                                         m.spz, m.spv, m.start);
     f.launches += 2;
     // ping-pong between key1 and key0 (key0 is free once pass 0 has read it)
@@ -1687,7 +1735,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
   f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
   f.heavy = f.overlap ? kHeavyCell : INT_MAX;
-  k_fuse<<<gridFor(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
+  launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
                                                m.stats, f.heavy, m.heavy, m.heavy + f.ncell);
   ++f.launches;
   if (f.overlap) {
@@ -1727,11 +1775,11 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
   cudaStream_t s = f.s;
   const RayArgs ra = rayArgs(f);
   if (ra.cleanup || ra.bound) {
-    k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
+    launchPdl(k_classify, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
                                                         f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
-      k_rays_pass1<false><<<gridFor(N, kP1Threads), kP1Threads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+      launchPdl(k_rays_pass1<false>, gridFor(N, kP1Threads), kP1Threads, 0, s, N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
                                                    m.kstar, m.raylist, m.stats, 0, ray_base, m.probe,
                                                    f.point_cells);
       ++f.launches;
@@ -1741,12 +1789,12 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
     // Join the long-cell fold; redo the ray pass only if a heavy cell fused
     // nothing (both kernels return immediately otherwise).
     checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
-    k_classify<<<streamGrid(f.ncell), kThreads, 0, s>>>(m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
+    launchPdl(k_classify, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
                                                         -1, 1, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
-      k_rays_pass1<true><<<std::min(gridFor(N, kP1Threads), 148u * RB_PASS1_MIN_BLOCKS),
-                     kP1Threads, 0, s>>>(N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
+      launchPdl(k_rays_pass1<true>, std::min(gridFor(N, kP1Threads), 148u * RB_PASS1_MIN_BLOCKS),
+                     kP1Threads, 0, s, N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
                                                    m.kstar, m.raylist, m.stats, 1, ray_base, m.probe,
                                                    f.point_cells);
       ++f.launches;
@@ -1760,10 +1808,10 @@ void phaseRemovePass2(Frame& f, uint32_t ray_base) {
   DeviceMap& m = f.m;
   const RayArgs ra = rayArgs(f);
   if (!ra.cleanup) return;
-  k_remove<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, m.kstar, m.stats);
+  launchPdl(k_remove, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.kstar, m.stats);
   ++f.launches;
   if (ra.bound) {
-    k_rays_pass2<<<148 * 8, kThreads, 0, f.s>>>(m.raylist, m.stats, m.px, m.py, m.pz, ra, m.cur,
+    launchPdl(k_rays_pass2, 148 * 8, kThreads, 0, f.s, m.raylist, m.stats, m.px, m.py, m.pz, ra, m.cur,
                                                 m.cls, m.kstar, ray_base);
     ++f.launches;
   }
@@ -1800,7 +1848,7 @@ void phaseCells(Frame& f) {
     checkCuda(cudaFuncSetAttribute(k_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sm)),
               "smem attribute");
-  k_cells<<<grid, dim3(kTileX, kTileY), sm, f.s>>>(m.cur, m.count, m.start, ca, m.stats);
+  launchPdl(k_cells, grid, dim3(kTileX, kTileY), sm, f.s, m.cur, m.count, m.start, ca, m.stats);
   ++f.launches;
   checkCuda(cudaEventRecord(m.ev[7], f.s), "event");  // cell phases done
   // Conv-net traversability (reference integration.cpp:242-244): reads the
@@ -1864,10 +1912,10 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   phaseIngest(f, d_xyz, N, sg, true, chunked);
   checkCuda(cudaEventRecord(m.ev[2], f.s), "event");  // ingest done
   if (n > 0 && P.drift.enabled) {
-    k_drift_finalize<<<1, 1024, 0, f.s>>>(m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
+    launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
                                           P.drift.min_points, P.drift.max_offset_per_scan,
                                           m.drift_offset, m.stats);
-    k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, m.drift_offset);
+    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
     f.launches += 2;
   }
   checkCuda(cudaEventRecord(m.ev[3], f.s), "event");  // drift done
@@ -1970,10 +2018,10 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   checkCuda(cudaEventRecord(m.ev_consumed[slot], f.s), "event");
   checkCuda(cudaEventRecord(m.ev[2], f.s), "event");
   if (n > 0 && P.drift.enabled) {
-    k_drift_finalize<<<1, 1024, 0, f.s>>>(m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
+    launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
                                           P.drift.min_points, P.drift.max_offset_per_scan,
                                           m.drift_offset, m.stats);
-    k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, f.ncell, m.drift_offset);
+    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
     f.launches += 2;
   }
   checkCuda(cudaEventRecord(m.ev[3], f.s), "event");
