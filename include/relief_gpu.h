@@ -50,6 +50,11 @@ RELIEF_API relief_status relief_gpu_map_phase_seconds(const relief_map* map, dou
  * upload (+ recenter shift), ingest, drift, cell sort, gated fusion, ray
  * casting, cell phases, total excluding the upload. */
 RELIEF_API relief_status relief_gpu_map_kernel_seconds(const relief_map* map, double out[8]);
+/* Per-phase device timing (default off): with it on, every frame records CUDA events at the
+ * phase boundaries and relief_gpu_map_phase_seconds / _kernel_seconds report each phase; off,
+ * only the upload and the device total are recorded, because an event between two kernels
+ * also ends their programmatic (overlapped) launch. The runners turn it on. */
+RELIEF_API relief_status relief_gpu_map_set_phase_timing(relief_map* map, int on);
 
 /* Kernel launches issued by the last integrate call (evidence for bench.py). */
 RELIEF_API int64_t relief_gpu_map_last_launches(const relief_map* map);

@@ -119,6 +119,7 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_map_integrate_device": (_I, [_P, _P, ctypes.c_void_p, _SZ, _DP, _D, ctypes.POINTER(ScanStats)]),
     "relief_gpu_map_phase_seconds": (_I, [_P, _DP]),
     "relief_gpu_map_kernel_seconds": (_I, [_P, _DP]),
+    "relief_gpu_map_set_phase_timing": (_I, [_P, ctypes.c_int]),
     "relief_gpu_map_last_launches": (ctypes.c_int64, [_P]),
     "relief_gpu_map_last_visits": (ctypes.c_int64, [_P]),
     "relief_gpu_map_layer_device": (_I, [_P, _CS, ctypes.c_void_p, _SZ]),
@@ -335,6 +336,11 @@ class ReliefMap:
         out = np.zeros(7, dtype=np.float64)
         _check(self.lib, self.lib.relief_gpu_map_phase_seconds(self.handle, _dptr(out)))
         return out
+
+    def set_phase_timing(self, on: bool) -> None:
+        """relief_gpu_map_set_phase_timing: record per-phase events (costs the overlap of the
+        kernels at the phase boundaries; off by default)."""
+        _check(self.lib, self.lib.relief_gpu_map_set_phase_timing(self.handle, 1 if on else 0))
 
     def kernel_seconds(self) -> np.ndarray:
         """[upload, ingest, drift, sort, fusion, rays, cell phases, total excl. upload]."""

@@ -351,6 +351,12 @@ relief_status relief_gpu_map_phase_seconds(const relief_map* map, double out[7])
   });
 }
 
+relief_status relief_gpu_map_set_phase_timing(relief_map* map, int on) {
+  if (map == nullptr) return usage("null argument");
+  map->dev->phase_events = on != 0;
+  return RELIEF_OK;
+}
+
 relief_status relief_gpu_map_kernel_seconds(const relief_map* map, double out[8]) {
   if (map == nullptr || out == nullptr) return usage("null argument");
   return guard([&] {

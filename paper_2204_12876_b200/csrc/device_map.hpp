@@ -184,6 +184,11 @@ struct DeviceMap {
   double phase_seconds[7] = {0, 0, 0, 0, 0, 0, 0};
   double kernel_seconds[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // upload ingest drift sort fuse rays cells total
   bool timing_pending = false;  // the arrays above still to be read from the events (resolveTiming)
+#ifndef RB_PHASE_EVENTS_DEFAULT
+#define RB_PHASE_EVENTS_DEFAULT false
+#endif
+  bool phase_events = RB_PHASE_EVENTS_DEFAULT;  // record per-phase events (relief_gpu_map_set_phase_timing)
+  bool timing_phases = false;   // the pending frame recorded them
   bool timing_chunked = false;
   long long last_launches = 0;
   long long last_visits = 0;

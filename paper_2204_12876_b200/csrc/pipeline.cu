@@ -1526,6 +1526,14 @@ void launchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem
 #endif
 }
 
+// Phase-boundary events (per-phase device times); an event between two
+// kernels also ends their programmatic overlap, so they are recorded only
+// when phase timing is requested (DeviceMap::phase_events).
+#define RB_PHASE_EVENT(k, stream) \
+  do {                           \
+    if (m.phase_events) checkCuda(cudaEventRecord(m.ev[k], stream), "event"); \
+  } while (0)
+
 inline unsigned gridFor(size_t n, int threads = kThreads) {
   return static_cast<unsigned>((n + threads - 1) / threads);
 }
@@ -1721,7 +1729,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     kin = next_in;
     std::swap(vin, vout);
   }
-  checkCuda(cudaEventRecord(m.ev[4], s), "event");  // sort done
+  RB_PHASE_EVENT(4, s);  // sort done
 
   const UpdateParams& U = f.P.update;
   FuseArgs fa;
@@ -1748,7 +1756,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     ++f.launches;
     checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
   }
-  checkCuda(cudaEventRecord(m.ev[5], s), "event");  // fusion done (short cells when overlapped)
+  RB_PHASE_EVENT(5, s);  // fusion done (short cells when overlapped)
 }
 
 RayArgs rayArgs(const Frame& f) {
@@ -1850,7 +1858,7 @@ void phaseCells(Frame& f) {
               "smem attribute");
   launchPdl(k_cells, grid, dim3(kTileX, kTileY), sm, f.s, m.cur, m.count, m.start, ca, m.stats);
   ++f.launches;
-  checkCuda(cudaEventRecord(m.ev[7], f.s), "event");  // cell phases done
+  RB_PHASE_EVENT(7, f.s);  // cell phases done
   // Conv-net traversability (reference integration.cpp:242-244): reads the
   // post-overlap elevation, writes the traversability of every cell.
   if (f.P.use_convnet_traversability)
@@ -1908,9 +1916,9 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   phaseBegin(f, false);
   // count[] is all zero here: k_cells clears it after its last use each scan.
   const SortGeom sg = phaseSortGeometry(f, N);
-  checkCuda(cudaEventRecord(m.ev[1], f.s), "event");  // resets done
+  RB_PHASE_EVENT(1, f.s);  // resets done
   phaseIngest(f, d_xyz, N, sg, true, chunked);
-  checkCuda(cudaEventRecord(m.ev[2], f.s), "event");  // ingest done
+  RB_PHASE_EVENT(2, f.s);  // ingest done
   if (n > 0 && P.drift.enabled) {
     launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
                                           P.drift.min_points, P.drift.max_offset_per_scan,
@@ -1918,17 +1926,17 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
     f.launches += 2;
   }
-  checkCuda(cudaEventRecord(m.ev[3], f.s), "event");  // drift done
+  RB_PHASE_EVENT(3, f.s);  // drift done
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
     phaseRaysPass1(f, N, 0);
     phaseRemovePass2(f, 0);
   } else {
-    checkCuda(cudaEventRecord(m.ev[4], f.s), "event");
-    checkCuda(cudaEventRecord(m.ev[5], f.s), "event");
+    RB_PHASE_EVENT(4, f.s);
+    RB_PHASE_EVENT(5, f.s);
   }
-  checkCuda(cudaEventRecord(m.ev[6], f.s), "event");  // rays done
+  RB_PHASE_EVENT(6, f.s);  // rays done
   phaseCells(f);
   const DevStats& d = phaseStats(f);
   ScanResult out = resultFrom(d, n);
@@ -1937,6 +1945,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // (resolveTiming): nine event queries cost ~30 us of host time per call.
   m.timing_pending = true;
   m.timing_chunked = chunked;
+  m.timing_phases = m.phase_events;
   out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call).count();
   m.last_launches = f.launches;
   m.last_visits = static_cast<long long>(d.visits);
@@ -1950,6 +1959,17 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
 void resolveTiming(DeviceMap& m) {
   if (!m.timing_pending) return;
   m.timing_pending = false;
+  if (!m.timing_phases) {  // only the upload and the device total were recorded
+    float ms_copy = 0.0f, ms_total = 0.0f;
+    checkCuda(cudaEventElapsedTime(&ms_copy, m.ev[0], m.ev[13]), "timing");
+    checkCuda(cudaEventElapsedTime(&ms_total, m.ev[13], m.ev[12]), "timing");
+    for (double& v : m.kernel_seconds) v = 0.0;
+    for (double& v : m.phase_seconds) v = 0.0;
+    m.kernel_seconds[0] = ms_copy * 1e-3;
+    m.kernel_seconds[7] = std::max(0.0f, ms_total) * 1e-3;
+    m.phase_seconds[6] = m.kernel_seconds[7];
+    return;
+  }
   float ms[7], ms_trav = 0.0f, ms_copy = 0.0f, ms_reset = 0.0f;
   for (int k = 1; k < 7; ++k) checkCuda(cudaEventElapsedTime(&ms[k], m.ev[k], m.ev[k + 1]), "timing");
   checkCuda(cudaEventElapsedTime(&ms_trav, m.ev[7], m.ev[12]), "timing");
@@ -2013,10 +2033,10 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   const SortGeom sg = phaseSortGeometry(f, N);  // count[] is zero (cleared by k_cells)
   if (n > 0) checkCuda(cudaStreamWaitEvent(f.s, m.ev_copied[slot], 0), "stream wait");
   checkCuda(cudaEventRecord(m.ev_start[slot], f.s), "event");
-  checkCuda(cudaEventRecord(m.ev[1], f.s), "event");
+  RB_PHASE_EVENT(1, f.s);
   phaseIngest(f, d_xyz, N, sg, true);
   checkCuda(cudaEventRecord(m.ev_consumed[slot], f.s), "event");
-  checkCuda(cudaEventRecord(m.ev[2], f.s), "event");
+  RB_PHASE_EVENT(2, f.s);
   if (n > 0 && P.drift.enabled) {
     launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
                                           P.drift.min_points, P.drift.max_offset_per_scan,
@@ -2024,17 +2044,17 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
     launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
     f.launches += 2;
   }
-  checkCuda(cudaEventRecord(m.ev[3], f.s), "event");
+  RB_PHASE_EVENT(3, f.s);
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
     phaseRaysPass1(f, N, 0);
     phaseRemovePass2(f, 0);
   } else {
-    checkCuda(cudaEventRecord(m.ev[4], f.s), "event");
-    checkCuda(cudaEventRecord(m.ev[5], f.s), "event");
+    RB_PHASE_EVENT(4, f.s);
+    RB_PHASE_EVENT(5, f.s);
   }
-  checkCuda(cudaEventRecord(m.ev[6], f.s), "event");
+  RB_PHASE_EVENT(6, f.s);
   phaseCells(f);
   checkCuda(cudaMemcpyAsync(m.h_slot[slot], m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, f.s),
             "stats");

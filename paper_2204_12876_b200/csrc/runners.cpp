@@ -42,7 +42,9 @@ int currentDevice() {
 // Stateful wrapper tracking the inter-scan dt (reference integration.hpp:146-169).
 class Pipeline {
  public:
-  Pipeline(const Grid& g, const PipelineParams& p) : map_(createDeviceMap(currentDevice(), g)), params_(p) {}
+  Pipeline(const Grid& g, const PipelineParams& p) : map_(createDeviceMap(currentDevice(), g)), params_(p) {
+    map_->phase_events = true;  // the runners report the reference's per-phase timings
+  }
   ScanResult integrate(const std::vector<double>& xyz, const Pose& pose, double stamp) {
     if (!pose.isValid()) fail(Err::kInvalidPose, "rotation is not orthonormal");
     const double dt = has_prev_ ? std::max(0.0, stamp - last_) : 0.0;
