@@ -1,0 +1,51 @@
+// Launch chaining shared by the frame pipeline and the post-processing chain.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <utility>
+
+#include "device_map.hpp"
+
+namespace rb200 {
+
+// Programmatic dependent launch (sm_90+): consecutive frame kernels on the
+// library stream are launched with programmatic stream serialisation, and
+// every such kernel lets its dependent launch as soon as all of its blocks
+// are resident, then waits for its predecessor's completion (and memory)
+// before touching any data. The dependent's launch and block scheduling thus
+// overlap the predecessor's tail; the data order is unchanged.
+#ifndef RB_PDL
+#define RB_PDL 1
+#endif
+__device__ __forceinline__ void pdlEnter() {
+#if RB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+void launchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+               Args&&... args) {
+#if RB_PDL
+  if (s == nullptr) {  // the legacy default stream: plain launch
+    kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  checkCuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+#else
+  kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+#endif
+}
+
+}  // namespace rb200

@@ -28,6 +28,7 @@
 #include <cstring>
 
 #include "device_map.hpp"
+#include "launch.cuh"
 #include "fp_exact.cuh"
 
 namespace rb200 {
@@ -36,21 +37,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// Programmatic dependent launch (sm_90+): consecutive frame kernels on the
-// library stream are launched with programmatic stream serialisation, and
-// every such kernel lets its dependent launch as soon as all of its blocks
-// are resident, then waits for its predecessor's completion (and memory)
-// before touching any data. The dependent's launch and block scheduling thus
-// overlap the predecessor's tail; the data order is unchanged.
-#ifndef RB_PDL
-#define RB_PDL 1
-#endif
-__device__ __forceinline__ void pdlEnter() {
-#if RB_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-}
 constexpr double kInf = __builtin_huge_val();
 
 __device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
@@ -1505,26 +1491,6 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   if (((threadIdx.y * kTileX + threadIdx.x) & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
 }
 
-
-template <typename... KArgs, typename... Args>
-void launchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
-               Args&&... args) {
-#if RB_PDL
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  checkCuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
-#else
-  kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
-#endif
-}
 
 // Phase-boundary events (per-phase device times); an event between two
 // kernels also ends their programmatic overlap, so they are recorded only

@@ -18,6 +18,7 @@
 
 #include "device_map.hpp"
 #include "fp_exact.cuh"
+#include "launch.cuh"
 #include "runners.hpp"
 #include "snapshot.hpp"
 
@@ -36,6 +37,7 @@ __global__ void __launch_bounds__(kT) k_linear(const double* __restrict__ v,
                                                const uint8_t* __restrict__ ok, int W, int H,
                                                int R, Weights wt, double* __restrict__ out,
                                                uint8_t* __restrict__ ok_out) {
+  pdlEnter();
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= W * H) return;
   ok_out[i] = ok[i];
@@ -65,6 +67,7 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
                                                const uint8_t* __restrict__ ok, int W, int H,
                                                int R, double* __restrict__ out,
                                                uint8_t* __restrict__ ok_out) {
+  pdlEnter();
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= W * H) return;
   ok_out[i] = ok[i];
@@ -106,6 +109,7 @@ __global__ void __launch_bounds__(kSX* kSY) k_stencil_tile(const double* __restr
                                                            int H, Weights wt,
                                                            double* __restrict__ out,
                                                            uint8_t* __restrict__ ok_out) {
+  pdlEnter();
   static_assert(KIND == 0, "linear filter only");
   constexpr int TW = kSX + 2 * R, TH = kSY + 2 * R, k = 2 * R + 1;
   __shared__ double sv[TH * TW];
@@ -155,9 +159,9 @@ bool launchStencilTile(int R, const double* v, const uint8_t* ok, int W, int H, 
                        double* out, uint8_t* ok_out, cudaStream_t s) {
   const dim3 grid((W + kSX - 1) / kSX, (H + kSY - 1) / kSY), block(kSX, kSY);
   switch (R) {
-    case 1: k_stencil_tile<1, KIND><<<grid, block, 0, s>>>(v, ok, W, H, wt, out, ok_out); return true;
-    case 2: k_stencil_tile<2, KIND><<<grid, block, 0, s>>>(v, ok, W, H, wt, out, ok_out); return true;
-    case 3: k_stencil_tile<3, KIND><<<grid, block, 0, s>>>(v, ok, W, H, wt, out, ok_out); return true;
+    case 1: launchPdl(k_stencil_tile<1, KIND>, grid, block, 0, s, v, ok, W, H, wt, out, ok_out); return true;
+    case 2: launchPdl(k_stencil_tile<2, KIND>, grid, block, 0, s, v, ok, W, H, wt, out, ok_out); return true;
+    case 3: launchPdl(k_stencil_tile<3, KIND>, grid, block, 0, s, v, ok, W, H, wt, out, ok_out); return true;
     default: return false;
   }
 }
@@ -223,6 +227,7 @@ constexpr int kTileCC = 32;
 __global__ void __launch_bounds__(kTileCC* kTileCC)
     k_cc_tile(const uint8_t* ok, int W, int H, int* parent, unsigned long long* key,
               uint8_t* border, int* any_valid) {
+  pdlEnter();
   __shared__ int lab[kTileCC * kTileCC];
   const int tx = threadIdx.x % kTileCC, ty = threadIdx.x / kTileCC;
   const int c = blockIdx.x * kTileCC + tx, r = blockIdx.y * kTileCC + ty;
@@ -275,6 +280,7 @@ __global__ void __launch_bounds__(kTileCC* kTileCC)
 // usually join the same pair of tile roots, so each warp hooks every distinct
 // (root, root) pair once.
 __global__ void __launch_bounds__(kT) k_cc_merge(const uint8_t* ok, int W, int H, int* parent) {
+  pdlEnter();
   const int q = blockIdx.x * kT + threadIdx.x;
   const int vx = (W - 1) / kTileCC;  // vertical boundaries
   const int hy = (H - 1) / kTileCC;  // horizontal boundaries
@@ -304,6 +310,7 @@ __global__ void __launch_bounds__(kT) k_cc_merge(const uint8_t* ok, int W, int H
 __global__ void __launch_bounds__(kT) k_cc_border(const double* v, const uint8_t* ok, int W, int H,
                                                   int* parent, unsigned long long* key,
                                                   uint8_t* border, int* flag) {
+  pdlEnter();
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i == 0) {
     if (flag[0] == 0) flag[1] = 1;
@@ -341,6 +348,7 @@ __global__ void __launch_bounds__(kT) k_cc_fill(const double* v, const uint8_t* 
                                                 const int* parent, const unsigned long long* key,
                                                 const uint8_t* border, double* out,
                                                 uint8_t* ok_out) {
+  pdlEnter();
   const int i = blockIdx.x * kT + threadIdx.x;
   if (i >= n) return;
   if (ok[i]) {
@@ -429,18 +437,18 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
           wt.w[(dr + st.radius) * kk + (dc + st.radius)] =
               st.kind == 1 ? 1.0 : std::exp(-(dr * dr + dc * dc) / (2.0 * st.sigma * st.sigma));
       if (!launchStencilTile<0>(st.radius, cv, co, W, H, wt, nv, no, s))
-        k_linear<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, wt, nv, no);
+        launchPdl(k_linear, grid, kT, 0, s, cv, co, W, H, st.radius, wt, nv, no);
       ++launches;
     } else if (st.kind == 2) {
-      k_median<<<grid, kT, 0, s>>>(cv, co, W, H, st.radius, nv, no);
+      launchPdl(k_median, grid, kT, 0, s, cv, co, W, H, st.radius, nv, no);
       ++launches;
     } else {
       const dim3 tiles((W + kTileCC - 1) / kTileCC, (H + kTileCC - 1) / kTileCC);
-      k_cc_tile<<<tiles, kTileCC * kTileCC, 0, s>>>(co, W, H, sc.parent, sc.key, sc.border, sc.flag);
+      launchPdl(k_cc_tile, tiles, kTileCC * kTileCC, 0, s, co, W, H, sc.parent, sc.key, sc.border, sc.flag);
       const int edges = H * ((W - 1) / kTileCC) + W * ((H - 1) / kTileCC);
-      if (edges > 0) k_cc_merge<<<(edges + kT - 1) / kT, kT, 0, s>>>(co, W, H, sc.parent);
-      k_cc_border<<<grid, kT, 0, s>>>(cv, co, W, H, sc.parent, sc.key, sc.border, sc.flag);
-      k_cc_fill<<<grid, kT, 0, s>>>(cv, co, n, sc.parent, sc.key, sc.border, nv, no);
+      if (edges > 0) launchPdl(k_cc_merge, (edges + kT - 1) / kT, kT, 0, s, co, W, H, sc.parent);
+      launchPdl(k_cc_border, grid, kT, 0, s, cv, co, W, H, sc.parent, sc.key, sc.border, sc.flag);
+      launchPdl(k_cc_fill, grid, kT, 0, s, cv, co, n, sc.parent, sc.key, sc.border, nv, no);
       launches += 3 + (edges > 0 ? 1 : 0);
     }
     cv = nv;
