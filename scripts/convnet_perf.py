@@ -28,6 +28,7 @@ cfgp.write_text(w.config_text)
 cfg = pk.Config.load(lib, cfgp)
 cfg.load_convnet(model)
 m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height)
+m.set_phase_timing(True)  # per-phase split (phase events on)
 calls = [w.calls(f)[0] for f in range(2)]
 clouds = [pk.sim_render(lib, cfgp, c.pose, c.time, c.seed, c.scan_index) for c in calls]
 names = ["transform", "drift", "update+rays", "overlap+normals", "traversability", "normals", "total"]
