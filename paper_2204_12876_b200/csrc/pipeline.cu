@@ -1530,6 +1530,7 @@ struct Frame {
   GridArgs g;
   long long launches = 0;
   bool overlap = false;  // heavy cells folded on stream2 during the ray pass
+  FuseArgs fa{};          // fusion parameters of the frame (for the side-stream fold)
   // Per-ray endpoint cell from k_ingest (indexed like the rays), or null when
   // the sort has overwritten it (3 passes) or the rays are a shard's.
   const uint32_t* point_cells = nullptr;
@@ -1674,6 +1675,21 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
 // K2 over N keys (cells; >= WH = not sorted) with payload (z, var) indexed
 // by key position; then K3 gated fusion. Long cells go to stream2 when the
 // ray pass can overlap them.
+// The long-cell fold on the side stream, after the short-cell fold (whose
+// ballots build its lists) and before the ray pass it overlaps.
+void launchHeavy(Frame& f) {
+  if (!f.overlap) return;
+  DeviceMap& m = f.m;
+  const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
+  checkCuda(cudaEventRecord(m.ev[10], f.s), "event");
+  checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
+  k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.heavy + f.ncell, m.stats,
+                                                    m.start, m.spz, m.spv, f.fa, m.stats,
+                                                    f.P.cleanup.t_free, cleanup, bound);
+  ++f.launches;
+  checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
+}
+
 void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, const double* var,
                    const SortGeom& sg) {
   DeviceMap& m = f.m;
@@ -1712,16 +1728,10 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
                                                m.stats, f.heavy, m.heavy, m.heavy + f.ncell);
   ++f.launches;
-  if (f.overlap) {
-    checkCuda(cudaEventRecord(m.ev[10], s), "event");
-    checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
-    k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.heavy + f.ncell, m.stats,
-                                                      m.start, m.spz,
-                                                      m.spv, fa, m.stats, f.P.cleanup.t_free, cleanup,
-                                                      bound);
-    ++f.launches;
-    checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
-  }
+  f.fa = fa;
+  // (Launching it after k_classify instead, to keep that kernel boundary programmatic, made
+  // the frame 15 % slower: the side-stream blocks then queue behind the ray pass.)
+  launchHeavy(f);
   RB_PHASE_EVENT(5, s);  // fusion done (short cells when overlapped)
 }
 
