@@ -1381,6 +1381,9 @@ constexpr int kTileX = 32, kTileY = 8;
 // (grid.cpp:113-124, integration.cpp:252-257) in one pass over a shared
 // memory tile with a (radius)-cell halo. Overlap is evaluated for halo cells
 // too, so every thread sees the post-clearance validity of its window.
+// RT: the traversability window radius when known at compile time (the 5x5
+// default and 3x3 are instantiated; 0 = from CellArgs).
+template <int RT>
 __global__ void __launch_bounds__(kTileX* kTileY)
     k_cells(Layers L, int32_t* __restrict__ count, uint32_t* __restrict__ seg_start, CellArgs a,
             DevStats* st) {
@@ -1462,12 +1465,13 @@ __global__ void __launch_bounds__(kTileX* kTileY)
         const double s_slope = sclamp(1.0 - slope / a.slope_max, 0.0, 1.0);
         double max_step = 0.0, sum = 0.0, sum_sq = 0.0;
         int cntw = 0;
-        for (int dr = -a.radius; dr <= a.radius; ++dr) {
-          const int rr = r + dr;
-          if (rr < 0 || rr >= H) continue;
-          for (int dc = -a.radius; dc <= a.radius; ++dc) {
-            const int cc = c + dc;
-            if (cc < 0 || cc >= W) continue;
+        // Row-major window over valid cells (cells outside the grid are staged
+        // as invalid, so they are skipped like the reference's bounds test).
+        const int R = RT > 0 ? RT : a.radius;
+#pragma unroll
+        for (int dr = -R; dr <= R; ++dr) {
+#pragma unroll
+          for (int dc = -R; dc <= R; ++dc) {
             const int q = (lr + dr) * tw + (lc + dc);
             if (!sv[q]) continue;
             const double v = se[q];
@@ -1828,11 +1832,12 @@ void phaseCells(Frame& f) {
   const int halo = std::max(1, ca.radius);
   const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
   const dim3 grid((f.g.W + kTileX - 1) / kTileX, (f.g.H + kTileY - 1) / kTileY);
+  auto* kern = ca.radius == 2 ? k_cells<2> : (ca.radius == 1 ? k_cells<1> : k_cells<0>);
   if (sm > 48 * 1024)
-    checkCuda(cudaFuncSetAttribute(k_cells, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    checkCuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(sm)),
               "smem attribute");
-  launchPdl(k_cells, grid, dim3(kTileX, kTileY), sm, f.s, m.cur, m.count, m.start, ca, m.stats);
+  launchPdl(kern, grid, dim3(kTileX, kTileY), sm, f.s, m.cur, m.count, m.start, ca, m.stats);
   ++f.launches;
   RB_PHASE_EVENT(7, f.s);  // cell phases done
   // Conv-net traversability (reference integration.cpp:242-244): reads the
