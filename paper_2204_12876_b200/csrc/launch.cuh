@@ -18,6 +18,16 @@ namespace rb200 {
 #ifndef RB_PDL
 #define RB_PDL 1
 #endif
+__device__ __forceinline__ void pdlTrigger() {
+#if RB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdlWait() {
+#if RB_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void pdlEnter() {
 #if RB_PDL
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
