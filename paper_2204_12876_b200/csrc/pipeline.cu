@@ -886,14 +886,10 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
                                                        const int32_t* __restrict__ count,
                                                        int heavy, int retry, DevStats* st,
                                                        ProbeT* probe) {
-#ifdef RB_P1_PROLOGUE
   // wait first: the ray pass launched on our trigger may then read anything
   // older than this kernel before its own wait
   pdlWait();
   pdlTrigger();
-#else
-  pdlEnter();
-#endif
   if (retry) {
     if (!st->respeculate) return;
     __syncthreads();
@@ -1178,9 +1174,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   const double dy = py - o[1];
   const double res = g.res;
   if (!(fabs(dx) >= 2e-12 || fabs(dy) >= 2e-12) && libm_hypot(dx, dy) < 1e-12) {
-#ifdef RB_P1_PROLOGUE
     pdlWait();
-#endif
     if (o[0] >= g.ox && o[0] < g.xmax && o[1] >= g.oy && o[1] < g.ymax) {
       const uint32_t idx =
           static_cast<uint32_t>(clampCell(x86_to_int(floor((o[1] - g.oy) / res)), g.H)) * g.W +
@@ -1234,9 +1228,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   int xl = step_col > 0 ? g.W - 1 - col : (step_col < 0 ? col : 0);
   int yl = step_row > 0 ? g.H - 1 - row : (step_row < 0 ? row : 0);
   const ProbeT* __restrict__ probe = c.probe;
-#ifdef RB_P1_PROLOGUE
   pdlWait();  // class / probe words come from k_classify
-#endif
   uint32_t wd = probe[idx];
   double t_enter = t0;
   // The axis step is written without branches around it (both sides predicate
@@ -1297,11 +1289,7 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
                  DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
                  const uint32_t* __restrict__ pcell) {
-#ifdef RB_P1_PROLOGUE
   pdlTrigger();  // the per-ray setup below runs before the wait (inputs from k_ingest)
-#else
-  pdlEnter();
-#endif
   if (retry && !st->respeculate) return;
   // kStride (the retry launch): grid-stride over ray tiles with a one-wave
   // grid, so its common no-op case costs one wave of returning blocks. The
@@ -1318,9 +1306,7 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
     if (isfinite(c.vx) && isfinite(c.vy)) {
       pass1Finite(a.g, a.o, ex, ey, c, touched, visits, a, pcell ? pcell[k] : 0xffffffffu);
     } else {
-#ifdef RB_P1_PROLOGUE
       pdlWait();
-#endif
       walkRay(a.g, a.o, ex, ey, [&](uint32_t cell, double te, double tn, bool vertical) {
         ++visits;
         const uint8_t cl = cls[cell];
