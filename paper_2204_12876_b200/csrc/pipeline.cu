@@ -1314,6 +1314,9 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
       });
     }
   }
+  // Every thread is past the wait before the counters (a retry's k_classify
+  // resets them); rays that needed no class data skipped it so far.
+  pdlWait();
   // Queue rays that crossed a removal candidate for the k* pass (one atomic per warp).
   const unsigned lane = threadIdx.x & 31;
   const unsigned want = __ballot_sync(0xffffffffu, touched && a.bound);
