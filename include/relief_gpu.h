@@ -32,7 +32,9 @@ RELIEF_API int relief_gpu_map_device(const relief_map* map);
 
 /* relief_map_integrate with the point stream already in device memory of the
  * map's device (d_xyz: 3*n doubles, x y z packed). Synchronous like the
- * reference call: stats are final on return. */
+ * reference call: stats are final on return. d_xyz must be complete when the
+ * call is made: produced on another stream, order it first with
+ * relief_gpu_map_after_stream. */
 RELIEF_API relief_status relief_gpu_map_integrate_device(relief_map* map,
                                                          const relief_config* config,
                                                          const double* d_xyz, size_t n_points,
@@ -150,7 +152,13 @@ RELIEF_API relief_status relief_gpu_convnet_infer(const relief_config* config, c
  * The result equals relief_map_integrate of the whole frame on one GPU (bit for
  * bit; with drift enabled the offset is the ranks' partial sums added in rank
  * order, so heights agree to the drift tolerance). Device pointers stay valid
- * until the next integrate / shard call on the map. */
+ * until the next integrate / shard call on the map.
+ * Ordering: every shard call returns with its outputs complete. The exchanged
+ * inputs of the next call (records, k*, bounds) are read on the map's own
+ * stream: if the caller's transport wrote them on another stream (NCCL under
+ * torch.distributed, cudaMemcpyAsync, ...), it must call
+ * relief_gpu_map_after_stream(map, that_stream) (or synchronise it) first.
+ * relief_gpu_group_* does the whole frame, exchanges included, in-library. */
 typedef struct relief_gpu_shard_io {
   int64_t n_records;
   double drift[2];       /* local drift vote: sum, count */
@@ -177,6 +185,64 @@ RELIEF_API relief_status relief_gpu_shard_remove(relief_map* map, int64_t* remov
                                                  relief_gpu_shard_io* io);
 RELIEF_API relief_status relief_gpu_shard_finish(relief_map* map, const int64_t counters_total[3],
                                                  uint64_t points_total, relief_scan_stats* stats);
+
+/* ---- Group frames: one frame split across GPUs, exchanges inside the library
+ * (SURVEY.md §8e exact variant). Replaces the point loop of the
+ * reference's integrateScan (integration.cpp:142-224) by a split of the
+ * frame's points into contiguous batches, one per rank, in scan order:
+ *   relief_gpu_group_bounds(n_total, n_ranks, rank) -> [lo, hi) of the rank
+ *   (whole radix tiles, so the gathered arrays equal the single-GPU ones).
+ * Every rank keeps a full replica of the map. Per frame each rank ingests its
+ * batch; the library all-gathers the cell keys, p_z, sigma_p^2 and drift
+ * partials, runs the (identical) count, sort, gated fusion and drift offset on
+ * every rank, casts its own rays, and merges k* / bounds / validity with
+ * min / min / max all-reduces -- all on the map's stream, one host sync per
+ * frame (the stats). The maps and stats equal relief_map_integrate of the
+ * whole frame on one GPU bit for bit, drift compensation included.
+ * Transports:
+ *   relief_gpu_group_create: one process per GPU over NCCL (libnccl.so.2,
+ *   loaded at run time; a copy already in the process is reused). Rank 0 makes
+ *   the id with relief_gpu_group_unique_id and the caller broadcasts its 128
+ *   bytes (MPI, torch.distributed, a file); every rank then calls create
+ *   collectively. relief_gpu_group_integrate takes this rank's batch
+ *   (xyz = points [lo, hi) of the frame, n_points = hi - lo) and must be
+ *   called by every rank for every frame, in the same order.
+ *   relief_gpu_group_create_local: one process drives n_maps maps (on several
+ *   GPUs, or replicas on one GPU); the exchanges are peer copies and a
+ *   reduction kernel. relief_gpu_group_integrate then takes the whole frame.
+ * The maps must have the same geometry and history. The group does not own
+ * them: free the group before its maps. Ordering: the group's work runs on
+ * the maps' streams; device input must be complete before the call (see
+ * relief_gpu_map_after_stream). Errors: RELIEF_ERROR_USAGE (bad rank / batch
+ * size / geometry), RELIEF_ERROR_DATA (CUDA / NCCL failure, message set). */
+typedef struct relief_gpu_group relief_gpu_group;
+#define RELIEF_GPU_GROUP_ID_BYTES 128
+RELIEF_API relief_status relief_gpu_group_unique_id(uint8_t id_out[RELIEF_GPU_GROUP_ID_BYTES]);
+RELIEF_API relief_gpu_group* relief_gpu_group_create(relief_map* map,
+                                                     const uint8_t id[RELIEF_GPU_GROUP_ID_BYTES],
+                                                     int n_ranks, int rank);
+RELIEF_API relief_gpu_group* relief_gpu_group_create_local(relief_map* const* maps, int n_maps);
+RELIEF_API void relief_gpu_group_free(relief_gpu_group* group);
+RELIEF_API relief_status relief_gpu_group_bounds(uint64_t n_total, int n_ranks, int rank,
+                                                 uint64_t* lo, uint64_t* hi);
+RELIEF_API relief_status relief_gpu_group_integrate(relief_gpu_group* group,
+                                                    const relief_config* config,
+                                                    const double* xyz, size_t n_points,
+                                                    int xyz_on_device, uint64_t n_total,
+                                                    const double pose[12], double stamp,
+                                                    relief_scan_stats* stats_out);
+/* Version of the NCCL library the group transport uses (e.g. 22809), or -1. */
+RELIEF_API int relief_gpu_nccl_version(void);
+
+/* Stream ordering for device-resident input: everything enqueued so far on
+ * cuda_stream (a cudaStream_t of this process, on the map's device; NULL = the
+ * legacy default stream) completes before the map's next device work reads
+ * anything. The library runs on its own non-blocking stream, so a caller that
+ * produces d_xyz (or exchanged shard buffers) on another stream calls this
+ * before relief_gpu_map_integrate_device / relief_gpu_shard_* / the group
+ * calls. Host synchronisation is not needed. Outputs are complete when a
+ * synchronous call returns. */
+RELIEF_API relief_status relief_gpu_map_after_stream(relief_map* map, void* cuda_stream);
 
 /* Synthetic scan: scene + sensor of a reliefmap config file, rendered from
  * pose (row-major [R|t]) at `time` with splitmix64 stream (seed, scan_index)

@@ -146,6 +146,16 @@ RELIEF_GPU_H_SIGNATURES = {
                                      ctypes.POINTER(ScanStats)]),
     "relief_gpu_sim_render": (ctypes.c_int64, [_CS, _DP, _D, ctypes.c_uint64, ctypes.c_uint64, _DP,
                                                ctypes.c_int64]),
+    "relief_gpu_map_after_stream": (_I, [_P, ctypes.c_void_p]),
+    "relief_gpu_group_unique_id": (_I, [ctypes.c_void_p]),
+    "relief_gpu_group_create": (_P, [_P, ctypes.c_void_p, _I, _I]),
+    "relief_gpu_group_create_local": (_P, [ctypes.POINTER(_P), _I]),
+    "relief_gpu_group_free": (None, [_P]),
+    "relief_gpu_group_bounds": (_I, [ctypes.c_uint64, _I, _I, ctypes.POINTER(ctypes.c_uint64),
+                                     ctypes.POINTER(ctypes.c_uint64)]),
+    "relief_gpu_group_integrate": (_I, [_P, _P, ctypes.c_void_p, _SZ, _I, ctypes.c_uint64, _DP, _D,
+                                        ctypes.POINTER(ScanStats)]),
+    "relief_gpu_nccl_version": (_I, []),
 }
 
 
@@ -377,9 +387,92 @@ class ReliefMap:
             ctypes.c_void_p(d_valid)))
         return float(self.lib.relief_gpu_map_chain_seconds(self.handle))
 
+    def after_stream(self, stream_handle: int) -> None:
+        """relief_gpu_map_after_stream: order the map's next device work after everything
+        already enqueued on that cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        _check(self.lib, self.lib.relief_gpu_map_after_stream(self.handle, ctypes.c_void_p(stream_handle)))
+
     def close(self) -> None:
         if self.handle:
             self.lib.relief_map_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def group_bounds(lib, n_total: int, ranks: int, rank: int):
+    """relief_gpu_group_bounds: rank's batch [lo, hi) of an n_total-point frame."""
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib, lib.relief_gpu_group_bounds(n_total, ranks, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return int(lo.value), int(hi.value)
+
+
+def group_unique_id(lib) -> bytes:
+    """relief_gpu_group_unique_id: the 128-byte NCCL id rank 0 broadcasts."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib, lib.relief_gpu_group_unique_id(buf))
+    return bytes(buf)
+
+
+class Group:
+    """relief_gpu_group: one frame split across the ranks of a group (include/relief_gpu.h).
+
+    nccl(lib, map, uid, ranks, rank): one process per GPU, NCCL transport -- integrate() takes
+    this rank's batch. local(lib, maps): one process drives every map -- integrate() takes the
+    whole frame."""
+
+    def __init__(self, lib, handle, maps, ranks: int, rank: int, local: bool):
+        self.lib, self.handle, self.maps = lib, handle, maps
+        self.ranks, self.rank, self.local = ranks, rank, local
+
+    @classmethod
+    def nccl(cls, lib, rmap: ReliefMap, uid: bytes, ranks: int, rank: int) -> "Group":
+        if len(uid) != 128:
+            raise ValueError("the NCCL unique id is 128 bytes")
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = lib.relief_gpu_group_create(rmap.handle, buf, ranks, rank)
+        if not h:
+            raise ReliefError(2, lib.relief_last_error().decode())
+        return cls(lib, h, [rmap], ranks, rank, False)
+
+    @classmethod
+    def local(cls, lib, maps: Sequence[ReliefMap]) -> "Group":
+        arr = (_P * len(maps))(*[m.handle for m in maps])
+        h = lib.relief_gpu_group_create_local(arr, len(maps))
+        if not h:
+            raise ReliefError(1, lib.relief_last_error().decode())
+        return cls(lib, h, list(maps), len(maps), 0, True)
+
+    def bounds(self, n_total: int, rank: Optional[int] = None):
+        return group_bounds(self.lib, n_total, self.ranks, self.rank if rank is None else rank)
+
+    def integrate(self, xyz, n_total: int, pose, stamp: float, config: Optional[Config] = None) -> ScanStats:
+        """Host points: this rank's batch (NCCL) or the whole frame (local)."""
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1)
+        pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+        st = ScanStats()
+        _check(self.lib, self.lib.relief_gpu_group_integrate(
+            self.handle, config.handle if config is not None else None,
+            xyz.ctypes.data_as(ctypes.c_void_p) if xyz.size else None, xyz.size // 3, 0, n_total,
+            _dptr(pose), stamp, ctypes.byref(st)))
+        return st
+
+    def integrate_device(self, d_xyz_ptr: int, n: int, n_total: int, pose, stamp: float,
+                         config: Optional[Config] = None) -> ScanStats:
+        pose = np.ascontiguousarray(pose, dtype=np.float64).reshape(12)
+        st = ScanStats()
+        _check(self.lib, self.lib.relief_gpu_group_integrate(
+            self.handle, config.handle if config is not None else None, ctypes.c_void_p(d_xyz_ptr), n, 1,
+            n_total, _dptr(pose), stamp, ctypes.byref(st)))
+        return st
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.relief_gpu_group_free(self.handle)
             self.handle = None
 
     def __del__(self):

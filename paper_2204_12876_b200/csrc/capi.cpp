@@ -8,9 +8,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "../../include/relief_gpu.h"
 #include "device_map.hpp"
@@ -23,6 +25,11 @@ struct relief_config {
 
 struct relief_map {
   rb200::DeviceMap* dev = nullptr;
+};
+
+struct relief_gpu_group {
+  rb200::Group* g = nullptr;
+  std::vector<relief_map*> maps;
 };
 
 namespace {
@@ -536,6 +543,113 @@ relief_status relief_gpu_shard_finish(relief_map* map, const int64_t counters_to
   return guard([&] {
     const rb200::ScanResult r = rb200::shardFinish(*map->dev, counters_total, points_total);
     fillStats(r, stats);
+  });
+}
+
+relief_status relief_gpu_map_after_stream(relief_map* map, void* cuda_stream) {
+  if (map == nullptr) return usage("null argument");
+  return guard([&] {
+    rb200::DeviceMap& m = *map->dev;
+    rb200::checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+    rb200::checkCuda(cudaEventRecord(m.ev_after, static_cast<cudaStream_t>(cuda_stream)),
+                     "event record on the caller's stream");
+    rb200::checkCuda(cudaStreamWaitEvent(m.stream, m.ev_after, 0), "stream wait");
+  });
+}
+
+relief_status relief_gpu_group_unique_id(uint8_t id_out[RELIEF_GPU_GROUP_ID_BYTES]) {
+  if (id_out == nullptr) return usage("null argument");
+  return guard([&] { rb200::groupUniqueId(id_out); });
+}
+
+int relief_gpu_nccl_version(void) {
+  int v = -1;
+  guard([&] { v = rb200::groupNcclVersion(); });
+  return v;
+}
+
+relief_gpu_group* relief_gpu_group_create(relief_map* map,
+                                          const uint8_t id[RELIEF_GPU_GROUP_ID_BYTES],
+                                          int n_ranks, int rank) {
+  if (map == nullptr || id == nullptr) {
+    t_last_error = "null argument";
+    return nullptr;
+  }
+  return guardCreate<relief_gpu_group>([&] {
+    auto* g = new relief_gpu_group{};
+    try {
+      g->g = rb200::groupCreateNccl(map->dev, id, n_ranks, rank);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    g->maps = {map};
+    return g;
+  });
+}
+
+relief_gpu_group* relief_gpu_group_create_local(relief_map* const* maps, int n_maps) {
+  if (maps == nullptr || n_maps <= 0) {
+    t_last_error = "null argument";
+    return nullptr;
+  }
+  return guardCreate<relief_gpu_group>([&] {
+    std::vector<rb200::DeviceMap*> dev;
+    for (int r = 0; r < n_maps; ++r) {
+      if (maps[r] == nullptr) rb200::fail(rb200::Err::kUsage, "null map in the group");
+      dev.push_back(maps[r]->dev);
+    }
+    auto* g = new relief_gpu_group{};
+    try {
+      g->g = rb200::groupCreateLocal(dev);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    g->maps.assign(maps, maps + n_maps);
+    return g;
+  });
+}
+
+void relief_gpu_group_free(relief_gpu_group* group) {
+  if (group == nullptr) return;
+  rb200::groupDestroy(group->g);
+  delete group;
+}
+
+relief_status relief_gpu_group_bounds(uint64_t n_total, int n_ranks, int rank, uint64_t* lo,
+                                      uint64_t* hi) {
+  if (lo == nullptr || hi == nullptr) return usage("null argument");
+  return guard([&] {
+    const rb200::GroupGeom g = rb200::groupGeom(n_total, n_ranks, rank);
+    *lo = g.lo;
+    *hi = static_cast<uint64_t>(g.lo) + g.n_local;
+  });
+}
+
+relief_status relief_gpu_group_integrate(relief_gpu_group* group, const relief_config* config,
+                                         const double* xyz, size_t n_points, int xyz_on_device,
+                                         uint64_t n_total, const double pose[12], double stamp,
+                                         relief_scan_stats* stats_out) {
+  if (group == nullptr || pose == nullptr || (xyz == nullptr && n_points > 0))
+    return usage("null argument");
+  return guard([&] {
+    const rb200::Pose p = rb200::Pose::fromRowMajor34(pose);
+    const rb200::PipelineParams params =
+        config ? config->config.pipeline : rb200::PipelineParams{};
+    validateScan(params, p);
+    std::vector<double> dts;
+    for (relief_map* m : group->maps)
+      dts.push_back(m->dev->has_last ? std::max(0.0, stamp - m->dev->last_stamp) : 0.0);
+    const auto t0 = std::chrono::steady_clock::now();
+    rb200::ScanResult r = rb200::groupIntegrate(*group->g, params, xyz, n_points,
+                                                xyz_on_device != 0, n_total, p, stamp, dts);
+    r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (relief_map* m : group->maps) {
+      m->dev->last_stamp = stamp;
+      m->dev->has_last = true;
+    }
+    fillStats(r, stats_out);
   });
 }
 

@@ -125,6 +125,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
     checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
+    checkCuda(cudaEventCreateWithFlags(&m->ev_after, cudaEventDisableTiming), "event create");
     checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev_chunk)
       checkCuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
@@ -194,6 +195,7 @@ void destroyDeviceMap(DeviceMap* m) {
   }
   for (auto& e : m->ev)
     if (e) cudaEventDestroy(e);
+  if (m->ev_after) cudaEventDestroy(m->ev_after);
   for (auto& e : m->ev_chunk)
     if (e) cudaEventDestroy(e);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -256,6 +258,7 @@ void uploadLayers(DeviceMap& m, const double* const host[8], const uint8_t* vali
   checkCuda(cudaMemcpyAsync(m.cur.valid, valid, n, cudaMemcpyHostToDevice, m.stream), "upload");
   checkCuda(cudaMemcpyAsync(m.cur.ubv, ubv, n, cudaMemcpyHostToDevice, m.stream), "upload");
   checkCuda(cudaStreamSynchronize(m.stream), "upload sync");
+  m.scrub_invalid = true;
 }
 
 void downloadLayers(const DeviceMap& m, double* const host[8], uint8_t* valid, uint8_t* ubv) {

@@ -15,6 +15,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "relief_internal.hpp"
 
@@ -157,6 +158,9 @@ struct DeviceMap {
   // host-side bookkeeping
   double last_stamp = 0.0;
   bool has_last = false;
+  // Invalid cells may hold non-zero normals / traversability (snapshot load,
+  // conv-net frame): the next cell pass zeroes them (CellArgs::scrub).
+  bool scrub_invalid = false;
   double* export_buf = nullptr;  // masked-layer staging for get_layer
   ChainScratch chain;            // post-processing chain scratch
   ConvScratch conv;              // conv-net traversability scratch
@@ -177,6 +181,7 @@ struct DeviceMap {
   double last_chain_seconds = 0.0;
   int last_chain_launches = 0;
   cudaEvent_t ev[14] = {};
+  cudaEvent_t ev_after = nullptr;  // relief_gpu_map_after_stream
   // Synchronous host-input frames: the upload is split into kChunks copies on
   // copy_stream and each chunk is ingested as soon as it lands.
   static constexpr int kChunks = 2;  // 2 and 4 measured alike; 8 slower
@@ -254,6 +259,55 @@ void shardUpdate(DeviceMap& m, const double* drift_pairs, int n_ranks, const uin
                  const double* d_z, const double* d_var, std::size_t n_records, ShardIO& io);
 int64_t shardRemove(DeviceMap& m, ShardIO& io);
 ScanResult shardFinish(DeviceMap& m, const int64_t counters_total[3], uint64_t points_total);
+
+// Group frames (pipeline.cu, SURVEY.md §8e exact variant): one frame split
+// over the ranks of a group, every rank keeping a full replica. The phases
+// enqueue on the map's stream and list the buffers to exchange after them;
+// the group's transport (group.cpp: NCCL across processes, or peer copies +
+// reduction kernels inside one process) runs the exchanges on the same stream.
+enum class XType { kU8, kI32, kU32, kU64, kF64 };
+enum class XOp { kSum, kMin, kMax };
+// All-gather: `count` elements per rank, in place (rank r's part at r*count).
+// All-reduce: `count` elements, op applied elementwise.
+struct XBuf {
+  void* ptr;
+  std::size_t count;
+  XType type;
+  XOp op;
+};
+std::size_t xtypeSize(XType t);
+struct GroupGeom {
+  int ranks = 1, rank = 0;
+  uint64_t n_total = 0;
+  uint32_t chunk = 0;    // points per rank: ceil(n_total / ranks) rounded up to a radix tile
+  uint32_t lo = 0;       // this rank's batch [lo, lo + n_local) of the frame
+  uint32_t n_local = 0;
+};
+GroupGeom groupGeom(uint64_t n_total, int ranks, int rank);
+struct GroupFrame;
+GroupFrame* groupBegin(DeviceMap& m, const PipelineParams& P, const GroupGeom& g, const Pose& pose,
+                       double stamp, double dt);
+void groupEnd(GroupFrame* gf);
+void groupPhaseIngest(GroupFrame& gf, const double* xyz, bool on_device,
+                      std::vector<XBuf>& gathers);
+void groupPhaseUpdate(GroupFrame& gf, std::vector<XBuf>& reduces);
+void groupPhaseRemove(GroupFrame& gf, std::vector<XBuf>& reduces);
+void groupPhaseCells(GroupFrame& gf, std::vector<XBuf>& reduces);
+ScanResult groupFinish(GroupFrame& gf);
+// group.cu: the group object and its transports.
+struct Group;
+void groupUniqueId(unsigned char out[128]);
+int groupNcclVersion();
+Group* groupCreateNccl(DeviceMap* m, const unsigned char id[128], int ranks, int rank);
+Group* groupCreateLocal(const std::vector<DeviceMap*>& maps);
+void groupDestroy(Group* g);
+int groupRanks(const Group& g);
+int groupRank(const Group& g);
+bool groupIsLocal(const Group& g);
+const std::vector<DeviceMap*>& groupMaps(const Group& g);
+ScanResult groupIntegrate(Group& g, const PipelineParams& P, const double* xyz, std::size_t n,
+                          bool on_device, uint64_t n_total, const Pose& pose, double stamp,
+                          const std::vector<double>& dts);
 
 // Post-processing chain on a masked layer held in device memory (postchain.cu).
 struct ChainStep {

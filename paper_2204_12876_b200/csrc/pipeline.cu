@@ -25,7 +25,9 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
+#include <vector>
 
 #include "device_map.hpp"
 #include "launch.cuh"
@@ -158,19 +160,22 @@ __global__ void __launch_bounds__(kThreads)
              double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
              uint8_t* __restrict__ kept, double* __restrict__ drift_part,
              int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
-             uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base) {
+             uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base, uint32_t in_base) {
   pdlEnter();
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
   // k_base: first point of this launch (a chunk of a frame whose upload is
   // split); block partials are indexed by the frame-wide block k / kThreads.
+  // in_base: frame index of xyz[0] (0, or a group rank's first point, whose
+  // outputs land at their frame-wide indices).
   const uint32_t k = k_base + blockIdx.x * kThreads + threadIdx.x;
   int oor = 0, exc = 0, oom = 0, dn = 0;
   double ds = 0.0;
   uint32_t cell = WH;
   if (k < n) {
-    const double x = xyz[3 * static_cast<size_t>(k)];
-    const double y = xyz[3 * static_cast<size_t>(k) + 1];
-    const double z = xyz[3 * static_cast<size_t>(k) + 2];
+    const size_t ki = 3 * static_cast<size_t>(k - in_base);
+    const double x = xyz[ki];
+    const double y = xyz[ki + 1];
+    const double z = xyz[ki + 2];
     const double sq = (x * x + y * y) + z * z;
     bool keep = false;
     if (sq > a.max_range2) {
@@ -408,10 +413,12 @@ __global__ void __launch_bounds__(kCompact)
 // gathered records of a sharded frame (the records are the sort's input).
 __global__ void __launch_bounds__(kThreads)
     k_records_count(const uint32_t* __restrict__ rcell, uint32_t m, int32_t* __restrict__ count,
-                    uint32_t* __restrict__ tc0, uint32_t pitch, uint32_t dmask) {
+                    uint32_t* __restrict__ tc0, uint32_t pitch, uint32_t dmask, uint32_t WH) {
+  pdlEnter();
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
-  const bool ok = k < m;
-  const uint32_t cell = ok ? rcell[k] : 0xffffffffu;
+  uint32_t cell = k < m ? rcell[k] : 0xffffffffu;
+  const bool ok = cell < WH;  // keys >= WH: not in the map (group frames gather them too)
+  if (!ok) cell = 0xffffffffu;
   const unsigned peers = __match_any_sync(0xffffffffu, cell);
   if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
   countTileDigit(tc0, pitch, cell & dmask, k / kTile, ok);
@@ -1381,17 +1388,149 @@ struct CellArgs {
   int time_var;
   double growth, sigma_max2;
   int geo_trav;  // geometric traversability (off when the conv-net writes the layer)
+  // Zero the normals (and the geometric traversability) of invalid cells, as the
+  // reference rebuilds both layers every scan (analysis.cpp:44-48,93). They are
+  // zero already unless a snapshot was loaded or a conv-net frame wrote the
+  // traversability of every cell, so this runs only after those.
+  int scrub;
 };
 
 constexpr int kTileX = 32, kTileY = 8;
+constexpr std::size_t kCellsMaxSmem = 200 * 1024;
 
-// Overlap clearance (analysis.cpp:296-317), normals (analysis.cpp:41-86),
-// geometric traversability (analysis.cpp:88-132) and time variance
-// (grid.cpp:113-124, integration.cpp:252-257) in one pass over a shared
-// memory tile with a (radius)-cell halo. Overlap is evaluated for halo cells
-// too, so every thread sees the post-clearance validity of its window.
-// RT: the traversability window radius when known at compile time (the 5x5
-// default and 3x3 are instantiated; 0 = from CellArgs).
+// Post-overlap validity and elevation of cell (rr, cc): overlap clearance
+// (analysis.cpp:296-317) evaluated by every reader, so the result does not
+// depend on whether the cell's own thread has invalidated it yet.
+__device__ __forceinline__ uint8_t stageCell(const Layers& L, const CellArgs& a, int rr, int cc,
+                                             double& e) {
+  e = 0.0;
+  if (rr < 0 || rr >= a.g.H || cc < 0 || cc >= a.g.W) return 0;
+  const size_t j = static_cast<size_t>(rr) * a.g.W + cc;
+  uint8_t v = L.valid[j];
+  if (v) {
+    e = L.elev[j];
+    if (a.overlap) {
+      const double cx = a.g.ox + (cc + 0.5) * a.g.res;
+      const double cy = a.g.oy + (rr + 0.5) * a.g.res;
+      const double ddx = cx - a.rx, ddy = cy - a.ry;
+      if (!(ddx * ddx + ddy * ddy > a.ov_r2) && !(fabs(e - a.rz) <= a.ov_thr)) v = 0;
+    }
+  }
+  return v;
+}
+
+// Window access for the cell body: a shared-memory tile with a halo, or (for
+// windows whose tile exceeds shared memory) the map itself.
+struct TileWin {
+  const double* se;
+  const uint8_t* sv;
+  int tw, lr, lc;
+  __device__ __forceinline__ bool ok(int dr, int dc) const { return sv[(lr + dr) * tw + lc + dc] != 0; }
+  __device__ __forceinline__ double e(int dr, int dc) const { return se[(lr + dr) * tw + lc + dc]; }
+};
+struct GlobalWin {
+  const Layers* L;
+  const CellArgs* a;
+  int r, c;
+  __device__ __forceinline__ bool ok(int dr, int dc) const {
+    double e;
+    return stageCell(*L, *a, r + dr, c + dc, e) != 0;
+  }
+  __device__ __forceinline__ double e(int dr, int dc) const {
+    double v;
+    stageCell(*L, *a, r + dr, c + dc, v);
+    return v;
+  }
+};
+
+// One cell: overlap clearance, normals (analysis.cpp:41-86), geometric
+// traversability (analysis.cpp:88-132), time variance (grid.cpp:113-124).
+template <int RT, typename Win>
+__device__ __forceinline__ void cellBody(const Layers& L, const CellArgs& a, int r, int c,
+                                         const Win& w, int32_t* __restrict__ count,
+                                         uint32_t* __restrict__ seg_start,
+                                         unsigned long long& cleared) {
+  const int W = a.g.W, H = a.g.H;
+  const size_t i = static_cast<size_t>(r) * W + c;
+  const int32_t cnt_i = count[i];
+  if (cnt_i != 0) {  // last reader this scan: ready for the next one (the sort's
+    count[i] = 0;     // atomicMin segment starts need 0xffffffff)
+    seg_start[i] = 0xffffffffu;
+  }
+  const bool was_valid = L.valid[i] != 0;
+  const bool ok = w.ok(0, 0);
+  if (was_valid && !ok) {
+    invalidateCell(L, i);
+    cleared = 1;
+  } else if (ok) {
+    const double res = a.g.res;
+    const double center = w.e(0, 0);
+    const bool hl = c > 0 && w.ok(0, -1), hr = c < W - 1 && w.ok(0, 1);
+    const bool hd = r > 0 && w.ok(-1, 0), hu = r < H - 1 && w.ok(1, 0);
+    double nx = 0.0, ny = 0.0, nz = 0.0;
+    bool has = true;
+    double dhdx = 0.0, dhdy = 0.0;
+    if (hl && hr) dhdx = (w.e(0, 1) - w.e(0, -1)) / (2.0 * res);
+    else if (hr) dhdx = (w.e(0, 1) - center) / res;
+    else if (hl) dhdx = (center - w.e(0, -1)) / res;
+    else has = false;
+    if (has) {
+      if (hd && hu) dhdy = (w.e(1, 0) - w.e(-1, 0)) / (2.0 * res);
+      else if (hu) dhdy = (w.e(1, 0) - center) / res;
+      else if (hd) dhdy = (center - w.e(-1, 0)) / res;
+      else has = false;
+    }
+    if (has) {
+      const double norm = sqrt((dhdx * dhdx + dhdy * dhdy) + 1.0);
+      nx = -dhdx / norm;
+      ny = -dhdy / norm;
+      nz = 1.0 / norm;
+    }
+    L.nx[i] = nx;
+    L.ny[i] = ny;
+    L.nz[i] = nz;
+    double trav = 0.0;
+    if (a.geo_trav && (nx != 0.0 || ny != 0.0 || nz != 0.0)) {
+      const double slope = acos(sclamp(nz, -1.0, 1.0));
+      const double s_slope = sclamp(1.0 - slope / a.slope_max, 0.0, 1.0);
+      double max_step = 0.0, sum = 0.0, sum_sq = 0.0;
+      int cntw = 0;
+      // Row-major window over valid cells (cells outside the grid read as
+      // invalid, so they are skipped like the reference's bounds test).
+      const int R = RT > 0 ? RT : a.radius;
+#pragma unroll
+      for (int dr = -R; dr <= R; ++dr) {
+#pragma unroll
+        for (int dc = -R; dc <= R; ++dc) {
+          if (!w.ok(dr, dc)) continue;
+          const double v = w.e(dr, dc);
+          max_step = smax(max_step, fabs(v - center));
+          sum += v;
+          sum_sq += v * v;
+          ++cntw;
+        }
+      }
+      const double s_step = sclamp(1.0 - max_step / a.step_max, 0.0, 1.0);
+      const double mean = sum / cntw;
+      const double var = smax(0.0, sum_sq / cntw - mean * mean);
+      const double s_rough = sclamp(1.0 - sqrt(var) / a.rough_max, 0.0, 1.0);
+      trav = a.w_slope * s_slope + a.w_step * s_step + a.w_rough * s_rough;
+    }
+    if (a.geo_trav) L.trav[i] = trav;
+    if (a.time_var && cnt_i == 0) L.var[i] = smin(L.var[i] + a.growth, a.sigma_max2);
+  } else if (a.scrub) {
+    L.nx[i] = 0.0;
+    L.ny[i] = 0.0;
+    L.nz[i] = 0.0;
+    if (a.geo_trav) L.trav[i] = 0.0;
+  }
+}
+
+// Overlap clearance, normals, geometric traversability and time variance in
+// one pass over a shared memory tile with a (radius)-cell halo. Overlap is
+// evaluated for halo cells too, so every thread sees the post-clearance
+// validity of its window. RT: the traversability window radius when known at
+// compile time (the 5x5 default and 3x3 are instantiated; 0 = from CellArgs).
 template <int RT>
 __global__ void __launch_bounds__(kTileX* kTileY)
     k_cells(Layers L, int32_t* __restrict__ count, uint32_t* __restrict__ seg_start, CellArgs a,
@@ -1406,102 +1545,31 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   const int c0 = blockIdx.x * kTileX - halo, r0 = blockIdx.y * kTileY - halo;
   const int tid = threadIdx.y * kTileX + threadIdx.x;
   for (int q = tid; q < tw * th; q += kTileX * kTileY) {
-    const int rr = r0 + q / tw, cc = c0 + q % tw;
-    uint8_t v = 0;
-    double e = 0.0;
-    if (rr >= 0 && rr < H && cc >= 0 && cc < W) {
-      const size_t j = static_cast<size_t>(rr) * W + cc;
-      v = L.valid[j];
-      if (v) {
-        e = L.elev[j];
-        if (a.overlap) {
-          const double cx = a.g.ox + (cc + 0.5) * a.g.res;
-          const double cy = a.g.oy + (rr + 0.5) * a.g.res;
-          const double ddx = cx - a.rx, ddy = cy - a.ry;
-          if (!(ddx * ddx + ddy * ddy > a.ov_r2) && !(fabs(e - a.rz) <= a.ov_thr)) v = 0;
-        }
-      }
-    }
-    sv[q] = v;
+    double e;
+    sv[q] = stageCell(L, a, r0 + q / tw, c0 + q % tw, e);
     se[q] = e;
   }
   __syncthreads();
   const int r = blockIdx.y * kTileY + threadIdx.y, c = blockIdx.x * kTileX + threadIdx.x;
   unsigned long long cleared = 0;
-  if (r < H && c < W) {
-    const size_t i = static_cast<size_t>(r) * W + c;
-    const int32_t cnt_i = count[i];
-    if (cnt_i != 0) {  // last reader this scan: ready for the next one (the sort's
-      count[i] = 0;     // atomicMin segment starts need 0xffffffff)
-      seg_start[i] = 0xffffffffu;
-    }
-    const int lr = threadIdx.y + halo, lc = threadIdx.x + halo;
-    const bool was_valid = L.valid[i] != 0;
-    const bool ok = sv[lr * tw + lc] != 0;
-    if (was_valid && !ok) {
-      invalidateCell(L, i);
-      cleared = 1;
-    } else if (ok) {
-      const double res = a.g.res;
-      const double center = se[lr * tw + lc];
-      const bool hl = c > 0 && sv[lr * tw + lc - 1], hr = c < W - 1 && sv[lr * tw + lc + 1];
-      const bool hd = r > 0 && sv[(lr - 1) * tw + lc], hu = r < H - 1 && sv[(lr + 1) * tw + lc];
-      double nx = 0.0, ny = 0.0, nz = 0.0;
-      bool has = true;
-      double dhdx = 0.0, dhdy = 0.0;
-      if (hl && hr) dhdx = (se[lr * tw + lc + 1] - se[lr * tw + lc - 1]) / (2.0 * res);
-      else if (hr) dhdx = (se[lr * tw + lc + 1] - center) / res;
-      else if (hl) dhdx = (center - se[lr * tw + lc - 1]) / res;
-      else has = false;
-      if (has) {
-        if (hd && hu) dhdy = (se[(lr + 1) * tw + lc] - se[(lr - 1) * tw + lc]) / (2.0 * res);
-        else if (hu) dhdy = (se[(lr + 1) * tw + lc] - center) / res;
-        else if (hd) dhdy = (center - se[(lr - 1) * tw + lc]) / res;
-        else has = false;
-      }
-      if (has) {
-        const double norm = sqrt((dhdx * dhdx + dhdy * dhdy) + 1.0);
-        nx = -dhdx / norm;
-        ny = -dhdy / norm;
-        nz = 1.0 / norm;
-      }
-      L.nx[i] = nx;
-      L.ny[i] = ny;
-      L.nz[i] = nz;
-      double trav = 0.0;
-      if (a.geo_trav && (nx != 0.0 || ny != 0.0 || nz != 0.0)) {
-        const double slope = acos(sclamp(nz, -1.0, 1.0));
-        const double s_slope = sclamp(1.0 - slope / a.slope_max, 0.0, 1.0);
-        double max_step = 0.0, sum = 0.0, sum_sq = 0.0;
-        int cntw = 0;
-        // Row-major window over valid cells (cells outside the grid are staged
-        // as invalid, so they are skipped like the reference's bounds test).
-        const int R = RT > 0 ? RT : a.radius;
-#pragma unroll
-        for (int dr = -R; dr <= R; ++dr) {
-#pragma unroll
-          for (int dc = -R; dc <= R; ++dc) {
-            const int q = (lr + dr) * tw + (lc + dc);
-            if (!sv[q]) continue;
-            const double v = se[q];
-            max_step = smax(max_step, fabs(v - center));
-            sum += v;
-            sum_sq += v * v;
-            ++cntw;
-          }
-        }
-        const double s_step = sclamp(1.0 - max_step / a.step_max, 0.0, 1.0);
-        const double mean = sum / cntw;
-        const double var = smax(0.0, sum_sq / cntw - mean * mean);
-        const double s_rough = sclamp(1.0 - sqrt(var) / a.rough_max, 0.0, 1.0);
-        trav = a.w_slope * s_slope + a.w_step * s_step + a.w_rough * s_rough;
-      }
-      if (a.geo_trav) L.trav[i] = trav;
-      if (a.time_var && cnt_i == 0) L.var[i] = smin(L.var[i] + a.growth, a.sigma_max2);
-    }
-  }
+  if (r < H && c < W)
+    cellBody<RT>(L, a, r, c, TileWin{se, sv, tw, static_cast<int>(threadIdx.y) + halo, static_cast<int>(threadIdx.x) + halo}, count,
+                 seg_start, cleared);
   cleared = warpSum(cleared);
-  if (((threadIdx.y * kTileX + threadIdx.x) & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
+  if ((tid & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
+}
+
+// Same cell phases without the tile, for traversability windows too large to
+// stage in shared memory (the reference accepts any odd window).
+__global__ void __launch_bounds__(256)
+    k_cells_global(Layers L, int32_t* __restrict__ count, uint32_t* __restrict__ seg_start,
+                   CellArgs a, DevStats* st) {
+  pdlEnter();
+  const int r = blockIdx.y, c = blockIdx.x * 256 + threadIdx.x;
+  unsigned long long cleared = 0;
+  if (c < a.g.W) cellBody<0>(L, a, r, c, GlobalWin{&L, &a, r, c}, count, seg_start, cleared);
+  cleared = warpSum(cleared);
+  if ((threadIdx.x & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
 }
 
 
@@ -1547,6 +1615,9 @@ struct Frame {
   // Per-ray endpoint cell from k_ingest (indexed like the rays), or null when
   // the sort has overwritten it (3 passes) or the rays are a shard's.
   const uint32_t* point_cells = nullptr;
+  // Index of this process's first ray in the point arrays (a group rank's
+  // rays sit at their frame indices; shard and single frames start at 0).
+  uint32_t ray_at = 0;
   int heavy = INT_MAX;
   Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
       : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
@@ -1654,8 +1725,10 @@ SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
 }
 
 // K1 (reference integration.cpp:85-140, sensing.cpp:32-41, drift.cpp:24-42).
+// lo: frame index of the first of the N points (a group rank's batch; its
+// outputs land at frame indices lo .. lo+N-1).
 void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, bool count_cells,
-                 bool chunked = false) {
+                 bool chunked = false, uint32_t lo = 0) {
   if (N == 0) return;
   DeviceMap& m = f.m;
   const UpdateParams& U = f.P.update;
@@ -1678,9 +1751,10 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   const uint32_t chunk = chunked ? chunkPoints(N) : N;
   for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
     if (chunked) checkCuda(cudaStreamWaitEvent(f.s, m.ev_chunk[c], 0), "stream wait");
-    launchPdl(k_ingest, gridFor(std::min(chunk, N - base)), kThreads, 0, f.s, 
-        d_xyz, N, ia, m.cur, m.count, m.px, m.py, m.pz, m.pvar, m.key0, m.kept, m.drift_sum_part,
-        m.drift_n_part, sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0, m.stats, base);
+    launchPdl(k_ingest, gridFor(std::min(chunk, N - base)), kThreads, 0, f.s, d_xyz, lo + N, ia,
+              m.cur, m.count, m.px, m.py, m.pz, m.pvar, m.key0, m.kept, m.drift_sum_part,
+              m.drift_n_part, sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0, m.stats,
+              lo + base, lo);
     ++f.launches;
   }
 }
@@ -1776,9 +1850,9 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
                                                         f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
     ++f.launches;
     if (N > 0) {
-      launchPdl(k_rays_pass1<false>, gridFor(N, kP1Threads), kP1Threads, 0, s, N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 0, ray_base, m.probe,
-                                                   f.point_cells);
+      launchPdl(k_rays_pass1<false>, gridFor(N, kP1Threads), kP1Threads, 0, s, N, m.kept + f.ray_at,
+                m.px + f.ray_at, m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar,
+                m.raylist, m.stats, 0, ray_base, m.probe, f.point_cells);
       ++f.launches;
     }
   }
@@ -1791,9 +1865,9 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
     ++f.launches;
     if (N > 0) {
       launchPdl(k_rays_pass1<true>, std::min(gridFor(N, kP1Threads), 148u * RB_PASS1_MIN_BLOCKS),
-                     kP1Threads, 0, s, N, m.kept, m.px, m.py, m.pz, ra, m.cur, m.cls,
-                                                   m.kstar, m.raylist, m.stats, 1, ray_base, m.probe,
-                                                   f.point_cells);
+                kP1Threads, 0, s, N, m.kept + f.ray_at, m.px + f.ray_at, m.py + f.ray_at,
+                m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar, m.raylist, m.stats, 1, ray_base,
+                m.probe, f.point_cells);
       ++f.launches;
     }
   }
@@ -1808,8 +1882,8 @@ void phaseRemovePass2(Frame& f, uint32_t ray_base) {
   launchPdl(k_remove, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.kstar, m.stats);
   ++f.launches;
   if (ra.bound) {
-    launchPdl(k_rays_pass2, 148 * 8, kThreads, 0, f.s, m.raylist, m.stats, m.px, m.py, m.pz, ra, m.cur,
-                                                m.cls, m.kstar, ray_base);
+    launchPdl(k_rays_pass2, 148 * 8, kThreads, 0, f.s, m.raylist, m.stats, m.px + f.ray_at,
+              m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar, ray_base);
     ++f.launches;
   }
 }
@@ -1838,16 +1912,25 @@ void phaseCells(Frame& f) {
   ca.time_var = (f.dt != 0.0 && U.sigma_t2 != 0.0) ? 1 : 0;
   ca.growth = U.sigma_t2 * (f.dt / U.nominal_update_period);
   ca.sigma_max2 = U.sigma_max2;
+  ca.scrub = m.scrub_invalid ? 1 : 0;
   const int halo = std::max(1, ca.radius);
   const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
-  const dim3 grid((f.g.W + kTileX - 1) / kTileX, (f.g.H + kTileY - 1) / kTileY);
-  auto* kern = ca.radius == 2 ? k_cells<2> : (ca.radius == 1 ? k_cells<1> : k_cells<0>);
-  if (sm > 48 * 1024)
-    checkCuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(sm)),
-              "smem attribute");
-  launchPdl(kern, grid, dim3(kTileX, kTileY), sm, f.s, m.cur, m.count, m.start, ca, m.stats);
+  if (sm > kCellsMaxSmem) {  // window too large for a shared-memory tile
+    launchPdl(k_cells_global, dim3((f.g.W + 255) / 256, f.g.H), 256, 0, f.s, m.cur, m.count,
+              m.start, ca, m.stats);
+  } else {
+    const dim3 grid((f.g.W + kTileX - 1) / kTileX, (f.g.H + kTileY - 1) / kTileY);
+    auto* kern = ca.radius == 2 ? k_cells<2> : (ca.radius == 1 ? k_cells<1> : k_cells<0>);
+    if (sm > 48 * 1024)
+      checkCuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)),
+                "smem attribute");
+    launchPdl(kern, grid, dim3(kTileX, kTileY), sm, f.s, m.cur, m.count, m.start, ca, m.stats);
+  }
   ++f.launches;
+  // invalid cells' normals / traversability are zero again, unless the
+  // conv-net below writes the traversability of every cell
+  m.scrub_invalid = f.P.use_convnet_traversability;
   RB_PHASE_EVENT(7, f.s);  // cell phases done
   // Conv-net traversability (reference integration.cpp:242-244): reads the
   // post-overlap elevation, writes the traversability of every cell.
@@ -2183,7 +2266,7 @@ void shardUpdate(DeviceMap& m, const double* drift_pairs, int n_ranks, const uin
   if (M > 0) {
     const SortGeom sg = phaseSortGeometry(f, M);
     k_records_count<<<gridFor(M), kThreads, 0, f.s>>>(d_cells, M, m.count, sg.tc, sg.pitch,
-                                                      sg.buckets() - 1);
+                                                      sg.buckets() - 1, f.WH);
     ++f.launches;
     phaseSortFuse(f, d_cells, M, d_z, d_var, sg);
   } else {
@@ -2247,6 +2330,173 @@ ScanResult shardFinish(DeviceMap& m, const int64_t counters_total[3], uint64_t p
   m.last_stamp = st.stamp;
   m.has_last = true;
   st.stage = 0;
+  return out;
+}
+
+// ------------------------------------------------------- group frames
+// One frame split across the ranks of a group (exact variant;
+// DESIGN.md §7). Rank r ingests the contiguous batch [lo, lo + n_local) of
+// the frame into the frame-wide point arrays at the same indices; the batch
+// size is a whole number of radix tiles, so after the in-place all-gathers of
+// the cell keys, p_z, sigma_p^2 and the drift block partials every rank holds
+// exactly the arrays a single-GPU frame would have built: the count, sort,
+// gated fusion and drift offset that follow are the single-GPU kernels on the
+// same inputs (bit-identical maps, drift included). The ray passes run over
+// the rank's own rays with their frame-wide ids (the k* rule), and min / max
+// all-reduces of k*, the bounds and their validity merge them.
+GroupGeom groupGeom(uint64_t n_total, int ranks, int rank) {
+  if (ranks <= 0 || rank < 0 || rank >= ranks) fail(Err::kUsage, "bad group rank / size");
+  if (n_total >= 0x7fffffffULL) fail(Err::kUsage, "too many points in one scan");
+  GroupGeom g;
+  g.ranks = ranks;
+  g.rank = rank;
+  g.n_total = n_total;
+  const uint64_t per = (n_total + ranks - 1) / ranks;
+  g.chunk = static_cast<uint32_t>(std::max<uint64_t>((per + kTile - 1) / kTile, 1) * kTile);
+  const uint64_t lo = std::min<uint64_t>(static_cast<uint64_t>(rank) * g.chunk, n_total);
+  g.lo = static_cast<uint32_t>(lo);
+  g.n_local = static_cast<uint32_t>(std::min<uint64_t>(lo + g.chunk, n_total) - lo);
+  return g;
+}
+
+struct GroupFrame {
+  PipelineParams P;
+  GroupGeom geo;
+  SortGeom sg;
+  Frame f;
+  GroupFrame(DeviceMap& m, const PipelineParams& params, const GroupGeom& g, const Pose& pose,
+             double stamp, double dt)
+      : P(params), geo(g), f(m, P, pose, stamp, dt) {}
+};
+
+GroupFrame* groupBegin(DeviceMap& m, const PipelineParams& P, const GroupGeom& g, const Pose& pose,
+                       double stamp, double dt) {
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (m.shard.stage != 0) fail(Err::kUsage, "a sharded frame is in progress on this map");
+  if (m.async_count != 0) fail(Err::kUsage, "streaming frames in flight: call relief_gpu_map_wait");
+  return new GroupFrame(m, P, g, pose, stamp, dt);
+}
+
+void groupEnd(GroupFrame* gf) { delete gf; }
+
+// Recenter, this rank's batch through K1 (no counts: the gathered keys are
+// counted in the update phase). Gathers: keys, p_z, sigma_p^2, drift partials.
+void groupPhaseIngest(GroupFrame& gf, const double* xyz, bool on_device,
+                      std::vector<XBuf>& gathers) {
+  Frame& f = gf.f;
+  DeviceMap& m = f.m;
+  const GroupGeom& g = gf.geo;
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
+  const double* d_xyz = xyz;
+  if (g.n_total > 0) {
+    phaseScratch(f, static_cast<std::size_t>(g.ranks) * g.chunk);
+    if (g.n_local > 0 && !on_device) {
+      checkCuda(cudaMemcpyAsync(m.xyz_in, xyz, g.n_local * 3 * sizeof(double),
+                                cudaMemcpyHostToDevice, f.s),
+                "point upload");
+      d_xyz = m.xyz_in;
+    } else if (g.n_local > 0) {
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, xyz) == cudaSuccess && pa.type == cudaMemoryTypeDevice &&
+          pa.device != m.device) {  // a frame resident on another device of the process
+        checkCuda(cudaMemcpyPeerAsync(m.xyz_in, m.device, xyz, pa.device,
+                                      g.n_local * 3 * sizeof(double), f.s),
+                  "point copy");
+        d_xyz = m.xyz_in;
+      }
+      cudaGetLastError();
+    }
+  }
+  checkCuda(cudaEventRecord(m.ev[13], f.s), "event");  // input resident
+  phaseBegin(f, false);
+  if (g.n_total == 0) return;
+  gf.sg = phaseSortGeometry(f, static_cast<uint32_t>(g.n_total));
+  RB_PHASE_EVENT(1, f.s);
+  phaseIngest(f, d_xyz, g.n_local, gf.sg, false, false, g.lo);
+  RB_PHASE_EVENT(2, f.s);
+  gathers.push_back({m.key0, g.chunk, XType::kU32, XOp::kSum});
+  gathers.push_back({m.pz, g.chunk, XType::kF64, XOp::kSum});
+  gathers.push_back({m.pvar, g.chunk, XType::kF64, XOp::kSum});
+  if (gf.P.drift.enabled) {
+    gathers.push_back({m.drift_sum_part, g.chunk / kThreads, XType::kF64, XOp::kSum});
+    gathers.push_back({m.drift_n_part, g.chunk / kThreads, XType::kI32, XOp::kSum});
+  }
+}
+
+// Drift offset, counts + sort + gated fusion of the whole frame (every rank,
+// identical), ray pass 1 over this rank's rays. Reduces: k*, bounds.
+void groupPhaseUpdate(GroupFrame& gf, std::vector<XBuf>& reduces) {
+  Frame& f = gf.f;
+  DeviceMap& m = f.m;
+  const GroupGeom& g = gf.geo;
+  const PipelineParams& P = gf.P;
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  const uint32_t N = static_cast<uint32_t>(g.n_total);
+  if (N == 0) return;
+  if (P.drift.enabled) {
+    launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part,
+              static_cast<int>(gridFor(N)), P.drift.min_points, P.drift.max_offset_per_scan,
+              m.drift_offset, m.stats);
+    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
+    f.launches += 2;
+  }
+  RB_PHASE_EVENT(3, f.s);
+  launchPdl(k_records_count, gridFor(N), kThreads, 0, f.s, m.key0, N, m.count, gf.sg.tc,
+            gf.sg.pitch, gf.sg.buckets() - 1, f.WH);
+  ++f.launches;
+  phaseSortFuse(f, m.key0, N, m.pz, m.pvar, gf.sg);
+  f.point_cells = gf.sg.passes <= 2 ? m.key0 + g.lo : nullptr;
+  f.ray_at = g.lo;
+  phaseRaysPass1(f, g.n_local, g.lo);
+  if (P.cleanup.cleanup_enabled) reduces.push_back({m.kstar, f.ncell, XType::kI32, XOp::kMin});
+  if (P.cleanup.upper_bound_enabled) {
+    reduces.push_back({m.cur.ub, f.ncell, XType::kF64, XOp::kMin});
+    reduces.push_back({m.cur.ubv, f.ncell, XType::kU8, XOp::kMax});
+  }
+}
+
+// Removal (identical on every rank: k* is merged) and ray pass 2 over this
+// rank's queued rays. Reduces: bounds of the removed cells.
+void groupPhaseRemove(GroupFrame& gf, std::vector<XBuf>& reduces) {
+  Frame& f = gf.f;
+  DeviceMap& m = f.m;
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (gf.geo.n_total == 0) return;
+  phaseRemovePass2(f, gf.geo.lo);
+  if (gf.P.cleanup.cleanup_enabled && gf.P.cleanup.upper_bound_enabled) {
+    reduces.push_back({m.cur.ub, f.ncell, XType::kF64, XOp::kMin});
+    reduces.push_back({m.cur.ubv, f.ncell, XType::kU8, XOp::kMax});
+  }
+  RB_PHASE_EVENT(6, f.s);
+}
+
+// Cell phases (identical on every rank). Reduces: the batch fate counters.
+void groupPhaseCells(GroupFrame& gf, std::vector<XBuf>& reduces) {
+  Frame& f = gf.f;
+  DeviceMap& m = f.m;
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  if (gf.geo.n_total == 0)
+    for (int k = 1; k <= 6; ++k) RB_PHASE_EVENT(k, f.s);
+  phaseCells(f);
+  // out_of_range, excluded, out_of_map: the first three DevStats counters
+  static_assert(offsetof(DevStats, excluded) == 8 && offsetof(DevStats, out_of_map) == 16,
+                "fate counters must be contiguous");
+  reduces.push_back({&m.stats->out_of_range, 3, XType::kU64, XOp::kSum});
+}
+
+ScanResult groupFinish(GroupFrame& gf) {
+  Frame& f = gf.f;
+  DeviceMap& m = f.m;
+  checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
+  checkCuda(cudaEventRecord(m.ev[12], f.s), "event");  // device end incl. the exchanges
+  const DevStats& d = phaseStats(f);
+  ScanResult out = resultFrom(d, gf.geo.n_total);
+  m.timing_pending = true;
+  m.timing_chunked = false;
+  m.timing_phases = m.phase_events;
+  m.last_launches = f.launches;
+  m.last_visits = static_cast<long long>(d.visits);
   return out;
 }
 

@@ -4,7 +4,12 @@ Two modes:
 
 * replicas -- every rank owns an independent map and frame stream on its own device; collectives
   only carry the barrier and the max-over-ranks reduction of device timings (bench.py).
-* exact point-batch sharding of ONE frame -- every rank keeps a full map
+* exact point-batch sharding of ONE frame through the library's group API (relief_gpu_group_*,
+  `create_nccl_group`): the frame's exchanges (all-gathers of the records, min / max all-reduces
+  of k* and the bounds) run inside the library over NCCL on the map's own stream; Python only
+  broadcasts the 128-byte NCCL id once. This is the production path (bench.py --gpus N).
+* the same split with host-driven exchanges (relief_gpu_shard_*), for embedders with their own
+  transport -- every rank keeps a full map
   replica and takes the contiguous batch [g*N/G, (g+1)*N/G) of the frame (`shard_bounds`), so the
   global point index stays the ray id used for k*. `integrate_sharded` drives the library's
   relief_gpu_shard_* phases and the exchanges between them: all-gather of the drift votes and of
@@ -92,6 +97,13 @@ class CudaShardAPI:
         from . import _check
         _check(self.lib, st)
 
+    def _after_caller(self):
+        """The library works on its own stream: order it after the caller's pending torch work
+        (the exchanged records / k* / bounds written by NCCL or torch ops on that stream)."""
+        import torch
+        self._check(self.lib.relief_gpu_map_after_stream(
+            self.map.handle, self._ct.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
     def ingest(self, xyz, ray_offset: int, n_total: int, pose, stamp: float) -> dict:
         import numpy as np
         ct = self._ct
@@ -114,6 +126,7 @@ class CudaShardAPI:
         ct = self._ct
         pairs = np.ascontiguousarray(drift_pairs, dtype=np.float64).reshape(-1)
         m = int(cells.numel())
+        self._after_caller()
         self._check(self.lib.relief_gpu_shard_update(
             self.map.handle, pairs.ctypes.data_as(ct.POINTER(ct.c_double)), pairs.size // 2,
             cells.data_ptr() if m else None, z.data_ptr() if m else None, var.data_ptr() if m else None,
@@ -132,6 +145,7 @@ class CudaShardAPI:
     def remove(self):
         ct = self._ct
         removed = ct.c_int64(0)
+        self._after_caller()
         self._check(self.lib.relief_gpu_shard_remove(self.map.handle, ct.byref(removed), ct.byref(self.io)))
         return int(removed.value), self._bounds(with_kstar=False)
 
@@ -141,6 +155,7 @@ class CudaShardAPI:
         ct = self._ct
         c = np.ascontiguousarray(counters, dtype=np.int64)
         st = ScanStats()
+        self._after_caller()
         self._check(self.lib.relief_gpu_shard_finish(self.map.handle, c.ctypes.data_as(ct.POINTER(ct.c_int64)),
                                                      n_total, ct.byref(st)))
         return st
@@ -194,6 +209,29 @@ class DistExchange:
 
     def reduce_max(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
+
+def create_nccl_group(lib, rmap, dist=None, group=None):
+    """relief_gpu_group over NCCL for this process's map: rank 0 makes the 128-byte NCCL id, the
+    torch.distributed process group broadcasts it, every rank creates its end collectively. The
+    frame's exchanges then run inside the library on the map's stream (no torch ops per frame)."""
+    from . import Group
+    uid, ranks, rank = broadcast_unique_id(lib, dist, group)
+    return Group.nccl(lib, rmap, uid, ranks, rank)
+
+
+def broadcast_unique_id(lib, dist=None, group=None):
+    """(id, ranks, rank): rank 0's relief_gpu_group_unique_id, broadcast over torch.distributed."""
+    import numpy as np
+    import torch
+    from . import group_unique_id
+    if dist is None or not dist.is_initialized():
+        return group_unique_id(lib), 1, 0
+    ranks, rank = dist.get_world_size(group), dist.get_rank(group)
+    uid = group_unique_id(lib) if rank == 0 else bytes(128)
+    t = torch.tensor(np.frombuffer(uid, dtype=np.uint8).copy(), device=_device_for(dist))
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(t.cpu().numpy().tobytes()), ranks, rank
 
 
 def integrate_sharded(api, ex, xyz_local, ray_offset: int, n_total: int, pose, stamp: float):

@@ -170,3 +170,51 @@ def test_gloo_world2_sharded_frame_exchanges():
         counters, n_total, ub_f, ubv_f = seen["finish"]
         assert np.array_equal(counters, np.sum([d["counters"] for d in data], axis=0)) and n_total == N
         assert np.array_equal(ub_f, ub2) and np.array_equal(ubv_f, ubv2)             # 2nd exchange
+
+
+# ----------------------------------------------------------------- group API (host side)
+def test_group_bounds_whole_tiles_in_scan_order(product):
+    """relief_gpu_group_bounds: contiguous batches in rank order, every batch but the tail a whole
+    number of 2048-point radix tiles (so the gathered arrays equal the single-GPU ones)."""
+    import paper_2204_12876_b200 as pk
+    for n in (0, 1, 2047, 2048, 2049, 19_477, 262_144, 1_000_064):
+        for G in (1, 2, 3, 4, 5, 8):
+            spans = [pk.group_bounds(product, n, G, r) for r in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            for lo, hi in spans:
+                assert lo % 2048 == 0 or lo == hi == n  # trailing ranks of a short frame are empty
+                assert hi == n or (hi - lo) % 2048 == 0
+    with pytest.raises(pk.ReliefError):
+        pk.group_bounds(product, 10, 2, 2)
+
+
+def _id_worker(rank, world, port, q, lib_path):
+    import torch.distributed as dist
+    import paper_2204_12876_b200 as pk
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lib = pk.load_library(lib_path, gpu_api=True)
+        uid, ranks, r = mg.broadcast_unique_id(lib, dist)
+        q.put((rank, ranks, r, uid))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_nccl_id_broadcast(product):
+    """create_nccl_group's id exchange: every rank receives rank 0's 128-byte NCCL id."""
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q, product._relief_path)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, n0, g0, u0), (r1, n1, g1, u1) = out
+    assert (n0, n1, g0, g1) == (2, 2, 0, 1)
+    assert len(u0) == 128 and u0 == u1 and any(u0)

@@ -300,3 +300,61 @@ def test_frame_sizes_changing_between_scans(gpu, reference, tmp_path):
         z = -1.0 + 0.05 * rng.standard_normal(n)
         pair.integrate(np.column_stack([xy, z]), pose, 0.1 * scan, context=f"n={n}")
         pair.compare(context=f"n={n}")
+
+
+def _raw_sections(path):
+    """Snapshot sections as float arrays (raw layers: the snapshot stores unmasked values)."""
+    secs = _sections(path.read_text())
+    return {k: np.array([[float(v) for v in row.split()] for row in rows if row.strip()])
+            for k, rows in secs.items() if k != "header"}
+
+
+def test_invalid_cells_normals_traversability_rebuilt(gpu, reference, tmp_path):
+    """The reference rebuilds the normal and traversability layers every scan, with 0 for
+    invalid cells (analysis.cpp:44-48,93). A loaded snapshot whose invalid cells carry non-zero
+    normals / traversability must come out of the next scan with those zeroed, like the
+    reference's (raw layers compared through save, not the NaN-masked export)."""
+    import snapshots as snap
+    res, W, H = 0.05, 48, 40
+    rng = np.random.default_rng(5)
+    layers = snap.fresh(H, W)
+    for r in range(H):
+        for c in range(W):
+            if (r + c) % 3:
+                snap.set_cell(layers, r, c, 0.01 * rng.standard_normal(), 0.01, 0.0, (0.0, 0.0, 1.0), 0.8)
+            else:  # invalid cell with stale normals / traversability
+                layers["normal_x"][r, c], layers["normal_z"][r, c] = 0.3, 0.9
+                layers["traversability"][r, c] = 0.7
+    p = tmp_path / "r.config"
+    p.write_text("drift.enabled = false\nupdate.sigma_t2 = 0\n")
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    xyz = np.column_stack([rng.uniform(-1.0, 1.0, 3000), rng.uniform(-0.9, 0.9, 3000),
+                           -1.0 + 0.01 * rng.standard_normal(3000)])
+    saved = []
+    for i, lib in enumerate((gpu, reference)):
+        f = tmp_path / f"m{i}.relief"
+        f.write_text(snap.text(layers, res))
+        m = pk.ReliefMap.load(lib, f)
+        cfg = pk.Config.load(lib, p)
+        m.integrate(xyz, pose, 1.0, cfg)
+        m.save(tmp_path / f"o{i}.relief")
+        saved.append(_raw_sections(tmp_path / f"o{i}.relief"))
+    a, b = saved
+    for name in ("normal_x", "normal_y", "normal_z", "valid", "elevation", "variance"):
+        assert np.array_equal(a[name], b[name], equal_nan=True), name
+    assert np.nanmax(np.abs(a["traversability"] - b["traversability"])) <= 1e-12
+    assert (a["traversability"][a["valid"] == 0] == 0).all()
+
+
+def test_traversability_window_larger_than_shared_memory(gpu, reference, tmp_path):
+    """A window whose shared-memory tile would exceed the SM's capacity runs the global-memory
+    variant of the cell pass (the reference accepts any odd window)."""
+    pair = Pair(gpu, reference, tmp_path, "drift.enabled = false\ntraversability.window = 151\n",
+                0.04, 180, 170)
+    rng = np.random.default_rng(9)
+    pose = wl.pose34(np.eye(3), (0.0, 0.0, 1.0))
+    for scan in range(2):
+        xy = rng.uniform(-3.4, 3.4, (40000, 2))
+        z = -1.0 + 0.05 * np.sin(xy[:, 0]) + 0.01 * rng.standard_normal(40000)
+        pair.integrate(np.column_stack([xy, z]), pose, 0.1 * scan, context=f"scan {scan}")
+        pair.compare(context=f"window 151 scan {scan}")
