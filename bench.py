@@ -363,13 +363,18 @@ def single_gpu_legs(lib, D, name, steps, warmup, local_rank, want_roofline=True,
     d_ok = torch.empty(cells, dtype=torch.uint8, device=D.dev)
 
     def run_device(m, s):
-        dev = 0.0
+        """(device seconds, host wall seconds of the library calls) of one step."""
+        dev = wall = 0.0
         for t, c in dev_frames[s % nf]:
+            t0 = time.perf_counter()
             m.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
+            wall += time.perf_counter() - t0
             dev += m.kernel_seconds()[7]  # device time, events at the frame ends only
         if chain:
+            t0 = time.perf_counter()
             dev += m.smooth_chain_device("elevation", wl.C5_CHAIN, d_vals.data_ptr(), d_ok.data_ptr())
-        return dev
+            wall += time.perf_counter() - t0
+        return dev, wall
 
     # value: device-resident input
     m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
@@ -381,9 +386,9 @@ def single_gpu_legs(lib, D, name, steps, warmup, local_rank, want_roofline=True,
     with cm:
         for s in range(warmup, warmup + steps):
             D.flush_l2()
-            t0 = time.perf_counter()
-            dev_t.append(run_device(m, s))
-            wall_t.append(time.perf_counter() - t0)
+            dv, wv = run_device(m, s)
+            dev_t.append(dv)
+            wall_t.append(wv)
             launches += m.last_launches() * calls
     D.barrier()
     dev_total = D.max(sum(dev_t))
@@ -391,6 +396,7 @@ def single_gpu_legs(lib, D, name, steps, warmup, local_rank, want_roofline=True,
            "wall_ms_per_frame": statistics.mean(wall_t) * 1e3,
            "host_overhead_us_per_call": (statistics.mean(wall_t) - statistics.mean(dev_t)) / calls * 1e6,
            "points_per_frame": pts, "calls_per_frame": calls, "gpu_launches": int(launches),
+           "graphs": {"instantiated": m.graph_stats()[0], "updated": m.graph_stats()[1]},
            "frame_device_ms": [round(x * 1e3, 4) for x in dev_t]}
     if chain:
         out["ms_per_frame_incl_post"] = out["ms_per_frame"]

@@ -58,6 +58,16 @@ RELIEF_API relief_status relief_gpu_map_kernel_seconds(const relief_map* map, do
  * also ends their programmatic (overlapped) launch. The runners turn it on. */
 RELIEF_API relief_status relief_gpu_map_set_phase_timing(relief_map* map, int on);
 
+/* CUDA graphs for synchronous frames (default off): each relief_map_integrate /
+ * relief_gpu_map_integrate_device call captures its launches and replays them
+ * as one graph launch, updating a cached executable graph in place. Off: the
+ * same launches are issued one by one, chained by programmatic dependent
+ * launch, which measured as fast on the device and cheaper on the host
+ * (DESIGN.md §5.0b). Results are identical either way. graph_stats: out[0]
+ * graphs instantiated, out[1] frames that updated a cached graph. */
+RELIEF_API relief_status relief_gpu_map_set_graphs(relief_map* map, int on);
+RELIEF_API relief_status relief_gpu_map_graph_stats(const relief_map* map, int64_t out[2]);
+
 /* Kernel launches issued by the last integrate call (evidence for bench.py). */
 RELIEF_API int64_t relief_gpu_map_last_launches(const relief_map* map);
 

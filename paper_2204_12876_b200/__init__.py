@@ -147,6 +147,8 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_sim_render": (ctypes.c_int64, [_CS, _DP, _D, ctypes.c_uint64, ctypes.c_uint64, _DP,
                                                ctypes.c_int64]),
     "relief_gpu_map_after_stream": (_I, [_P, ctypes.c_void_p]),
+    "relief_gpu_map_set_graphs": (_I, [_P, _I]),
+    "relief_gpu_map_graph_stats": (_I, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "relief_gpu_group_unique_id": (_I, [ctypes.c_void_p]),
     "relief_gpu_group_create": (_P, [_P, ctypes.c_void_p, _I, _I]),
     "relief_gpu_group_create_local": (_P, [ctypes.POINTER(_P), _I]),
@@ -386,6 +388,16 @@ class ReliefMap:
             self.handle, layer.encode(), kinds, radii, sig, len(steps), ctypes.c_void_p(d_values),
             ctypes.c_void_p(d_valid)))
         return float(self.lib.relief_gpu_map_chain_seconds(self.handle))
+
+    def set_graphs(self, on: bool) -> None:
+        """relief_gpu_map_set_graphs: one CUDA graph per synchronous frame (default) or direct launches."""
+        _check(self.lib, self.lib.relief_gpu_map_set_graphs(self.handle, 1 if on else 0))
+
+    def graph_stats(self):
+        """(graphs instantiated, frames that updated a cached graph)."""
+        out = (ctypes.c_int64 * 2)()
+        _check(self.lib, self.lib.relief_gpu_map_graph_stats(self.handle, out))
+        return int(out[0]), int(out[1])
 
     def after_stream(self, stream_handle: int) -> None:
         """relief_gpu_map_after_stream: order the map's next device work after everything

@@ -546,6 +546,19 @@ relief_status relief_gpu_shard_finish(relief_map* map, const int64_t counters_to
   });
 }
 
+relief_status relief_gpu_map_set_graphs(relief_map* map, int on) {
+  if (map == nullptr) return usage("null argument");
+  map->dev->use_graphs = on != 0;
+  return RELIEF_OK;
+}
+
+relief_status relief_gpu_map_graph_stats(const relief_map* map, int64_t out[2]) {
+  if (map == nullptr || out == nullptr) return usage("null argument");
+  out[0] = map->dev->graph_instantiations;
+  out[1] = map->dev->graph_updates;
+  return RELIEF_OK;
+}
+
 relief_status relief_gpu_map_after_stream(relief_map* map, void* cuda_stream) {
   if (map == nullptr) return usage("null argument");
   return guard([&] {

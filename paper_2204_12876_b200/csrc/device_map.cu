@@ -126,6 +126,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_after, cudaEventDisableTiming), "event create");
+    checkCuda(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "event create");
     checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev_chunk)
       checkCuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
@@ -196,6 +197,8 @@ void destroyDeviceMap(DeviceMap* m) {
   for (auto& e : m->ev)
     if (e) cudaEventDestroy(e);
   if (m->ev_after) cudaEventDestroy(m->ev_after);
+  if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+  for (int k = 0; k < m->graph_count; ++k) cudaGraphExecDestroy(m->graphs[k]);
   for (auto& e : m->ev_chunk)
     if (e) cudaEventDestroy(e);
   if (m->stream) cudaStreamDestroy(m->stream);

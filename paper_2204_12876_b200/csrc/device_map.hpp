@@ -182,6 +182,16 @@ struct DeviceMap {
   int last_chain_launches = 0;
   cudaEvent_t ev[14] = {};
   cudaEvent_t ev_after = nullptr;  // relief_gpu_map_after_stream
+  cudaEvent_t ev_fork = nullptr;   // frame stream -> copy stream (chunked upload)
+  // Executable graphs of recent synchronous-frame topologies, most recent
+  // first (pipeline.cu FrameCapture); off: direct launches.
+  static constexpr int kGraphs = 4;
+  cudaGraphExec_t graphs[kGraphs] = {};
+  int graph_count = 0;
+  long long graph_instantiations = 0, graph_updates = 0;
+  // Off by default: measured no device-time gain over PDL-chained direct
+  // launches and more host time per call (profiles/r2_host_overhead.txt).
+  bool use_graphs = false;
   // Synchronous host-input frames: the upload is split into kChunks copies on
   // copy_stream and each chunk is ingested as soon as it lands.
   static constexpr int kChunks = 2;  // 2 and 4 measured alike; 8 slower

@@ -1576,9 +1576,18 @@ __global__ void __launch_bounds__(256)
 // Phase-boundary events (per-phase device times); an event between two
 // kernels also ends their programmatic overlap, so they are recorded only
 // when phase timing is requested (DeviceMap::phase_events).
+// Timing events are recorded as external event nodes when the frame is
+// captured into a graph (a plain record inside a capture only orders streams).
+inline void recordTiming(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  checkCuda(cudaStreamIsCapturing(s, &cs), "capture status");
+  checkCuda(cudaEventRecordWithFlags(e, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                               : cudaEventRecordDefault),
+            "event");
+}
 #define RB_PHASE_EVENT(k, stream) \
   do {                           \
-    if (m.phase_events) checkCuda(cudaEventRecord(m.ev[k], stream), "event"); \
+    if (m.phase_events) recordTiming(m.ev[k], stream); \
   } while (0)
 
 inline unsigned gridFor(size_t n, int threads = kThreads) {
@@ -1627,7 +1636,7 @@ struct Frame {
 // Stats reset + move_to (reference grid.cpp:87-111).
 void phaseBegin(Frame& f, bool record_start = true) {
   DeviceMap& m = f.m;
-  if (record_start) checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
+  if (record_start) recordTiming(m.ev[0], f.s);
   checkCuda(cudaMemsetAsync(m.stats, 0, sizeof(DevStats), f.s), "memset");
   const int sx = quantizedShift(f.pose.t[0] - m.grid.center_x, m.grid.resolution);
   const int sy = quantizedShift(f.pose.t[1] - m.grid.center_y, m.grid.resolution);
@@ -1686,33 +1695,35 @@ const double* phaseUpload(Frame& f, const double* xyz, std::size_t n, bool on_de
 const double* phaseUploadChunked(Frame& f, const double* xyz, uint32_t N) {
   DeviceMap& m = f.m;
   phaseScratch(f, N);
-  checkCuda(cudaStreamWaitEvent(m.copy_stream, m.ev[0], 0), "stream wait");
+  checkCuda(cudaEventRecord(m.ev_fork, f.s), "event");
+  checkCuda(cudaStreamWaitEvent(m.copy_stream, m.ev_fork, 0), "stream wait");
   const uint32_t chunk = chunkPoints(N);
   for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
     const std::size_t len = std::min(chunk, N - base);
     checkCuda(cudaMemcpyAsync(m.xyz_in + 3 * static_cast<std::size_t>(base), xyz + 3 * static_cast<std::size_t>(base),
                               len * 3 * sizeof(double), cudaMemcpyHostToDevice, m.copy_stream),
               "point upload");
+    // upload done (timing) before the last chunk's event, which the frame
+    // stream waits on: the copy stream ends joined to it (graph capture)
+    if (base + chunk >= N) recordTiming(m.ev[13], m.copy_stream);
     checkCuda(cudaEventRecord(m.ev_chunk[c], m.copy_stream), "event");
   }
-  checkCuda(cudaEventRecord(m.ev[13], m.copy_stream), "event");  // upload done
   return m.xyz_in;
 }
 
 // K2 geometry for N keys: 1-3 LSD passes over the bits of the cell id. The
 // tile digit counts are accumulated upstream, so they are zeroed here.
-SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
-  DeviceMap& m = f.m;
+SortGeom sortGeometry(DeviceMap& m, uint32_t WH, uint32_t N) {
   SortGeom sg;
   if (N == 0) return sg;
-  const int bits = 32 - __builtin_clz(f.WH);
+  const int bits = 32 - __builtin_clz(WH);
   sg.passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
   sg.dbits = (bits + sg.passes - 1) / sg.passes;
   sg.ntiles = (N + kTile - 1) / kTile;
   sg.pitch = (sg.ntiles + 3) & ~3u;
   const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
   const std::size_t need = tcn + static_cast<std::size_t>(sg.passes) * sg.buckets();
-  if (m.hist_cap < need) {
+  if (m.hist_cap < need) {  // (reserved before a graph capture: no allocation inside one)
     cudaFree(m.hist);
     m.hist = nullptr;
     m.hist_cap = need;
@@ -1720,6 +1731,13 @@ SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
   }
   sg.tc = m.hist;
   sg.rowsum = m.hist + tcn;
+  return sg;
+}
+
+SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
+  const SortGeom sg = sortGeometry(f.m, f.WH, N);
+  if (N == 0) return sg;
+  const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
   checkCuda(cudaMemsetAsync(sg.tc, 0, tcn * sizeof(uint32_t), f.s), "memset");
   return sg;
 }
@@ -1937,17 +1955,89 @@ void phaseCells(Frame& f) {
   if (f.P.use_convnet_traversability)
     f.launches += convnetEnqueue(f.s, m.conv, m.cur.elev, m.cur.valid, f.g.W, f.g.H, f.P.convnet,
                                  m.cur.trav);
-  checkCuda(cudaEventRecord(m.ev[12], f.s), "event");  // traversability done
+  recordTiming(m.ev[12], f.s);  // traversability done
 }
 
 // Stats to the host (one sync).
-const DevStats& phaseStats(Frame& f) {
+void phaseStatsEnqueue(Frame& f) {
   DeviceMap& m = f.m;
   checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, f.s), "stats");
   checkCuda(cudaGetLastError(), "kernel launch");
+}
+const DevStats& phaseStatsWait(Frame& f) {
+  DeviceMap& m = f.m;
   checkCuda(cudaStreamSynchronize(f.s), "integrate");
   if (m.h_stats->error_code == 1) fail(Err::kInvalidVariance, "variances must be positive");
   return *m.h_stats;
+}
+const DevStats& phaseStats(Frame& f) {
+  phaseStatsEnqueue(f);
+  return phaseStatsWait(f);
+}
+
+// One CUDA graph per synchronous frame: the frame's launches
+// are captured from the map's stream and the capture updates a cached
+// executable graph (cudaGraphExecUpdate: new kernel arguments, copy sources,
+// grid sizes); a topology not seen recently is instantiated once and kept
+// (DeviceMap::kGraphs entries). Host cost per frame: the capture (~0.3 us per
+// launch) + update + one launch, instead of ~3 us per direct launch
+// (scripts/graph_overhead.cu). Programmatic (PDL) edges are kept in the graph.
+struct FrameCapture {
+  DeviceMap& m;
+  cudaStream_t s;
+  bool on;
+  FrameCapture(DeviceMap& map, cudaStream_t st, bool enable) : m(map), s(st), on(enable) {
+    if (on) checkCuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+  }
+  ~FrameCapture() {  // an exception mid-frame: end (and drop) the capture
+    if (on) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+    }
+  }
+  void launch() {
+    if (!on) return;
+    on = false;
+    cudaGraph_t g = nullptr;
+    checkCuda(cudaStreamEndCapture(s, &g), "end capture");
+    cudaGraphExec_t exec = nullptr;
+    // most recently used first
+    for (int k = 0; k < m.graph_count && exec == nullptr; ++k) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(m.graphs[k], g, &info) == cudaSuccess) {
+        exec = m.graphs[k];
+        std::rotate(m.graphs, m.graphs + k, m.graphs + k + 1);
+        ++m.graph_updates;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (exec == nullptr) {
+      const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        checkCuda(e, "graph instantiate");
+      }
+      if (m.graph_count == DeviceMap::kGraphs) cudaGraphExecDestroy(m.graphs[--m.graph_count]);
+      std::copy_backward(m.graphs, m.graphs + m.graph_count, m.graphs + m.graph_count + 1);
+      m.graphs[0] = exec;
+      ++m.graph_count;
+      ++m.graph_instantiations;
+    }
+    cudaGraphDestroy(g);
+    checkCuda(cudaGraphLaunch(exec, s), "graph launch");
+  }
+};
+
+bool hostPinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
 }
 
 ScanResult resultFrom(const DevStats& d, std::size_t n) {
@@ -1980,12 +2070,30 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   if (m.async_count != 0) fail(Err::kUsage, "streaming frames in flight: call relief_gpu_map_wait");
   Frame f(m, P, pose, stamp, dt);
   const uint32_t N = static_cast<uint32_t>(n);
+  // Scratch first: nothing may allocate inside a graph capture.
+  if (n > 0) {
+    phaseScratch(f, n);
+    sortGeometry(m, f.WH, N);
+  }
+  // Pageable host input cannot be a graph's copy source: it is uploaded
+  // before the capture (the frame then reads it like device input).
+  const bool pageable = !xyz_on_device && n > 0 && !hostPinned(xyz);
+  const bool graph = m.use_graphs && !P.use_convnet_traversability;
   // ev0 -> ev13: the input copy (host input only); everything after it is the
   // frame's device time (stats / count / tile-count resets, recenter, kernels).
-  checkCuda(cudaEventRecord(m.ev[0], f.s), "event");
-  const bool chunked = !xyz_on_device && N >= 2 * kTile;
-  const double* d_xyz = chunked ? phaseUploadChunked(f, xyz, N) : phaseUpload(f, xyz, n, xyz_on_device);
-  if (!chunked) checkCuda(cudaEventRecord(m.ev[13], f.s), "event");  // copy done
+  const double* d_xyz = xyz;
+  if (pageable) {
+    recordTiming(m.ev[0], f.s);
+    d_xyz = phaseUpload(f, xyz, n, false);
+    recordTiming(m.ev[13], f.s);
+  }
+  FrameCapture cap(m, f.s, graph);
+  const bool chunked = !xyz_on_device && !pageable && N >= 2 * kTile;
+  if (!pageable) {
+    recordTiming(m.ev[0], f.s);
+    d_xyz = chunked ? phaseUploadChunked(f, xyz, N) : phaseUpload(f, xyz, n, xyz_on_device);
+    if (!chunked) recordTiming(m.ev[13], f.s);  // copy done
+  }
   phaseBegin(f, false);
   // count[] is all zero here: k_cells clears it after its last use each scan.
   const SortGeom sg = phaseSortGeometry(f, N);
@@ -2011,7 +2119,9 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   }
   RB_PHASE_EVENT(6, f.s);  // rays done
   phaseCells(f);
-  const DevStats& d = phaseStats(f);
+  phaseStatsEnqueue(f);
+  cap.launch();
+  const DevStats& d = phaseStatsWait(f);
   ScanResult out = resultFrom(d, n);
 
   // Per-phase device times are read from the events only when asked for

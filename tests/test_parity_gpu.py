@@ -358,3 +358,37 @@ def test_traversability_window_larger_than_shared_memory(gpu, reference, tmp_pat
         z = -1.0 + 0.05 * np.sin(xy[:, 0]) + 0.01 * rng.standard_normal(40000)
         pair.integrate(np.column_stack([xy, z]), pose, 0.1 * scan, context=f"scan {scan}")
         pair.compare(context=f"window 151 scan {scan}")
+
+
+def test_graph_and_direct_launches_identical(gpu, reference, tmp_path):
+    """One CUDA graph per frame vs direct launches (the default) vs the reference: frames whose size,
+    recenter and input kind (pinned host / pageable host / device) change from call to call, so
+    cached graphs are updated, re-instantiated and reused."""
+    import torch
+    text = wl._map(0.04, 200, 200) + "noise.alpha_d = 0.0002\n" + wl.lidar(300, rings=48) + wl.SCENE_S0
+    pair = Pair(gpu, reference, tmp_path, text, 0.04, 200, 200)
+    pair.maps[0].set_graphs(True)
+    direct = pk.ReliefMap.create(gpu, 0.04, 200, 200)  # direct launches (the default)
+    cfg = pair.cfgs[0]
+    for f in range(12):
+        pose = wl.pose34(np.eye(3), (0.05 * (f // 3), 0.0, 1.0))  # recenter on every third frame
+        xyz = ref_render(reference, pair.cfg_path, pose, 0.1 * f, 9, f)
+        xyz = xyz[: len(xyz) - 997 * (f % 4)]                      # sizes change
+        kind = f % 3
+        if kind == 0:
+            got = pair.maps[0].integrate(torch.from_numpy(xyz.copy()).pin_memory().numpy(), pose, 0.1 * f, cfg)
+        elif kind == 1:
+            got = pair.maps[0].integrate(xyz, pose, 0.1 * f, cfg)
+        else:
+            t = torch.from_numpy(xyz.copy()).cuda()
+            torch.cuda.synchronize()
+            got = pair.maps[0].integrate_device(t.data_ptr(), len(xyz), pose, 0.1 * f, cfg)
+        want = pair.maps[1].integrate(xyz, pose, 0.1 * f, pair.cfgs[1])
+        d = direct.integrate(xyz, pose, 0.1 * f, cfg)
+        assert_stats_match(got, want, drift_tol=1e-12, context=f"frame {f}")
+        assert_stats_match(d, got, context=f"direct frame {f}")
+        assert_layers_match(direct.layers(), pair.maps[0].layers(), tol_trav=0.0, context=f"direct {f}")
+        pair.compare(height_tol=1e-9, context=f"frame {f}")
+    inst, upd = pair.maps[0].graph_stats()
+    assert inst >= 2 and upd >= 6, (inst, upd)
+    assert direct.graph_stats() == (0, 0)
