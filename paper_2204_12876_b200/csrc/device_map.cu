@@ -57,7 +57,14 @@ void carveLayers(Carver& c, Layers& L, std::size_t n) {
   L.ubv = c.take<uint8_t>(n);
 }
 
-__global__ void k_fill_fresh(Layers L, std::size_t n, int32_t* kstar) {
+// Probe words of the padded grid: the border is tag 3 ("outside the grid")
+// for good; the interior is rewritten by every frame's classification.
+__global__ void k_probe_border(uint16_t* probe, std::size_t n) {
+  const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  if (i < n) probe[i] = 3;
+}
+
+__global__ void k_fill_fresh(Layers L, std::size_t n, int32_t* kstar, double* ub2) {
   const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
@@ -72,6 +79,8 @@ __global__ void k_fill_fresh(Layers L, std::size_t n, int32_t* kstar) {
   L.valid[i] = 0;
   L.ubv[i] = 0;
   kstar[i] = INT_MAX;
+  if (i == 0) kstar[-1] = INT_MAX;
+  ub2[i] = __longlong_as_double(0x7ff0000000000000LL);
 }
 
 // Layer ids for the masked export; order = reference snapshot.cpp:43-48.
@@ -139,22 +148,27 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
       checkCuda(cudaMallocHost(&m->h_slot[k], sizeof(DevStats)), "pinned stats");
     }
     const std::size_t n = grid.cells();
-    const std::size_t bytes = 2 * layerBytes(n) + 5 * alignUp(n * 4) + alignUp((n + 1) * 4) +
-                              alignUp(n) + 7 * kAlign;
+    const std::size_t np = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2);
+    const std::size_t bytes = 2 * layerBytes(n) + 4 * alignUp(n * 4) + alignUp(np * 2) +
+                              alignUp((n + 1) * 4) + alignUp(n) + alignUp(n * 8) + 8 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
     Carver c{static_cast<char*>(m->slab)};
     carveLayers(c, m->cur, n);
     carveLayers(c, m->alt, n);
     m->count = c.take<int32_t>(n);
-    m->kstar = c.take<int32_t>(n);
+    m->kstar = c.take<int32_t>(n + 32) + 32;  // kstar[-1]: the frame's "any removal" flag
     m->heavy = c.take<uint32_t>(2 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
-    m->probe = c.take<uint16_t>(n);
+    m->probe = c.take<uint16_t>(static_cast<std::size_t>(grid.width + 2) * (grid.height + 2));
+    m->ub2 = c.take<double>(n);
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
     fillFresh(*m);
+    const std::size_t np2 = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2);
+    k_probe_border<<<static_cast<unsigned>((np2 + 255) / 256), 256, 0, m->stream>>>(m->probe, np2);
+    checkCuda(cudaGetLastError(), "probe init");
     checkCuda(cudaMemsetAsync(m->count, 0, n * sizeof(int32_t), m->stream), "map init");
     checkCuda(cudaMemsetAsync(m->start, 0xff, (n + 1) * sizeof(uint32_t), m->stream), "map init");
     checkCuda(cudaStreamSynchronize(m->stream), "map init");
@@ -208,7 +222,7 @@ void destroyDeviceMap(DeviceMap* m) {
 
 void fillFresh(DeviceMap& m) {
   const std::size_t n = m.grid.cells();
-  k_fill_fresh<<<static_cast<unsigned>((n + 255) / 256), 256, 0, m.stream>>>(m.cur, n, m.kstar);
+  k_fill_fresh<<<static_cast<unsigned>((n + 255) / 256), 256, 0, m.stream>>>(m.cur, n, m.kstar, m.ub2);
   checkCuda(cudaGetLastError(), "fill launch");
 }
 

@@ -54,6 +54,7 @@ struct DevStats {
   int drift_clamped;
   int error_code;                     // 0 ok, 1 non-positive variance
   int respeculate;                    // a heavy cell fused nothing: redo the ray pass
+  unsigned int ingest_done;           // ingest blocks finished (the last one reduces the drift vote)
 };
 
 // Geometry + parameters passed by value to kernels.
@@ -120,8 +121,9 @@ struct DeviceMap {
   int32_t* count = nullptr;
   uint32_t* start = nullptr;
   uint8_t* cls = nullptr;
-  uint16_t* probe = nullptr;  // pass-1 probe words (class + conservative gate bound)
+  uint16_t* probe = nullptr;  // pass-1 probe words (class + conservative gate bound), (W+2)x(H+2)
   int32_t* kstar = nullptr;
+  double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
   // per-point scratch (grown on demand)
   std::size_t cap = 0;
@@ -257,7 +259,8 @@ struct ShardIO {
   uint32_t* rec_cell = nullptr;     // device, n_records (scan order)
   double* rec_z = nullptr;
   double* rec_var = nullptr;
-  int32_t* kstar = nullptr;   // device, cells: first removing ray per cell
+  int32_t* kstar = nullptr;
+  double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)   // device, cells: first removing ray per cell
   double* ub = nullptr;       // device, cells: upper-bound layer
   uint8_t* ubv = nullptr;     // device, cells: upper-bound validity
   std::size_t cells = 0;

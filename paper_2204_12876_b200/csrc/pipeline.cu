@@ -6,18 +6,17 @@
 //   K4a k_shift          recenter: streaming copy of the 10 persistent layers
 //   K1  k_ingest         range / exclusion / transform / sigma_p^2 / cell /
 //                        drift vote / per-cell count      (one thread per point)
-//       k_drift_finalize fixed-order reduction of the drift vote (1 block)
-//   K4b k_apply_offset   drift offset on valid heights and finite bounds
+//                        (+ drift vote mean, fixed-order, in the last block)
 //   K2  radix sort       stable LSD sort of (cell, point) -> per-cell segments
 //                        in scan order; exclusive scan count -> segment start
-//   K3  k_fuse           gated Kalman fold, one thread per occupied cell
-//       k_classify       per-cell ray class (nothing / bound / removal candidate)
+//   K3  k_fuse           drift offset + gated Kalman fold + ray class, one
+//                        thread per cell (long cells: k_fuse_heavy, side stream)
 //   K5  k_rays_pass1     exact 2-D DDA per kept point: bounds of invalid cells,
 //                        k* = first removing ray per candidate cell
-//       k_remove         invalidate cells with k* < inf
-//   K6  k_rays_pass2     bounds of removed cells from rays k >= k*
-//   K7  k_cells          overlap clearance + normals + traversability + time
-//                        variance, one shared-memory tile with a halo
+//   K6  k_rays_pass2     bounds of removed cells from rays k >= k* (scratch)
+//   K7  k_cells          removal (k* < inf) + overlap clearance + normals +
+//                        traversability + time variance, one shared-memory
+//                        tile with a halo
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -138,6 +137,81 @@ __global__ void __launch_bounds__(kThreads) k_shift(Layers in, Layers out, int W
   }
 }
 
+// ------------------------------------------------------ drift reduction
+// Mean error over the votes and the clamped offset (reference drift.cpp:24-55,
+// integration.cpp:119-128) from the per-block partials. The sums run in one
+// fixed tree whatever block runs it -- 1024 strided lanes, warp trees, the 32
+// warp sums in order -- so the result is run-to-run deterministic and the same
+// in the single-GPU frame (last block of k_ingest) and the group frame
+// (k_drift_finalize over the gathered partials); it differs from the
+// reference's sequential sum only in the last bits.
+constexpr int kDriftLanes = 1024;
+__device__ __forceinline__ void driftFinalizeBlock(const double* part, const int* npart, int nblocks,
+                                                   int min_points, double max_off,
+                                                   double* offset_out, DevStats* st) {
+  __shared__ double s_dsum[32];
+  __shared__ long long s_dcnt[32];
+  __shared__ double s_lane[kDriftLanes];
+  __shared__ long long s_lcnt[kDriftLanes];
+  const int lane = threadIdx.x & 31;
+  // lane v's strided sum part[v] + part[v + 1024] + ..., all lanes' loads in flight together
+  for (int v = threadIdx.x; v < kDriftLanes; v += blockDim.x) {
+    double sum = 0.0;
+    long long c = 0;
+    if (v < nblocks) {
+      const int nb = (nblocks - 1 - v) / kDriftLanes + 1;
+      double pv[4];
+      int nv[4];
+      for (int b0 = 0; b0 < nb; b0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int b = v + (b0 + u) * kDriftLanes;
+          pv[u] = b0 + u < nb ? __ldcg(part + b) : 0.0;
+          nv[u] = b0 + u < nb ? __ldcg(npart + b) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (b0 + u < nb) {
+            sum += pv[u];
+            c += nv[u];
+          }
+      }
+    }
+    s_lane[v] = sum;
+    s_lcnt[v] = c;
+  }
+  __syncthreads();
+  for (int vw = threadIdx.x >> 5; vw < 32; vw += blockDim.x >> 5) {
+    double sum = s_lane[vw * 32 + lane];
+    long long c = s_lcnt[vw * 32 + lane];
+    sum = warpSum(sum);
+    c = warpSum(c);
+    if (lane == 0) {
+      s_dsum[vw] = sum;
+      s_dcnt[vw] = c;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = s_dsum[0];
+    long long cnt = s_dcnt[0];
+    for (int w = 1; w < 32; ++w) {
+      total += s_dsum[w];
+      cnt += s_dcnt[w];
+    }
+    const int nvote = static_cast<int>(cnt);
+    double off = 0.0;
+    if (nvote >= min_points) {
+      const double mean = total / nvote;
+      off = sclamp(mean, -max_off, max_off);
+      st->drift_offset = off;
+      st->drift_clamped = off != mean;
+      st->drift_n = nvote;
+    }
+    *offset_out = off;
+  }
+}
+
 // ------------------------------------------------------------- K1 ingest
 struct IngestArgs {
   GridArgs g;
@@ -149,6 +223,12 @@ struct IngestArgs {
   double alpha_d, sigma_p_min2;
   int drift_enabled;
   double drift_thr;
+  // drift offset computed by the last block to finish (0: not here -- a group
+  // frame reduces the gathered partials in k_drift_finalize)
+  uint32_t drift_blocks;  // frame-wide block count of the ingest
+  int drift_min_points;
+  double drift_max_off;
+  double* drift_offset;
 };
 
 // Per point (reference integration.cpp:85-113,134-140; sensing.cpp:32-41;
@@ -262,6 +342,19 @@ __global__ void __launch_bounds__(kThreads)
     if (c2) atomicAdd(&st->excluded, static_cast<unsigned long long>(c2));
     if (c3) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c3));
   }
+  if (a.drift_blocks == 0) return;
+  // The last block of the frame's ingest (over all chunk launches) reduces the
+  // partials: no separate finalize launch.
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&st->ingest_done, 1u) == a.drift_blocks - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  driftFinalizeBlock(drift_part, drift_npart, static_cast<int>(a.drift_blocks), a.drift_min_points,
+                     a.drift_max_off, a.drift_offset, st);
 }
 
 // ------------------------------------------------------ drift (one block)
@@ -273,42 +366,10 @@ __global__ void __launch_bounds__(1024)
     k_drift_finalize(const double* part, const int* npart, int nblocks, int min_points,
                      double max_off, double* offset_out, DevStats* st) {
   pdlEnter();
-  __shared__ double s_sum[32];
-  __shared__ long long s_cnt[32];
-  double s = 0.0;
-  long long c = 0;
-  for (int b = threadIdx.x; b < nblocks; b += 1024) {
-    s += part[b];
-    c += npart[b];
-  }
-  s = warpSum(s);
-  c = warpSum(c);
-  if ((threadIdx.x & 31) == 0) {
-    s_sum[threadIdx.x >> 5] = s;
-    s_cnt[threadIdx.x >> 5] = c;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double total = s_sum[0];
-    long long cnt = s_cnt[0];
-    for (int w = 1; w < 32; ++w) {
-      total += s_sum[w];
-      cnt += s_cnt[w];
-    }
-    const int nvote = static_cast<int>(cnt);
-    double off = 0.0;
-    if (nvote >= min_points) {
-      const double mean = total / nvote;
-      off = sclamp(mean, -max_off, max_off);
-      st->drift_offset = off;
-      st->drift_clamped = off != mean;
-      st->drift_n = nvote;
-    }
-    *offset_out = off;
-  }
+  driftFinalizeBlock(part, npart, nblocks, min_points, max_off, offset_out, st);
 }
 
-// Reference drift.cpp:44-55.
+// Reference drift.cpp:44-55 as a separate sweep (RB_FUSE_OFFSET=0 builds).
 __global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, const double* off_p) {
   pdlEnter();
   const double off = *off_p;
@@ -573,6 +634,80 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ----------------------------------------------------- ray classes
+enum : uint8_t { kClsNone = 0, kClsBound = 1, kClsCandidate = 2 };
+
+struct RayArgs {
+  GridArgs g;
+  double o[3];  // sensor origin = pose translation
+  double now, t_free, alpha_n;
+  int cleanup, bound;
+  // Per-frame ray constants: the origin lies in the closed map extent, and its
+  // cell (the start cell of every ray that is not clipped at its start).
+  int origin_in, ocol, orow;
+};
+
+// Post-fusion ray class per cell; also resets k* (reference raycast.cpp:
+// 132-183 gates that do not depend on the ray).
+//
+// Speculation (heavy >= 0): cells longer than `heavy` are still being folded
+// by k_fuse_heavy when this runs. A cell that fuses at least one point ends
+// valid with last_update = now, i.e. class "none" whenever t_free >= 0, so
+// those cells are classified "none" up front; k_fuse_heavy flags any heavy
+// cell that fused nothing and the ray pass is then redone (retry = 1: this
+// kernel and pass 1 run only if the flag is set).
+// Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
+// above it, an f16 bound F >= T of the cell's gate threshold T (T =
+// upper_bound for a bound cell, elevation - sqrt(variance) for a removal
+// candidate), so that a visit with ray height h >= F is rejected without
+// loading the cell state: the reference's own test (h < ub, resp.
+// !(h >= elev - sqrt(var))) rejects it too. F is T rounded up (double -> f32
+// -> f16) and then up again to a multiple of 4 ulps (for negative values:
+// towards zero); NaN thresholds become +inf, values beyond the f16 range +inf
+// or -65504 (both still >= T).
+typedef uint16_t ProbeT;
+__device__ __forceinline__ ProbeT probeWord(uint8_t cls, double t) {
+  if (cls == kClsNone) return 0u;
+  // up-rounded twice (double -> f32 -> f16) stays >= t
+  const __half hf = (t == t) ? __float2half_ru(__double2float_ru(t)) : __ushort_as_half(0x7c00);
+  uint32_t b = __half_as_ushort(hf);
+  b = (b >> 15) ? (b & ~3u) : ((b + 3u) & ~3u);
+  return static_cast<ProbeT>(b | cls);
+}
+__device__ __forceinline__ double probeBound(uint32_t w) {
+  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & ~3u))));
+}
+
+// Ray class + probe word of cell i from its post-fusion state, k* reset
+// (the reference's ray-independent gates, raycast.cpp:132-183). A cell still
+// being folded on the side stream is speculated "none" (see k_fuse_heavy).
+struct ClassArgs {
+  double now, t_free;
+  int cleanup, bound;
+  int W;  // grid width: the probe words sit on the (W+2) x (H+2) padded grid
+};
+__device__ __forceinline__ void classifyCell(const Layers& L, size_t i, bool speculated,
+                                             const ClassArgs& a, uint8_t* cls, ProbeT* probe,
+                                             int32_t* kstar) {
+  uint8_t c = kClsNone;
+  double t = 0.0;
+  if (speculated) {
+    c = kClsNone;
+  } else if (!L.valid[i]) {
+    c = a.bound ? kClsBound : kClsNone;
+    if (c) t = L.ub[i];
+  } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
+             (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
+    c = kClsCandidate;
+    t = L.elev[i] - sqrt(L.var[i]);
+  }
+  cls[i] = c;
+  const size_t r = i / static_cast<unsigned>(a.W);
+  probe[i + static_cast<size_t>(a.W) + 3 + 2 * r] = probeWord(c, t);  // padded (r+1, c+1)
+  kstar[i] = INT_MAX;
+  if (i == 0) kstar[-1] = INT_MAX;  // the frame's "any removal" flag (candidateVisit)
+}
+
 // ------------------------------------------------------------- K3 fusion
 struct FuseArgs {
   double now;
@@ -726,14 +861,31 @@ __device__ __forceinline__ void flushCounts(FoldCounts k, DevStats* st) {
 // concurrently with the ray pass: cells
 // with more than kVeryHeavyCell points on their own list (one warp each there).
 constexpr int kVeryHeavyCell = 256;
+//
+// Every cell also gets the frame's drift offset first (reference drift.cpp:
+// 44-55, off_p: device scalar from the ingest's drift reduction; null = none)
+// and, after its fold, its ray class and probe word (classify != 0), so the
+// ray pass follows without a separate classification sweep.
 __global__ void __launch_bounds__(kThreads)
     k_fuse(Layers L, size_t ncell, const int32_t* __restrict__ count,
            const uint32_t* __restrict__ start, const double* __restrict__ spz,
            const double* __restrict__ spv, FuseArgs a, DevStats* st, int heavy,
-           uint32_t* heavy_list, uint32_t* vheavy_list) {
-  pdlEnter();
+           uint32_t* heavy_list, uint32_t* vheavy_list, const double* __restrict__ off_p,
+           int classify, ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
+           int32_t* __restrict__ kstar) {
+  // wait first: the ray pass launched on our trigger may then read anything
+  // older than this kernel before its own wait
+  pdlWait();
+  pdlTrigger();
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const int cnt = i < ncell ? count[i] : 0;
+  if (off_p != nullptr && i < ncell) {
+    const double off = *off_p;
+    if (off != 0.0) {
+      if (L.valid[i]) L.elev[i] += off;
+      if (L.ubv[i]) L.ub[i] += off;
+    }
+  }
   const bool is_heavy = cnt > heavy;
   const bool is_vheavy = is_heavy && cnt > kVeryHeavyCell;
   const int lane = threadIdx.x & 31;
@@ -755,6 +907,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   FoldCounts k;
   if (cnt > 0 && !is_heavy) foldCell(L, i, cnt, start, spz, spv, a, st, k);
+  if (classify && i < ncell) classifyCell(L, i, is_heavy, ca, cls, probe, kstar);
   flushCounts(k, st);
 }
 
@@ -845,49 +998,9 @@ __global__ void __launch_bounds__(32)
 }
 
 // ------------------------------------------------------------- K5/K6 rays
-enum : uint8_t { kClsNone = 0, kClsBound = 1, kClsCandidate = 2 };
-
-struct RayArgs {
-  GridArgs g;
-  double o[3];  // sensor origin = pose translation
-  double now, t_free, alpha_n;
-  int cleanup, bound;
-  // Per-frame ray constants: the origin lies in the closed map extent, and its
-  // cell (the start cell of every ray that is not clipped at its start).
-  int origin_in, ocol, orow;
-};
-
-// Post-fusion ray class per cell; also resets k* (reference raycast.cpp:
-// 132-183 gates that do not depend on the ray).
-//
-// Speculation (heavy >= 0): cells longer than `heavy` are still being folded
-// by k_fuse_heavy when this runs. A cell that fuses at least one point ends
-// valid with last_update = now, i.e. class "none" whenever t_free >= 0, so
-// those cells are classified "none" up front; k_fuse_heavy flags any heavy
-// cell that fused nothing and the ray pass is then redone (retry = 1: this
-// kernel and pass 1 run only if the flag is set).
-// Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
-// above it, an f16 bound F >= T of the cell's gate threshold T (T =
-// upper_bound for a bound cell, elevation - sqrt(variance) for a removal
-// candidate), so that a visit with ray height h >= F is rejected without
-// loading the cell state: the reference's own test (h < ub, resp.
-// !(h >= elev - sqrt(var))) rejects it too. F is T rounded up (double -> f32
-// -> f16) and then up again to a multiple of 4 ulps (for negative values:
-// towards zero); NaN thresholds become +inf, values beyond the f16 range +inf
-// or -65504 (both still >= T).
-typedef uint16_t ProbeT;
-__device__ __forceinline__ ProbeT probeWord(uint8_t cls, double t) {
-  if (cls == kClsNone) return 0u;
-  // up-rounded twice (double -> f32 -> f16) stays >= t
-  const __half hf = (t == t) ? __float2half_ru(__double2float_ru(t)) : __ushort_as_half(0x7c00);
-  uint32_t b = __half_as_ushort(hf);
-  b = (b >> 15) ? (b & ~3u) : ((b + 3u) & ~3u);
-  return static_cast<ProbeT>(b | cls);
-}
-__device__ __forceinline__ double probeBound(uint32_t w) {
-  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & ~3u))));
-}
-
+// Classification sweep for the retry of a wrong speculation (retry = 1: runs
+// only if k_fuse_heavy flagged it) and for frames whose classes k_fuse did not
+// write (a shard frame without records).
 __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayArgs a, uint8_t* cls,
                                                        int32_t* kstar,
                                                        const int32_t* __restrict__ count,
@@ -905,24 +1018,10 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
       st->visits = 0;
     }
   }
+  const ClassArgs ca{a.now, a.t_free, a.cleanup, a.bound, a.g.W};
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    uint8_t c = kClsNone;
-    double t = 0.0;
-    if (heavy >= 0 && count[i] > heavy) {
-      c = kClsNone;
-    } else if (!L.valid[i]) {
-      c = a.bound ? kClsBound : kClsNone;
-      if (c) t = L.ub[i];
-    } else if (a.cleanup && !(a.now - L.last[i] <= a.t_free) &&
-               (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0)) {
-      c = kClsCandidate;
-      t = L.elev[i] - sqrt(L.var[i]);
-    }
-    cls[i] = c;
-    probe[i] = probeWord(c, t);
-    kstar[i] = INT_MAX;
-  }
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    classifyCell(L, i, heavy >= 0 && count[i] > heavy, ca, cls, probe, kstar);
 }
 
 // Liang-Barsky slab clip (reference raycast.cpp:30-42).
@@ -1124,8 +1223,8 @@ __device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) 
 // Removal gates for a candidate cell (reference raycast.cpp:138-150), literal
 // comparison forms; records the ray in k*.
 __device__ __forceinline__ void candidateVisit(const Layers& L, uint32_t c, double h, double vx,
-                                            double vy, double vz, double alpha_n, int32_t k,
-                                            int32_t* kstar) {
+                                               double vy, double vz, double alpha_n, int32_t k,
+                                               int32_t* kstar) {
   if (h >= L.elev[c] - sqrt(L.var[c])) return;
   const double n2 = (vx * vx + vy * vy) + vz * vz;
   double ux = vx, uy = vy, uz = vz;
@@ -1137,7 +1236,10 @@ __device__ __forceinline__ void candidateVisit(const Layers& L, uint32_t c, doub
   }
   const double align = fabs((ux * L.nx[c] + uy * L.ny[c]) + uz * L.nz[c]);
   if (align <= alpha_n) return;
-  if (k < kstar[c]) atomicMin(kstar + c, k);
+  if (k < kstar[c]) {
+    atomicMin(kstar + c, k);
+    kstar[-1] = 0;  // "some cell is removed this frame" (reset with k*)
+  }
 }
 
 struct Pass1Ctx {
@@ -1201,13 +1303,22 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
     if (t0 >= t1) return;
   }
-  uint32_t end_idx = 0xffffffffu;
+  // The probe words live on a grid padded by one border cell on every side
+  // (tag 3): the walk leaves the grid exactly when it steps onto the border
+  // (the reference's bounds test after a step, raycast.cpp:121,125), so the
+  // loop carries no per-axis step counters and no exit test of its own.
+  const uint32_t W = static_cast<uint32_t>(g.W), Wp = W + 2u;
+  uint32_t end_idx = 0xffffffffu;  // padded index of the endpoint's cell
   if (end_in) {
-    if (pcell < static_cast<uint32_t>(g.W) * static_cast<uint32_t>(g.H))
-      end_idx = pcell;
-    else
-      end_idx = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H)) * g.W +
-                clampCell(x86_to_int(floor((px - g.ox) / res)), g.W);
+    uint32_t er, ec;
+    if (pcell < W * static_cast<uint32_t>(g.H)) {
+      er = pcell / W;
+      ec = pcell - er * W;
+    } else {
+      er = static_cast<uint32_t>(clampCell(x86_to_int(floor((py - g.oy) / res)), g.H));
+      ec = static_cast<uint32_t>(clampCell(x86_to_int(floor((px - g.ox) / res)), g.W));
+    }
+    end_idx = (er + 1u) * Wp + ec + 1u;
   }
   int col = a.ocol, row = a.orow;
   if (t0 != 0.0) {
@@ -1228,22 +1339,16 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     div2_rn(res, (g.oy + (row + (step_row > 0 ? 1 : 0)) * res) - o[1], fabs(dy), tdy, q);
     tmy = dy < 0.0 ? -q : q;
   }
-  uint32_t idx = static_cast<uint32_t>(row) * g.W + col;
-  const int step_idx_row = step_row * g.W;
-  // Steps left along each axis before the walk leaves the grid (the
-  // reference's bounds test after a step, raycast.cpp:121,125).
-  int xl = step_col > 0 ? g.W - 1 - col : (step_col < 0 ? col : 0);
-  int yl = step_row > 0 ? g.H - 1 - row : (step_row < 0 ? row : 0);
+  uint32_t idx = (static_cast<uint32_t>(row) + 1u) * Wp + static_cast<uint32_t>(col) + 1u;
+  unsigned nx = 0, ny = 0;
+  const int step_idx_row = step_row * static_cast<int>(Wp);
   const ProbeT* __restrict__ probe = c.probe;
-  pdlWait();  // class / probe words come from k_classify
+  pdlWait();  // class / probe words come from the classification
   uint32_t wd = probe[idx];
   double t_enter = t0;
-  // The axis step is written without branches around it (both sides predicate
-  // cleanly: the exit tests are hoisted), and the step counters double as the
-  // visit count: iterations = steps taken + 1.
-  const int xl0 = xl, yl0 = yl;
-// Unrolled by 2: the compiler renames t_enter / t_next across the two copies
-// and interleaves them (pass 1 224 -> 194 us on C4).
+  bool exited = false;
+// Unrolled by 2: the compiler renames t_enter / m across the two copies and
+// interleaves them.
 #ifndef RB_P1_UNROLL
 #define RB_P1_UNROLL 2
 #endif
@@ -1253,31 +1358,45 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   RB_UNROLL(RB_P1_UNROLL)
   while (true) {
     const bool sx = tmx < tmy;
-    const double m = sx ? tmx : tmy;
-    const bool more = m < t1;
-    const double t_next = more ? m : t1;
-    if ((wd & 3u) != 0 && idx != end_idx && t_next > t_enter) {
-      const double h = c.oz + (0.5 * (t_enter + t_next)) * c.dz;
-      const uint8_t tag = static_cast<uint8_t>(wd & 3u);
-      if (tag == kClsCandidate) touched = true;
-      // probe filter: h >= F implies the exact gate rejects (see probeWord)
-      if (!(h >= probeBound(wd))) pass1Visit(c, tag, idx, h, touched);
+    const double m = sx ? tmx : tmy;  // = the reference's min (no NaN here)
+    bool more = m < t1;
+    // Only class / border cells leave the common path; the endpoint and
+    // zero-length tests of the reference's emission (t_next > t_enter) are
+    // made there, on the rare branch.
+    if ((wd & 3u) != 0) {
+      if ((wd & 3u) == 3u) {  // stepped out of the grid: stop before this cell
+        more = false;
+        exited = true;
+      } else {
+        const double t_next = more ? m : t1;
+        if (idx != end_idx && t_next > t_enter) {
+          const double h = c.oz + (0.5 * (t_enter + t_next)) * c.dz;
+          const uint8_t tag = static_cast<uint8_t>(wd & 3u);
+          if (tag == kClsCandidate) touched = true;
+          // probe filter: h >= F implies the exact gate rejects (see probeWord)
+          if (!(h >= probeBound(wd))) {
+            const uint32_t pr = idx / Wp;
+            pass1Visit(c, tag, (pr - 1u) * W + (idx - pr * Wp - 1u), h, touched);
+          }
+        }
+      }
     }
-    const int lim = sx ? xl : yl;
-    if (!more || lim == 0) break;
+    if (!more) break;
+    // (the step counters keep the axis step predicated: two predicated adds
+    // each, rather than both adds and four selects)
     if (sx) {
-      --xl;
       tmx += tdx;
+      ++nx;
     } else {
-      --yl;
       tmy += tdy;
+      ++ny;
     }
-    const int inc = sx ? step_col : step_idx_row;
-    idx += inc;
+    idx += sx ? step_col : step_idx_row;
     wd = probe[idx];
-    t_enter = t_next;
+    t_enter = m;
   }
-  visits += static_cast<unsigned>((xl0 - xl) + (yl0 - yl) + 1);
+  // cells iterated = steps taken + 1 (the step onto the border excluded)
+  visits += nx + ny + 1u - (exited ? 1u : 0u);
 }
 
 // 128-thread blocks, 9 per SM: 56 registers (no spills in the DDA loop) at 36
@@ -1357,14 +1476,19 @@ __global__ void __launch_bounds__(kThreads) k_remove(Layers L, size_t n, const i
 
 // Bounds of removed cells: only rays at or after the first removing ray saw
 // them invalid (reference integration.cpp:212-222 ordering).
+// kScratch: the removal itself happens later in k_cells, so the bounds go to
+// the scratch array ub2 (+inf when untouched) that k_cells moves into the
+// removed cells; otherwise (sharded frames) k_remove has run and the bounds go
+// to the map.
+template <bool kScratch>
 __global__ void __launch_bounds__(kThreads)
     k_rays_pass2(const uint32_t* __restrict__ raylist, const DevStats* st_in,
                  const double* __restrict__ px, const double* __restrict__ py,
                  const double* __restrict__ pz, RayArgs a, Layers L,
                  const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar,
-                 uint32_t ray_base) {
+                 uint32_t ray_base, double* ub2) {
   pdlEnter();
-  if (st_in->removed == 0) return;
+  if (kScratch ? kstar[-1] == INT_MAX : st_in->removed == 0) return;
   const unsigned total = static_cast<unsigned>(st_in->candidate_rays);
   for (unsigned q = blockIdx.x * kThreads + threadIdx.x; q < total; q += gridDim.x * kThreads) {
     const uint32_t k = raylist[q];
@@ -1372,7 +1496,20 @@ __global__ void __launch_bounds__(kThreads)
     walk(a.g, a.o, px[k], py[k], [&](uint32_t c, double te, double tn, bool vertical) {
       if (cls[c] != kClsCandidate) return;
       if (kstar[c] > static_cast<int32_t>(ray_base + k)) return;
-      boundMin(L, c, rayHeight(a.o[2], dz, te, tn, vertical));
+      const double h = rayHeight(a.o[2], dz, te, tn, vertical);
+      if (kScratch) {
+        unsigned long long* addr = reinterpret_cast<unsigned long long*>(ub2 + c);
+        double cur = ub2[c];
+        while (h < cur) {
+          const unsigned long long want = static_cast<unsigned long long>(__double_as_longlong(cur));
+          const unsigned long long got =
+              atomicCAS(addr, want, static_cast<unsigned long long>(__double_as_longlong(h)));
+          if (got == want) break;
+          cur = __longlong_as_double(static_cast<long long>(got));
+        }
+      } else {
+        boundMin(L, c, h);
+      }
     });
   }
 }
@@ -1393,6 +1530,12 @@ struct CellArgs {
   // zero already unless a snapshot was loaded or a conv-net frame wrote the
   // traversability of every cell, so this runs only after those.
   int scrub;
+  // Ray-cast cleanup of this frame folded in (reference raycast.cpp:132-157,
+  // grid.cpp:126-137): cells with k* < inf are removed here, their upper bound
+  // taken from pass 2's scratch (ub2, reset to +inf after use).
+  int fold_remove;
+  const int32_t* kstar;
+  double* ub2;
 };
 
 constexpr int kTileX = 32, kTileY = 8;
@@ -1407,6 +1550,7 @@ __device__ __forceinline__ uint8_t stageCell(const Layers& L, const CellArgs& a,
   if (rr < 0 || rr >= a.g.H || cc < 0 || cc >= a.g.W) return 0;
   const size_t j = static_cast<size_t>(rr) * a.g.W + cc;
   uint8_t v = L.valid[j];
+  if (v && a.fold_remove && a.kstar[j] != INT_MAX) v = 0;  // removed by the ray pass
   if (v) {
     e = L.elev[j];
     if (a.overlap) {
@@ -1449,7 +1593,8 @@ template <int RT, typename Win>
 __device__ __forceinline__ void cellBody(const Layers& L, const CellArgs& a, int r, int c,
                                          const Win& w, int32_t* __restrict__ count,
                                          uint32_t* __restrict__ seg_start,
-                                         unsigned long long& cleared) {
+                                         unsigned long long& cleared,
+                                         unsigned long long& removed) {
   const int W = a.g.W, H = a.g.H;
   const size_t i = static_cast<size_t>(r) * W + c;
   const int32_t cnt_i = count[i];
@@ -1459,7 +1604,16 @@ __device__ __forceinline__ void cellBody(const Layers& L, const CellArgs& a, int
   }
   const bool was_valid = L.valid[i] != 0;
   const bool ok = w.ok(0, 0);
-  if (was_valid && !ok) {
+  if (a.fold_remove && a.kstar[i] != INT_MAX) {  // removed by the ray pass
+    invalidateCell(L, i);
+    const double b = a.ub2[i];
+    if (b < dinf()) {  // bounds from rays at or after the removing one
+      L.ub[i] = b;
+      L.ubv[i] = 1;
+      a.ub2[i] = dinf();
+    }
+    removed = 1;
+  } else if (was_valid && !ok) {
     invalidateCell(L, i);
     cleared = 1;
   } else if (ok) {
@@ -1551,12 +1705,16 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   }
   __syncthreads();
   const int r = blockIdx.y * kTileY + threadIdx.y, c = blockIdx.x * kTileX + threadIdx.x;
-  unsigned long long cleared = 0;
+  unsigned long long cleared = 0, removed = 0;
   if (r < H && c < W)
-    cellBody<RT>(L, a, r, c, TileWin{se, sv, tw, static_cast<int>(threadIdx.y) + halo, static_cast<int>(threadIdx.x) + halo}, count,
-                 seg_start, cleared);
+    cellBody<RT>(L, a, r, c,
+                 TileWin{se, sv, tw, static_cast<int>(threadIdx.y) + halo,
+                         static_cast<int>(threadIdx.x) + halo},
+                 count, seg_start, cleared, removed);
   cleared = warpSum(cleared);
+  removed = warpSum(removed);
   if ((tid & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
+  if ((tid & 31) == 0 && removed) atomicAdd(&st->removed, removed);
 }
 
 // Same cell phases without the tile, for traversability windows too large to
@@ -1566,10 +1724,12 @@ __global__ void __launch_bounds__(256)
                    CellArgs a, DevStats* st) {
   pdlEnter();
   const int r = blockIdx.y, c = blockIdx.x * 256 + threadIdx.x;
-  unsigned long long cleared = 0;
-  if (c < a.g.W) cellBody<0>(L, a, r, c, GlobalWin{&L, &a, r, c}, count, seg_start, cleared);
+  unsigned long long cleared = 0, removed = 0;
+  if (c < a.g.W) cellBody<0>(L, a, r, c, GlobalWin{&L, &a, r, c}, count, seg_start, cleared, removed);
   cleared = warpSum(cleared);
+  removed = warpSum(removed);
   if ((threadIdx.x & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
+  if ((threadIdx.x & 31) == 0 && removed) atomicAdd(&st->removed, removed);
 }
 
 
@@ -1627,6 +1787,15 @@ struct Frame {
   // Index of this process's first ray in the point arrays (a group rank's
   // rays sit at their frame indices; shard and single frames start at 0).
   uint32_t ray_at = 0;
+  // Device scalar holding this frame's drift offset, applied by k_fuse (null:
+  // none, or applied already -- the sharded path's k_apply_offset_value).
+  const double* fuse_offset = nullptr;
+  bool classified = false;  // k_fuse wrote this frame's ray classes
+  // Removal of k* < inf cells: in k_cells (fold_remove, set when the ray pass
+  // ran with cleanup on), or by k_remove right after the ray pass
+  // (explicit_remove: sharded frames, whose host exchanges the bounds after it).
+  bool fold_remove = false;
+  bool explicit_remove = false;
   int heavy = INT_MAX;
   Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
       : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
@@ -1746,7 +1915,7 @@ SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
 // lo: frame index of the first of the N points (a group rank's batch; its
 // outputs land at frame indices lo .. lo+N-1).
 void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, bool count_cells,
-                 bool chunked = false, uint32_t lo = 0) {
+                 bool chunked = false, uint32_t lo = 0, bool finalize_drift = false) {
   if (N == 0) return;
   DeviceMap& m = f.m;
   const UpdateParams& U = f.P.update;
@@ -1766,6 +1935,17 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   ia.sigma_p_min2 = U.noise.sigma_p_min2;
   ia.drift_enabled = f.P.drift.enabled;
   ia.drift_thr = f.P.drift.traversability_threshold;
+// The drift vote reduced by the last ingest block instead of k_drift_finalize:
+// off by default -- the per-block completion atomics on one counter cost the
+// ingest more than the one-block finalize kernel (C4: ingest 19 -> 29 us).
+#ifndef RB_INGEST_FINALIZE
+#define RB_INGEST_FINALIZE 0
+#endif
+  ia.drift_blocks = (RB_INGEST_FINALIZE && finalize_drift && f.P.drift.enabled) ? gridFor(N) : 0u;
+  ia.drift_min_points = f.P.drift.min_points;
+  ia.drift_max_off = f.P.drift.max_offset_per_scan;
+  ia.drift_offset = m.drift_offset;
+  if (ia.drift_blocks) f.fuse_offset = m.drift_offset;  // applied by k_fuse (phaseSortFuse)
   const uint32_t chunk = chunked ? chunkPoints(N) : N;
   for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
     if (chunked) checkCuda(cudaStreamWaitEvent(f.s, m.ev_chunk[c], 0), "stream wait");
@@ -1775,6 +1955,35 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
               lo + base, lo);
     ++f.launches;
   }
+}
+
+RayArgs rayArgs(const Frame& f) {
+  RayArgs ra;
+  ra.g = f.g;
+  for (int i = 0; i < 3; ++i) ra.o[i] = f.pose.t[i];
+  ra.now = f.stamp;
+  ra.t_free = f.P.cleanup.t_free;
+  ra.alpha_n = f.P.cleanup.alpha_n;
+  ra.cleanup = f.P.cleanup.cleanup_enabled;
+  ra.bound = f.P.cleanup.upper_bound_enabled;
+  const GridArgs& g = f.g;
+  ra.origin_in = ra.o[0] >= g.ox && ra.o[0] <= g.xmax && ra.o[1] >= g.oy && ra.o[1] <= g.ymax;
+  auto clampc = [](int v, int n) { return v < 0 ? 0 : (v > n - 1 ? n - 1 : v); };
+  ra.ocol = clampc(x86_to_int(std::floor((ra.o[0] - g.ox) / g.res)), g.W);
+  ra.orow = clampc(x86_to_int(std::floor((ra.o[1] - g.oy) / g.res)), g.H);
+  return ra;
+}
+
+// Drift vote mean of a single-GPU frame (unless the ingest's last block
+// reduced it); the offset itself is applied before the fold (phaseSortFuse).
+void phaseDrift(Frame& f, uint32_t N) {
+  DeviceMap& m = f.m;
+  if (N == 0 || !f.P.drift.enabled || f.fuse_offset != nullptr) return;
+  launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part,
+            static_cast<int>(gridFor(N)), f.P.drift.min_points, f.P.drift.max_offset_per_scan,
+            m.drift_offset, m.stats);
+  ++f.launches;
+  f.fuse_offset = m.drift_offset;
 }
 
 // K2 over N keys (cells; >= WH = not sorted) with payload (z, var) indexed
@@ -1830,9 +2039,29 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
   f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
   f.heavy = f.overlap ? kHeavyCell : INT_MAX;
-  launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv, fa,
-                                               m.stats, f.heavy, m.heavy, m.heavy + f.ncell);
+// Drift offset and ray classification as their own sweeps (default) or inside
+// k_fuse: k_fuse runs at low occupancy (fold registers), so per-cell work for
+// every cell there costs more than a separate streaming sweep (C4 frame +11 /
+// +50 us measured).
+#ifndef RB_FUSE_OFFSET
+#define RB_FUSE_OFFSET 0
+#endif
+#ifndef RB_FUSE_CLASSIFY
+#define RB_FUSE_CLASSIFY 0
+#endif
+  if (!RB_FUSE_OFFSET && f.fuse_offset != nullptr) {
+    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, f.fuse_offset);
+    ++f.launches;
+    f.fuse_offset = nullptr;
+  }
+  const RayArgs ra = rayArgs(f);
+  const bool classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound);
+  launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv,
+            fa, m.stats, f.heavy, m.heavy, m.heavy + f.ncell, f.fuse_offset, classify ? 1 : 0,
+            ClassArgs{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W}, m.cls, m.probe, m.kstar);
   ++f.launches;
+  f.fuse_offset = nullptr;
+  f.classified = classify;
   f.fa = fa;
   // (Launching it after k_classify instead, to keep that kernel boundary programmatic, made
   // the frame 15 % slower: the side-stream blocks then queue behind the ray pass.)
@@ -1840,22 +2069,6 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   RB_PHASE_EVENT(5, s);  // fusion done (short cells when overlapped)
 }
 
-RayArgs rayArgs(const Frame& f) {
-  RayArgs ra;
-  ra.g = f.g;
-  for (int i = 0; i < 3; ++i) ra.o[i] = f.pose.t[i];
-  ra.now = f.stamp;
-  ra.t_free = f.P.cleanup.t_free;
-  ra.alpha_n = f.P.cleanup.alpha_n;
-  ra.cleanup = f.P.cleanup.cleanup_enabled;
-  ra.bound = f.P.cleanup.upper_bound_enabled;
-  const GridArgs& g = f.g;
-  ra.origin_in = ra.o[0] >= g.ox && ra.o[0] <= g.xmax && ra.o[1] >= g.oy && ra.o[1] <= g.ymax;
-  auto clampc = [](int v, int n) { return v < 0 ? 0 : (v > n - 1 ? n - 1 : v); };
-  ra.ocol = clampc(x86_to_int(std::floor((ra.o[0] - g.ox) / g.res)), g.W);
-  ra.orow = clampc(x86_to_int(std::floor((ra.o[1] - g.oy) / g.res)), g.H);
-  return ra;
-}
 
 // K5 pass 1 over this process's rays (ids ray_base + k), joined with the
 // long-cell fold (and redone if a speculated class was wrong).
@@ -1864,9 +2077,11 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
   cudaStream_t s = f.s;
   const RayArgs ra = rayArgs(f);
   if (ra.cleanup || ra.bound) {
-    launchPdl(k_classify, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
-                                                        f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
-    ++f.launches;
+    if (!f.classified) {
+      launchPdl(k_classify, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, ra, m.cls, m.kstar,
+                m.count, f.overlap ? f.heavy : -1, 0, m.stats, m.probe);
+      ++f.launches;
+    }
     if (N > 0) {
       launchPdl(k_rays_pass1<false>, gridFor(N, kP1Threads), kP1Threads, 0, s, N, m.kept + f.ray_at,
                 m.px + f.ray_at, m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar,
@@ -1878,8 +2093,8 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
     // Join the long-cell fold; redo the ray pass only if a heavy cell fused
     // nothing (both kernels return immediately otherwise).
     checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
-    launchPdl(k_classify, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, ra, m.cls, m.kstar, m.count,
-                                                        -1, 1, m.stats, m.probe);
+    launchPdl(k_classify, 148u * 4u, kThreads, 0, s, m.cur, f.ncell, ra, m.cls, m.kstar, m.count, -1, 1,
+              m.stats, m.probe);  // one wave: a no-op unless a speculation failed
     ++f.launches;
     if (N > 0) {
       launchPdl(k_rays_pass1<true>, std::min(gridFor(N, kP1Threads), 148u * RB_PASS1_MIN_BLOCKS),
@@ -1897,11 +2112,20 @@ void phaseRemovePass2(Frame& f, uint32_t ray_base) {
   DeviceMap& m = f.m;
   const RayArgs ra = rayArgs(f);
   if (!ra.cleanup) return;
-  launchPdl(k_remove, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.kstar, m.stats);
-  ++f.launches;
+  if (f.explicit_remove) {
+    launchPdl(k_remove, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.kstar, m.stats);
+    ++f.launches;
+    if (ra.bound) {
+      launchPdl(k_rays_pass2<false>, 148 * 8, kThreads, 0, f.s, m.raylist, m.stats, m.px + f.ray_at,
+                m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar, ray_base, m.ub2);
+      ++f.launches;
+    }
+    return;
+  }
+  f.fold_remove = true;  // k_cells removes the k* < inf cells
   if (ra.bound) {
-    launchPdl(k_rays_pass2, 148 * 8, kThreads, 0, f.s, m.raylist, m.stats, m.px + f.ray_at,
-              m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar, ray_base);
+    launchPdl(k_rays_pass2<true>, 148 * 8, kThreads, 0, f.s, m.raylist, m.stats, m.px + f.ray_at,
+              m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar, ray_base, m.ub2);
     ++f.launches;
   }
 }
@@ -1931,6 +2155,9 @@ void phaseCells(Frame& f) {
   ca.growth = U.sigma_t2 * (f.dt / U.nominal_update_period);
   ca.sigma_max2 = U.sigma_max2;
   ca.scrub = m.scrub_invalid ? 1 : 0;
+  ca.fold_remove = f.fold_remove ? 1 : 0;
+  ca.kstar = m.kstar;
+  ca.ub2 = m.ub2;
   const int halo = std::max(1, ca.radius);
   const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
   if (sm > kCellsMaxSmem) {  // window too large for a shared-memory tile
@@ -2098,15 +2325,9 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // count[] is all zero here: k_cells clears it after its last use each scan.
   const SortGeom sg = phaseSortGeometry(f, N);
   RB_PHASE_EVENT(1, f.s);  // resets done
-  phaseIngest(f, d_xyz, N, sg, true, chunked);
+  phaseIngest(f, d_xyz, N, sg, true, chunked, 0, true);
   RB_PHASE_EVENT(2, f.s);  // ingest done
-  if (n > 0 && P.drift.enabled) {
-    launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
-                                          P.drift.min_points, P.drift.max_offset_per_scan,
-                                          m.drift_offset, m.stats);
-    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
-    f.launches += 2;
-  }
+  phaseDrift(f, N);
   RB_PHASE_EVENT(3, f.s);  // drift done
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
@@ -2217,16 +2438,10 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   if (n > 0) checkCuda(cudaStreamWaitEvent(f.s, m.ev_copied[slot], 0), "stream wait");
   checkCuda(cudaEventRecord(m.ev_start[slot], f.s), "event");
   RB_PHASE_EVENT(1, f.s);
-  phaseIngest(f, d_xyz, N, sg, true);
+  phaseIngest(f, d_xyz, N, sg, true, false, 0, true);
   checkCuda(cudaEventRecord(m.ev_consumed[slot], f.s), "event");
   RB_PHASE_EVENT(2, f.s);
-  if (n > 0 && P.drift.enabled) {
-    launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part, static_cast<int>(gridFor(n)),
-                                          P.drift.min_points, P.drift.max_offset_per_scan,
-                                          m.drift_offset, m.stats);
-    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
-    f.launches += 2;
-  }
+  phaseDrift(f, N);
   RB_PHASE_EVENT(3, f.s);
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
@@ -2403,6 +2618,7 @@ int64_t shardRemove(DeviceMap& m, ShardIO& io) {
   checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
   Frame f(m, st.params, st.pose, st.stamp, st.dt);
   f.g = gridArgs(m.grid);
+  f.explicit_remove = true;
   phaseRemovePass2(f, st.ray_base);
   unsigned long long removed = 0;
   checkCuda(cudaMemcpyAsync(&m.h_stats->removed, &m.stats->removed, sizeof(removed),
@@ -2544,12 +2760,12 @@ void groupPhaseUpdate(GroupFrame& gf, std::vector<XBuf>& reduces) {
   checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
   const uint32_t N = static_cast<uint32_t>(g.n_total);
   if (N == 0) return;
-  if (P.drift.enabled) {
+  if (P.drift.enabled) {  // the gathered partials are the single-GPU frame's
     launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part,
               static_cast<int>(gridFor(N)), P.drift.min_points, P.drift.max_offset_per_scan,
               m.drift_offset, m.stats);
-    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, f.s, m.cur, f.ncell, m.drift_offset);
-    f.launches += 2;
+    ++f.launches;
+    f.fuse_offset = m.drift_offset;  // applied by k_fuse
   }
   RB_PHASE_EVENT(3, f.s);
   launchPdl(k_records_count, gridFor(N), kThreads, 0, f.s, m.key0, N, m.count, gf.sg.tc,
@@ -2559,7 +2775,9 @@ void groupPhaseUpdate(GroupFrame& gf, std::vector<XBuf>& reduces) {
   f.point_cells = gf.sg.passes <= 2 ? m.key0 + g.lo : nullptr;
   f.ray_at = g.lo;
   phaseRaysPass1(f, g.n_local, g.lo);
-  if (P.cleanup.cleanup_enabled) reduces.push_back({m.kstar, f.ncell, XType::kI32, XOp::kMin});
+  if (P.cleanup.cleanup_enabled) {
+    reduces.push_back({m.kstar - 1, f.ncell + 1, XType::kI32, XOp::kMin});  // + the removal flag
+  }
   if (P.cleanup.upper_bound_enabled) {
     reduces.push_back({m.cur.ub, f.ncell, XType::kF64, XOp::kMin});
     reduces.push_back({m.cur.ubv, f.ncell, XType::kU8, XOp::kMax});
@@ -2574,10 +2792,8 @@ void groupPhaseRemove(GroupFrame& gf, std::vector<XBuf>& reduces) {
   checkCuda(cudaSetDevice(m.device), "cudaSetDevice");
   if (gf.geo.n_total == 0) return;
   phaseRemovePass2(f, gf.geo.lo);
-  if (gf.P.cleanup.cleanup_enabled && gf.P.cleanup.upper_bound_enabled) {
-    reduces.push_back({m.cur.ub, f.ncell, XType::kF64, XOp::kMin});
-    reduces.push_back({m.cur.ubv, f.ncell, XType::kU8, XOp::kMax});
-  }
+  if (gf.P.cleanup.cleanup_enabled && gf.P.cleanup.upper_bound_enabled)
+    reduces.push_back({m.ub2, f.ncell, XType::kF64, XOp::kMin});  // bounds of removed cells
   RB_PHASE_EVENT(6, f.s);
 }
 
