@@ -101,25 +101,30 @@ __device__ __forceinline__ void invalidateCell(const Layers& L, size_t i) {
 
 // ------------------------------------------------------------- K4a shift
 // out[r][c] = in[r+dr][c+dc], exposed cells get the fresh fill
-// (reference grid.cpp:70-111).
-__global__ void __launch_bounds__(kThreads) k_shift(Layers in, Layers out, int W, int H, int dc,
-                                                    int dr) {
-  const size_t n = static_cast<size_t>(W) * H;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / W);
-    const int c = static_cast<int>(i - static_cast<size_t>(r) * W);
-    const int sr = r + dr, sc = c + dc;
-    if (sr >= 0 && sr < H && sc >= 0 && sc < W) {
-      const size_t j = static_cast<size_t>(sr) * W + sc;
-      out.elev[i] = in.elev[j];
-      out.var[i] = in.var[j];
-      out.last[i] = in.last[j];
-      out.ub[i] = in.ub[j];
-      out.trav[i] = in.trav[j];
-      out.nx[i] = in.nx[j];
-      out.ny[i] = in.ny[j];
-      out.nz[i] = in.nz[j];
+// (reference grid.cpp:70-111). One block row per map row (blockIdx.y), the
+// columns across the block's threads: no per-element division, 32-bit
+// offsets, every layer read and written along contiguous row segments.
+constexpr int kShiftThreads = 256;
+__global__ void __launch_bounds__(kShiftThreads) k_shift(Layers in, Layers out, int W, int H, int dc,
+                                                         int dr) {
+  const int r = blockIdx.y;
+  const int sr = r + dr;
+  const bool row_in = sr >= 0 && sr < H;
+  const size_t ro = static_cast<size_t>(r) * W;
+  const size_t so = static_cast<size_t>(row_in ? sr : 0) * W;
+  for (int c = blockIdx.x * kShiftThreads + threadIdx.x; c < W; c += gridDim.x * kShiftThreads) {
+    const int sc = c + dc;
+    const size_t i = ro + c;
+    if (row_in && sc >= 0 && sc < W) {
+      const size_t j = so + sc;
+      out.elev[i] = __ldcs(in.elev + j);
+      out.var[i] = __ldcs(in.var + j);
+      out.last[i] = __ldcs(in.last + j);
+      out.ub[i] = __ldcs(in.ub + j);
+      out.trav[i] = __ldcs(in.trav + j);
+      out.nx[i] = __ldcs(in.nx + j);
+      out.ny[i] = __ldcs(in.ny + j);
+      out.nz[i] = __ldcs(in.nz + j);
       out.valid[i] = in.valid[j];
       out.ubv[i] = in.ubv[j];
     } else {
@@ -136,6 +141,13 @@ __global__ void __launch_bounds__(kThreads) k_shift(Layers in, Layers out, int W
     }
   }
 }
+
+// The drift vote reduced by the last ingest block instead of k_drift_finalize:
+// off by default -- the per-block completion atomics on one counter cost the
+// ingest more than the one-block finalize kernel (C4: ingest 19 -> 29 us).
+#ifndef RB_INGEST_FINALIZE
+#define RB_INGEST_FINALIZE 0
+#endif
 
 // ------------------------------------------------------ drift reduction
 // Mean error over the votes and the clamped offset (reference drift.cpp:24-55,
@@ -251,11 +263,38 @@ __global__ void __launch_bounds__(kThreads)
   int oor = 0, exc = 0, oom = 0, dn = 0;
   double ds = 0.0;
   uint32_t cell = WH;
+  // The block's 256 points (6 KB of x y z) come in as 16-byte vector loads
+  // into shared memory (every byte fetched once, full sectors), then each
+  // thread reads its own triple; a misaligned caller pointer reads directly.
+  __shared__ double2 s_xyz[3 * kThreads / 2];
+  const uint32_t k0 = k_base + blockIdx.x * kThreads;
+  const double* blk = xyz + 3 * static_cast<size_t>(k0 - in_base);
+  const bool staged = (reinterpret_cast<uintptr_t>(blk) & 15u) == 0;
+  if (staged) {
+    const uint32_t nb = k0 < n ? min(static_cast<uint32_t>(kThreads), n - k0) : 0u;
+    const double2* src = reinterpret_cast<const double2*>(blk);
+    for (uint32_t q = threadIdx.x; 2 * q < 3 * nb; q += kThreads) {
+      if (2 * q + 1 < 3 * nb) {
+        s_xyz[q] = __ldcs(src + q);
+      } else {
+        s_xyz[q].x = __ldcs(blk + 2 * q);  // odd tail: the last double alone
+      }
+    }
+    __syncthreads();
+  }
   if (k < n) {
-    const size_t ki = 3 * static_cast<size_t>(k - in_base);
-    const double x = xyz[ki];
-    const double y = xyz[ki + 1];
-    const double z = xyz[ki + 2];
+    double x, y, z;
+    if (staged) {
+      const double* sp = reinterpret_cast<const double*>(s_xyz) + 3 * threadIdx.x;
+      x = sp[0];
+      y = sp[1];
+      z = sp[2];
+    } else {
+      const size_t ki = 3 * static_cast<size_t>(k - in_base);
+      x = xyz[ki];
+      y = xyz[ki + 1];
+      z = xyz[ki + 2];
+    }
     const double sq = (x * x + y * y) + z * z;
     bool keep = false;
     if (sq > a.max_range2) {
@@ -342,6 +381,7 @@ __global__ void __launch_bounds__(kThreads)
     if (c2) atomicAdd(&st->excluded, static_cast<unsigned long long>(c2));
     if (c3) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c3));
   }
+#if RB_INGEST_FINALIZE
   if (a.drift_blocks == 0) return;
   // The last block of the frame's ingest (over all chunk launches) reduces the
   // partials: no separate finalize launch.
@@ -355,6 +395,7 @@ __global__ void __launch_bounds__(kThreads)
   __threadfence();
   driftFinalizeBlock(drift_part, drift_npart, static_cast<int>(a.drift_blocks), a.drift_min_points,
                      a.drift_max_off, a.drift_offset, st);
+#endif
 }
 
 // ------------------------------------------------------ drift (one block)
@@ -1812,7 +1853,9 @@ void phaseBegin(Frame& f, bool record_start = true) {
   if (sx != 0 || sy != 0) {
     m.grid.center_x += sx * m.grid.resolution;
     m.grid.center_y += sy * m.grid.resolution;
-    k_shift<<<streamGrid(f.ncell), kThreads, 0, f.s>>>(m.cur, m.alt, m.grid.width, m.grid.height, sx, sy);
+    const int W = m.grid.width, H = m.grid.height;
+    k_shift<<<dim3(std::min((W + kShiftThreads - 1) / kShiftThreads, 4), H), kShiftThreads, 0, f.s>>>(
+        m.cur, m.alt, W, H, sx, sy);
     ++f.launches;
     std::swap(m.cur, m.alt);
   }
@@ -1935,12 +1978,6 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   ia.sigma_p_min2 = U.noise.sigma_p_min2;
   ia.drift_enabled = f.P.drift.enabled;
   ia.drift_thr = f.P.drift.traversability_threshold;
-// The drift vote reduced by the last ingest block instead of k_drift_finalize:
-// off by default -- the per-block completion atomics on one counter cost the
-// ingest more than the one-block finalize kernel (C4: ingest 19 -> 29 us).
-#ifndef RB_INGEST_FINALIZE
-#define RB_INGEST_FINALIZE 0
-#endif
   ia.drift_blocks = (RB_INGEST_FINALIZE && finalize_drift && f.P.drift.enabled) ? gridFor(N) : 0u;
   ia.drift_min_points = f.P.drift.min_points;
   ia.drift_max_off = f.P.drift.max_offset_per_scan;

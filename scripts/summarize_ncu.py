@@ -44,11 +44,20 @@ def main(rep, launches, tag):
             return None
 
     stall_cols = [n for n in h if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
+    peaks = ROOT / "MEASURED_PEAKS.json"
+    hbm = json.loads(peaks.read_text()).get("hbm_gbs", 6450.3) if peaks.exists() else 6450.3
     lines = [f"# ncu summary ({tag})", "",
              f"Source: `{Path(rep).name}` (`ncu --set full --clock-control none --import-source on`, one GPU). "
-             "Per-launch times here are cold-cache and serialised; compare shares, not absolutes.", "",
-             "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM GB/s | achieved occupancy % | IPC | regs | top stalls (samples) |",
-             "|---|---|---|---|---|---|---|---|---|"]
+             "Per-launch times here are cold-cache and serialised; compare shares, not absolutes.",
+             f"HBM % = (dram__bytes_read.sum + dram__bytes_write.sum) / duration against the measured "
+             f"{hbm:.0f} GB/s copy peak (MEASURED_PEAKS.json). lanes = smsp__thread_inst_executed_per_inst_executed"
+             ".ratio / 32 (SIMT lane efficiency). L2 atomics = lts__t_requests_srcunit_tex_op_atom_dot_alu + _cas + "
+             "op_red (requests reaching L2; warp-aggregated atomics count once per warp), their rate, and "
+             "lts__d_atomic_input_cycles_active (% of the L2 atomic units' peak). L2 GB/s = lts__t_sectors.sum x 32 B / "
+             "duration: all traffic through L2, which is where a frame's intermediates live (126 MB L2).", "",
+             "| kernel | duration us | DRAM read MB | DRAM write MB | DRAM GB/s | HBM % | L2 GB/s | occupancy % | IPC | "
+             "lanes | regs | L2 atomics | atomics/s | L2 atomic unit % | top stalls (samples) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = defaultdict(list)
     for r in rows:
         k = r[col["Kernel Name"]].split("(")[0].split("::")[-1]
@@ -61,7 +70,15 @@ def main(rep, launches, tag):
         stalls = sorted(((val(r, n) or 0.0, n.replace("smsp__pcsamp_warps_issue_stalled_", "")) for n in stall_cols),
                         reverse=True)[:3]
         bw = (rd + wr) * 1e6 / (dur * 1e-6) / 1e9 if dur and rd is not None else None
-        lines.append(f"| {k} | {dur:.1f} | {rd:.2f} | {wr:.2f} | {bw:.0f} | {occ:.1f} | {ipc:.2f} | {regs:.0f} | "
+        lanes = (val(r, "smsp__thread_inst_executed_per_inst_executed.ratio") or 0.0) / 32.0
+        atom = sum(val(r, n) or 0.0 for n in ("lts__t_requests_srcunit_tex_op_atom_dot_alu.sum",
+                                             "lts__t_requests_srcunit_tex_op_atom_dot_cas.sum",
+                                             "lts__t_requests_srcunit_tex_op_red.sum"))
+        aunit = val(r, "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed") or 0.0
+        arate = atom / (dur * 1e-6) if dur else 0.0
+        l2 = (val(r, "lts__t_sectors.sum") or 0.0) * 32 / (dur * 1e-6) / 1e9 if dur else 0.0
+        lines.append(f"| {k} | {dur:.1f} | {rd:.2f} | {wr:.2f} | {bw:.0f} | {100 * bw / hbm:.1f} | {l2:.0f} | {occ:.1f} | "
+                     f"{ipc:.2f} | {lanes:.2f} | {regs:.0f} | {atom:.0f} | {arate:.2e} | {aunit:.1f} | "
                      + ", ".join(f"{n} {v:.0f}" for v, n in stalls) + " |")
         base = k.split("<")[0]  # template instances (k_rays_pass1<0>/<1>)
         if base in GROUP:

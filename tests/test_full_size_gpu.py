@@ -9,6 +9,7 @@ path of the ray pass runs at full size too.
 """
 from __future__ import annotations
 
+import numpy as np
 import pytest
 
 import paper_2204_12876_b200 as pk
@@ -62,3 +63,37 @@ def test_c2_four_cameras_per_frame(gpu, reference, tmp_path):
 def test_c2_four_cameras_bit_exact_with_removals(gpu, reference, tmp_path):
     t = _run(gpu, reference, tmp_path, wl.c2(), 3, extra="drift.enabled = false\n", stamp_step=1.2)
     assert t["points_fused"] > 0
+
+
+def test_headline_full_size_bit_exact(gpu, reference, tmp_path):
+    """The north star's own config: 1,000,064 points into 500x500 (rays clipped at the map border
+    at full density), drift off, stamps 1.2 s apart so removal candidates are live."""
+    t = _run(gpu, reference, tmp_path, wl.headline(), 3, extra="drift.enabled = false\n", stamp_step=1.2)
+    assert t["points_fused"] > 1_000_000
+
+
+def test_headline_full_size_defaults(gpu, reference, tmp_path):
+    _run(gpu, reference, tmp_path, wl.headline(), 2, drift_tol=1e-12, height_tol=1e-9)
+
+
+def test_overlap_clearance_fires_full_size(gpu, reference, tmp_path):
+    """Overlap clearance (analysis.cpp:296-317) must actually clear cells: C3 frames with the
+    sensor at 1 m build the map, then the robot rises to 3.2 m (a second floor / elevator), so
+    valid ground cells within the (2 m) radius sit more than 1.5 m below it and are invalidated."""
+    w = wl.c3()
+    cfg_path = tmp_path / "ov.config"
+    cfg_path.write_text(w.config_text + "drift.enabled = false\noverlap.radius = 2.0\n")
+    libs = (gpu, reference)
+    cfgs = [pk.Config.load(lib, cfg_path) for lib in libs]
+    maps = [pk.ReliefMap.create(lib, w.resolution, w.width, w.height) for lib in libs]
+    cleared = 0
+    for f in range(4):
+        z = 1.0 if f < 3 else 3.2
+        pose = wl.pose34(np.eye(3), (0.0, 0.0, z))
+        xyz = ref_render(reference, cfg_path, pose, 0.1 * f, 3, f)
+        got = maps[0].integrate(xyz, pose, 0.1 * f, cfgs[0])
+        want = maps[1].integrate(xyz, pose, 0.1 * f, cfgs[1])
+        assert_stats_match(got, want, context=f"frame {f}")
+        assert_layers_match(maps[0].layers(), maps[1].layers(), context=f"frame {f}")
+        cleared += got.cells_cleared_by_overlap
+    assert cleared > 100, cleared
