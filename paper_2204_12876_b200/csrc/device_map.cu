@@ -57,11 +57,12 @@ void carveLayers(Carver& c, Layers& L, std::size_t n) {
   L.ubv = c.take<uint8_t>(n);
 }
 
-// Probe words of the padded grid: the border is tag 3 ("outside the grid")
-// for good; the interior is rewritten by every frame's classification.
+// Probe words of the padded grid and its guard rows: the border is 0xffff
+// (tag 3, "outside the grid", F = NaN) for good; the interior is rewritten by
+// every frame's classification.
 __global__ void k_probe_border(uint16_t* probe, std::size_t n) {
   const std::size_t i = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
-  if (i < n) probe[i] = 3;
+  if (i < n) probe[i] = 0xffffu;
 }
 
 __global__ void k_fill_fresh(Layers L, std::size_t n, int32_t* kstar, double* ub2) {
@@ -148,7 +149,8 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
       checkCuda(cudaMallocHost(&m->h_slot[k], sizeof(DevStats)), "pinned stats");
     }
     const std::size_t n = grid.cells();
-    const std::size_t np = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2);
+    const std::size_t guard = static_cast<std::size_t>(DeviceMap::kProbeGuardRows) * (grid.width + 2);
+    const std::size_t np = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2) + 2 * guard;
     const std::size_t bytes = 2 * layerBytes(n) + 4 * alignUp(n * 4) + alignUp(np * 2) +
                               alignUp((n + 1) * 4) + alignUp(n) + alignUp(n * 8) + 8 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
@@ -160,14 +162,14 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     m->heavy = c.take<uint32_t>(2 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
-    m->probe = c.take<uint16_t>(static_cast<std::size_t>(grid.width + 2) * (grid.height + 2));
+    m->probe = c.take<uint16_t>(np) + guard;
     m->ub2 = c.take<double>(n);
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
     fillFresh(*m);
-    const std::size_t np2 = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2);
-    k_probe_border<<<static_cast<unsigned>((np2 + 255) / 256), 256, 0, m->stream>>>(m->probe, np2);
+    k_probe_border<<<static_cast<unsigned>((np + 255) / 256), 256, 0, m->stream>>>(m->probe - guard,
+                                                                                  np);
     checkCuda(cudaGetLastError(), "probe init");
     checkCuda(cudaMemsetAsync(m->count, 0, n * sizeof(int32_t), m->stream), "map init");
     checkCuda(cudaMemsetAsync(m->start, 0xff, (n + 1) * sizeof(uint32_t), m->stream), "map init");

@@ -121,7 +121,11 @@ struct DeviceMap {
   int32_t* count = nullptr;
   uint32_t* start = nullptr;
   uint8_t* cls = nullptr;
-  uint16_t* probe = nullptr;  // pass-1 probe words (class + conservative gate bound), (W+2)x(H+2)
+  // pass-1 probe words (class + conservative gate bound), (W+2)x(H+2), with
+  // kProbeGuardRows padded rows of border words before and after the grid
+  // (pass 1's run lookahead may step that far past the border)
+  uint16_t* probe = nullptr;
+  static constexpr int kProbeGuardRows = 16;
   int32_t* kstar = nullptr;
   double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)

@@ -698,25 +698,30 @@ struct RayArgs {
 // cell that fused nothing and the ray pass is then redone (retry = 1: this
 // kernel and pass 1 run only if the flag is set).
 // Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
-// above it, an f16 bound F >= T of the cell's gate threshold T (T =
-// upper_bound for a bound cell, elevation - sqrt(variance) for a removal
-// candidate), so that a visit with ray height h >= F is rejected without
-// loading the cell state: the reference's own test (h < ub, resp.
+// above it, an order-preserving key of an f16 bound F >= T of the cell's gate
+// threshold T (T = upper_bound for a bound cell, elevation - sqrt(variance)
+// for a removal candidate), so that a visit with ray height h >= F is rejected
+// without loading the cell state: the reference's own test (h < ub, resp.
 // !(h >= elev - sqrt(var))) rejects it too. F is T rounded up (double -> f32
-// -> f16) and then up again to a multiple of 4 ulps (for negative values:
-// towards zero); NaN thresholds become +inf, values beyond the f16 range +inf
-// or -65504 (both still >= T).
+// -> f16), its key (sign-flipped f16 bits: unsigned order == value order)
+// rounded up to a multiple of 4; NaN thresholds become +inf. Class "none" is
+// word 0 (below every class word) and the padded grid's border is 0xffff (its
+// F decodes to NaN, which no test passes), so the unsigned max of the words
+// of a run of cells is the word of the run's largest F (pass 1's run test).
 typedef uint16_t ProbeT;
 __device__ __forceinline__ ProbeT probeWord(uint8_t cls, double t) {
   if (cls == kClsNone) return 0u;
   // up-rounded twice (double -> f32 -> f16) stays >= t
   const __half hf = (t == t) ? __float2half_ru(__double2float_ru(t)) : __ushort_as_half(0x7c00);
-  uint32_t b = __half_as_ushort(hf);
-  b = (b >> 15) ? (b & ~3u) : ((b + 3u) & ~3u);
-  return static_cast<ProbeT>(b | cls);
+  const uint32_t b = __half_as_ushort(hf);
+  uint32_t key = (b & 0x8000u) ? (~b & 0xffffu) : (b | 0x8000u);
+  key = (key + 3u) & ~3u;  // <= 0xfc00 (+inf) for every f16 <= +inf
+  return static_cast<ProbeT>(key | cls);
 }
 __device__ __forceinline__ double probeBound(uint32_t w) {
-  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & ~3u))));
+  const uint32_t key = w & 0xfffcu;
+  const uint32_t b = (key & 0x8000u) ? (key & 0x7fffu) : (~key & 0xffffu);
+  return static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(b))));
 }
 
 // Ray class + probe word of cell i from its post-fusion state, k* reset
@@ -1302,6 +1307,10 @@ __device__ __forceinline__ void pass1Visit(const Pass1Ctx& c, uint8_t cl, uint32
   candidateVisit(c.L, idx, h, c.vx, c.vy, c.dz, c.alpha_n, c.k, c.kstar);
 }
 
+#ifndef RB_P1_RUN
+#define RB_P1_RUN 8  // cells per lookahead run in pass 1 (<= 1: the per-cell loop)
+#endif
+
 // Pass-1 walk of a ray with finite xy deltas: the traversal of walkRayFinite
 // with the class probe software-pipelined -- the next cell's class byte is
 // loaded before the current cell is handled, so the L1 latency overlaps the
@@ -1381,12 +1390,114 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     tmy = dy < 0.0 ? -q : q;
   }
   uint32_t idx = (static_cast<uint32_t>(row) + 1u) * Wp + static_cast<uint32_t>(col) + 1u;
-  unsigned nx = 0, ny = 0;
   const int step_idx_row = step_row * static_cast<int>(Wp);
   const ProbeT* __restrict__ probe = c.probe;
   pdlWait();  // class / probe words come from the classification
   uint32_t wd = probe[idx];
   double t_enter = t0;
+#if RB_P1_RUN > 1
+  // Runs of RB_P1_RUN cells. The walk (cell sequence and crossing times)
+  // does not depend on the probe words, so the next RB_P1_RUN steps are taken
+  // with their words loaded back to back (one memory latency per run instead
+  // of one per cell), and the run is committed without per-cell work when
+  // (a) it is not the ray's last (its last crossing time is < t1, so every
+  //     cell of it continues the walk: crossing times are non-decreasing), and
+  // (b) no cell of it can pass its gate: every emitted height of the run lies
+  //     between fl(oz + t*dz) at the run's first entry and last crossing time
+  //     (the height's three correctly rounded operations are monotone in the
+  //     two times, which lie in that interval), and the smaller end is >= the
+  //     largest F of the run (the max of its words: 0 = no class, border =
+  //     NaN, see probeWord) -- so every class cell would be rejected by its
+  //     probe filter.
+  // Otherwise the run is redone one cell at a time (the loop below, the
+  // reference's step). A run's lookahead may step past the border into the
+  // guard rows (DeviceMap::kProbeGuardRows), hence the signed index. A run
+  // holding a candidate cell marks the ray touched even if that cell is not
+  // emitted (the endpoint or a zero-length cell): the ray is then queued for
+  // pass 2 without reason, which changes nothing (pass 2 only acts on removed
+  // cells, all of them candidates the ray would have touched).
+  static_assert(RB_P1_RUN < DeviceMap::kProbeGuardRows, "probe guard rows");
+  const bool runs = isfinite(c.oz) && isfinite(c.dz);
+  unsigned nv = 0;
+  while (true) {
+    if (runs) {
+      double ax = tmx, ay = tmy, mlast = 0.0;
+      int j = static_cast<int>(idx);
+      uint32_t kmax = wd, kor = wd, wl = 0;
+#pragma unroll
+      for (int s = 0; s < RB_P1_RUN; ++s) {
+        // m = min, then the axis step as two predicated adds (the compiler
+        // would otherwise compute both sums and select them)
+        int dj;
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.lt.f64 p, %0, %1;\n\t"
+            "selp.f64 %2, %0, %1, p;\n\t"
+            "selp.s32 %3, %6, %7, p;\n\t"
+            "@p add.rn.f64 %0, %0, %4;\n\t"
+            "@!p add.rn.f64 %1, %1, %5;\n\t}"
+            : "+d"(ax), "+d"(ay), "=d"(mlast), "=r"(dj)
+            : "d"(tdx), "d"(tdy), "r"(step_col), "r"(step_idx_row));
+        j += dj;
+        const uint32_t w = probe[j];
+        if (s + 1 < RB_P1_RUN) {
+          kmax = max(kmax, w);
+          kor |= w;
+        } else {
+          wl = w;
+        }
+      }
+      if (mlast < t1) {
+        const double ha = c.oz + t_enter * c.dz, hb = c.oz + mlast * c.dz;
+        if (kmax == 0u || (ha < hb ? ha : hb) >= probeBound(kmax)) {
+          tmx = ax;
+          tmy = ay;
+          idx = static_cast<uint32_t>(j);
+          wd = wl;
+          t_enter = mlast;
+          nv += RB_P1_RUN;
+          if (kor & kClsCandidate) touched = true;
+          continue;
+        }
+      }
+    }
+    bool done = false;
+#pragma unroll 1
+    for (int s = 0; s < RB_P1_RUN; ++s) {
+      const bool sx = tmx < tmy;
+      const double m = sx ? tmx : tmy;  // = the reference's min (no NaN here)
+      const bool more = m < t1;
+      if ((wd & 3u) != 0) {
+        if ((wd & 3u) == 3u) {  // stepped out of the grid: stop before this cell
+          done = true;
+          break;
+        }
+        const double t_next = more ? m : t1;
+        if (idx != end_idx && t_next > t_enter) {
+          const double h = c.oz + (0.5 * (t_enter + t_next)) * c.dz;
+          const uint8_t tag = static_cast<uint8_t>(wd & 3u);
+          if (tag == kClsCandidate) touched = true;
+          if (!(h >= probeBound(wd))) {
+            const uint32_t pr = idx / Wp;
+            pass1Visit(c, tag, (pr - 1u) * W + (idx - pr * Wp - 1u), h, touched);
+          }
+        }
+      }
+      ++nv;
+      if (!more) {
+        done = true;
+        break;
+      }
+      if (sx) tmx += tdx;
+      else tmy += tdy;
+      idx += sx ? step_col : step_idx_row;
+      wd = probe[idx];
+      t_enter = m;
+    }
+    if (done) break;
+  }
+  visits += nv;
+#else
+  unsigned nx = 0, ny = 0;
   bool exited = false;
 // Unrolled by 2: the compiler renames t_enter / m across the two copies and
 // interleaves them.
@@ -1438,6 +1549,7 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
   }
   // cells iterated = steps taken + 1 (the step onto the border excluded)
   visits += nx + ny + 1u - (exited ? 1u : 0u);
+#endif
 }
 
 // 128-thread blocks, 9 per SM: 56 registers (no spills in the DDA loop) at 36

@@ -1,6 +1,7 @@
 """Builds librelief_b200.so from the csrc/ of a git revision into ab/NAME (A/B baselines).
 
 Usage: python scripts/build_ref_variant.py REV NAME [-DFOO=1 ...]
+REV = WORKTREE builds the working tree's sources (with the given defines).
 """
 import subprocess
 import sys
@@ -14,6 +15,11 @@ rev, name, defs = sys.argv[1], sys.argv[2], sys.argv[3:]
 tmp = Path(tempfile.mkdtemp())
 for sub in ("paper_2204_12876_b200/csrc", "include"):
     (tmp / sub).mkdir(parents=True)
+    if rev == "WORKTREE":
+        for f in (b.ROOT / sub).iterdir():
+            if f.is_file():
+                (tmp / sub / f.name).write_bytes(f.read_bytes())
+        continue
     files = subprocess.run(["git", "-C", str(b.ROOT), "ls-tree", "--name-only", f"{rev}:{sub}"],
                            capture_output=True, text=True, check=True).stdout.split()
     for f in files:
