@@ -55,6 +55,7 @@ struct DevStats {
   int error_code;                     // 0 ok, 1 non-positive variance
   int respeculate;                    // a heavy cell fused nothing: redo the ray pass
   unsigned int ingest_done;           // ingest blocks finished (the last one reduces the drift vote)
+  unsigned int grid_bar[2];           // k_rays_tail's grid barrier (arrivals, generation)
 };
 
 // Geometry + parameters passed by value to kernels.

@@ -58,4 +58,24 @@ void launchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem
 #endif
 }
 
+// Cooperative launch (all blocks co-resident, for a grid barrier), chained
+// like launchPdl.
+template <typename... KArgs, typename... Args>
+void launchCoopPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem,
+                   cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (RB_PDL && s != nullptr) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  checkCuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+}
+
 }  // namespace rb200

@@ -1268,10 +1268,19 @@ __device__ __forceinline__ void boundMin(const Layers& L, uint32_t c, double h) 
 
 // Removal gates for a candidate cell (reference raycast.cpp:138-150), literal
 // comparison forms; records the ray in k*.
+#ifndef RB_CAND_LAZY
+#define RB_CAND_LAZY 1
+#endif
 __device__ __forceinline__ void candidateVisit(const Layers& L, uint32_t c, double h, double vx,
                                                double vy, double vz, double alpha_n, int32_t k,
                                                int32_t* kstar) {
-  if (h >= L.elev[c] - sqrt(L.var[c])) return;
+  const double gate = L.elev[c] - sqrt(L.var[c]);
+  if (h >= gate) return;
+#if RB_CAND_LAZY
+  // the direction is normalised here, on this rare path, not hoisted into
+  // every ray's setup (the empty asm makes it depend on the cell)
+  asm("" : "+d"(vx), "+d"(vy), "+d"(vz) : "d"(gate));
+#endif
   const double n2 = (vx * vx + vy * vy) + vz * vz;
   double ux = vx, uy = vy, uz = vz;
   if (n2 > 0.0) {
@@ -1307,14 +1316,21 @@ __device__ __forceinline__ void pass1Visit(const Pass1Ctx& c, uint8_t cl, uint32
   candidateVisit(c.L, idx, h, c.vx, c.vy, c.dz, c.alpha_n, c.k, c.kstar);
 }
 
+#ifdef RB_P1_DIAG
+__device__ unsigned long long g_p1diag[5];
+__global__ void k_p1diag() {
+  printf("P1DIAG fast_runs %llu end_runs %llu gate_runs %llu rays %llu cells %llu\n", g_p1diag[0],
+         g_p1diag[1], g_p1diag[2], g_p1diag[3], g_p1diag[4]);
+  for (int i = 0; i < 5; ++i) g_p1diag[i] = 0;
+}
+#endif
 #ifndef RB_P1_RUN
-#define RB_P1_RUN 8  // cells per lookahead run in pass 1 (<= 1: the per-cell loop)
+#define RB_P1_RUN 8  // cells per lookahead run in pass 1
 #endif
 
-// Pass-1 walk of a ray with finite xy deltas: the traversal of walkRayFinite
-// with the class probe software-pipelined -- the next cell's class byte is
-// loaded before the current cell is handled, so the L1 latency overlaps the
-// current visit. Visit side effects (bound min, k* min) are order independent.
+// Pass 1 of a ray with finite xy deltas, in two parts: pass1Setup (per lane:
+// the reference's clip, start / end cells and first crossing times) and
+// pass1Walk (the DDA, run by every lane of the warp together).
 //
 // Setup shortcuts, each equal to the reference's arithmetic:
 // * |dx| or |dy| >= 2e-12 implies hypot(dx, dy) >= 1e-12 (hypot is within an
@@ -1326,9 +1342,18 @@ __device__ __forceinline__ void pass1Visit(const Pass1Ctx& c, uint8_t cl, uint32
 // * the endpoint's cell is the point's cell from k_ingest (same expression
 //   floor((p - origin) / res), in range so the clamp is the identity) when
 //   that is known (pcell < W*H).
-__device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3], double px,
-                                            double py, const Pass1Ctx& c, bool& touched,
-                                            unsigned& visits, const RayArgs& a, uint32_t pcell) {
+struct P1Walk {
+  double tmx, tmy, tdx, tdy, t_enter, t1;
+  uint32_t idx, end_idx, wd;  // padded cell index, the endpoint's, the cell's probe word
+  int step_col, step_row;     // index steps (step_row = +-(W+2))
+};
+
+// Returns true when the ray has a walk left (the vertical and clipped-out
+// cases are finished here).
+__device__ __forceinline__ bool pass1Setup(const GridArgs& g, const double o[3], double px,
+                                           double py, const Pass1Ctx& c, bool& touched,
+                                           unsigned& visits, const RayArgs& a, uint32_t pcell,
+                                           P1Walk& w) {
   const double dx = px - o[0];
   const double dy = py - o[1];
   const double res = g.res;
@@ -1342,22 +1367,18 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
       const uint8_t cl = c.cls[idx];
       if (cl) pass1Visit(c, cl, idx, o[2] + 0.5 * c.dz, touched);
     }
-    return;
+    return false;
   }
   double t0 = 0.0, t1 = 1.0;
   const bool end_in = px >= g.ox && px < g.xmax && py >= g.oy && py < g.ymax;
   if (!(a.origin_in && end_in)) {
-    if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return;
-    if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return;
-    if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return;
-    if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return;
-    if (t0 >= t1) return;
+    if (!clipAxis(-dx, o[0] - g.ox, t0, t1)) return false;
+    if (!clipAxis(dx, g.xmax - o[0], t0, t1)) return false;
+    if (!clipAxis(-dy, o[1] - g.oy, t0, t1)) return false;
+    if (!clipAxis(dy, g.ymax - o[1], t0, t1)) return false;
+    if (t0 >= t1) return false;
   }
-  // The probe words live on a grid padded by one border cell on every side
-  // (tag 3): the walk leaves the grid exactly when it steps onto the border
-  // (the reference's bounds test after a step, raycast.cpp:121,125), so the
-  // loop carries no per-axis step counters and no exit test of its own.
-  const uint32_t W = static_cast<uint32_t>(g.W), Wp = W + 2u;
+  const uint32_t W = static_cast<uint32_t>(g.W), Wp = W + 2u;  // padded grid (pass1Exact)
   uint32_t end_idx = 0xffffffffu;  // padded index of the endpoint's cell
   if (end_in) {
     uint32_t er, ec;
@@ -1389,166 +1410,155 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
     div2_rn(res, (g.oy + (row + (step_row > 0 ? 1 : 0)) * res) - o[1], fabs(dy), tdy, q);
     tmy = dy < 0.0 ? -q : q;
   }
-  uint32_t idx = (static_cast<uint32_t>(row) + 1u) * Wp + static_cast<uint32_t>(col) + 1u;
-  const int step_idx_row = step_row * static_cast<int>(Wp);
-  const ProbeT* __restrict__ probe = c.probe;
-  pdlWait();  // class / probe words come from the classification
-  uint32_t wd = probe[idx];
-  double t_enter = t0;
-#if RB_P1_RUN > 1
-  // Runs of RB_P1_RUN cells. The walk (cell sequence and crossing times)
-  // does not depend on the probe words, so the next RB_P1_RUN steps are taken
-  // with their words loaded back to back (one memory latency per run instead
-  // of one per cell), and the run is committed without per-cell work when
-  // (a) it is not the ray's last (its last crossing time is < t1, so every
-  //     cell of it continues the walk: crossing times are non-decreasing), and
-  // (b) no cell of it can pass its gate: every emitted height of the run lies
-  //     between fl(oz + t*dz) at the run's first entry and last crossing time
-  //     (the height's three correctly rounded operations are monotone in the
-  //     two times, which lie in that interval), and the smaller end is >= the
-  //     largest F of the run (the max of its words: 0 = no class, border =
-  //     NaN, see probeWord) -- so every class cell would be rejected by its
-  //     probe filter.
-  // Otherwise the run is redone one cell at a time (the loop below, the
-  // reference's step). A run's lookahead may step past the border into the
-  // guard rows (DeviceMap::kProbeGuardRows), hence the signed index. A run
-  // holding a candidate cell marks the ray touched even if that cell is not
-  // emitted (the endpoint or a zero-length cell): the ray is then queued for
-  // pass 2 without reason, which changes nothing (pass 2 only acts on removed
-  // cells, all of them candidates the ray would have touched).
-  static_assert(RB_P1_RUN < DeviceMap::kProbeGuardRows, "probe guard rows");
-  const bool runs = isfinite(c.oz) && isfinite(c.dz);
-  unsigned nv = 0;
-  while (true) {
-    if (runs) {
-      double ax = tmx, ay = tmy, mlast = 0.0;
-      int j = static_cast<int>(idx);
-      uint32_t kmax = wd, kor = wd, wl = 0;
-#pragma unroll
-      for (int s = 0; s < RB_P1_RUN; ++s) {
-        // m = min, then the axis step as two predicated adds (the compiler
-        // would otherwise compute both sums and select them)
-        int dj;
-        asm("{\n\t.reg .pred p;\n\t"
-            "setp.lt.f64 p, %0, %1;\n\t"
-            "selp.f64 %2, %0, %1, p;\n\t"
-            "selp.s32 %3, %6, %7, p;\n\t"
-            "@p add.rn.f64 %0, %0, %4;\n\t"
-            "@!p add.rn.f64 %1, %1, %5;\n\t}"
-            : "+d"(ax), "+d"(ay), "=d"(mlast), "=r"(dj)
-            : "d"(tdx), "d"(tdy), "r"(step_col), "r"(step_idx_row));
-        j += dj;
-        const uint32_t w = probe[j];
-        if (s + 1 < RB_P1_RUN) {
-          kmax = max(kmax, w);
-          kor |= w;
-        } else {
-          wl = w;
-        }
-      }
-      if (mlast < t1) {
-        const double ha = c.oz + t_enter * c.dz, hb = c.oz + mlast * c.dz;
-        if (kmax == 0u || (ha < hb ? ha : hb) >= probeBound(kmax)) {
-          tmx = ax;
-          tmy = ay;
-          idx = static_cast<uint32_t>(j);
-          wd = wl;
-          t_enter = mlast;
-          nv += RB_P1_RUN;
-          if (kor & kClsCandidate) touched = true;
-          continue;
-        }
-      }
-    }
-    bool done = false;
+  w.tmx = tmx;
+  w.tmy = tmy;
+  w.tdx = tdx;
+  w.tdy = tdy;
+  w.t_enter = t0;
+  w.t1 = t1;
+  w.idx = (static_cast<uint32_t>(row) + 1u) * Wp + static_cast<uint32_t>(col) + 1u;
+  w.end_idx = end_idx;
+  w.step_col = step_col;
+  w.step_row = step_row * static_cast<int>(Wp);
+  return true;
+}
+
+// Exact cells of a walk, one at a time (the reference's step, raycast.cpp:
+// 112-129), at most `cells` of them; returns true when the walk ended. The
+// probe words live on a grid padded by one border cell on every side (word
+// 0xffff, tag 3): the walk leaves the grid exactly when it steps onto the
+// border (the reference's bounds test after a step), so the loop carries no
+// per-axis bounds tests. Only class cells leave the common path; the endpoint
+// and zero-length tests of the reference's emission (t_next > t_enter) are
+// made there, on the rare branch.
+__device__ __forceinline__ bool pass1Exact(P1Walk& w, const Pass1Ctx& c, uint32_t W,
+                                           unsigned cells, unsigned& nv, bool& touched) {
+  const uint32_t Wp = W + 2u;
 #pragma unroll 1
-    for (int s = 0; s < RB_P1_RUN; ++s) {
-      const bool sx = tmx < tmy;
-      const double m = sx ? tmx : tmy;  // = the reference's min (no NaN here)
-      const bool more = m < t1;
-      if ((wd & 3u) != 0) {
-        if ((wd & 3u) == 3u) {  // stepped out of the grid: stop before this cell
-          done = true;
-          break;
-        }
-        const double t_next = more ? m : t1;
-        if (idx != end_idx && t_next > t_enter) {
-          const double h = c.oz + (0.5 * (t_enter + t_next)) * c.dz;
-          const uint8_t tag = static_cast<uint8_t>(wd & 3u);
-          if (tag == kClsCandidate) touched = true;
-          if (!(h >= probeBound(wd))) {
-            const uint32_t pr = idx / Wp;
-            pass1Visit(c, tag, (pr - 1u) * W + (idx - pr * Wp - 1u), h, touched);
-          }
+  for (unsigned s = 0; s < cells; ++s) {
+    const bool sx = w.tmx < w.tmy;
+    const double m = sx ? w.tmx : w.tmy;  // = the reference's min (no NaN here)
+    const bool more = m < w.t1;
+    if ((w.wd & 3u) != 0) {
+      if ((w.wd & 3u) == 3u) return true;  // stepped out of the grid: stop before this cell
+      const double t_next = more ? m : w.t1;
+      if (w.idx != w.end_idx && t_next > w.t_enter) {
+        const double h = c.oz + (0.5 * (w.t_enter + t_next)) * c.dz;
+        const uint8_t tag = static_cast<uint8_t>(w.wd & 3u);
+        if (tag == kClsCandidate) touched = true;
+        // probe filter: h >= F implies the exact gate rejects (see probeWord)
+        if (!(h >= probeBound(w.wd))) {
+          const uint32_t pr = w.idx / Wp;
+          pass1Visit(c, tag, (pr - 1u) * W + (w.idx - pr * Wp - 1u), h, touched);
         }
       }
-      ++nv;
-      if (!more) {
-        done = true;
-        break;
-      }
-      if (sx) tmx += tdx;
-      else tmy += tdy;
-      idx += sx ? step_col : step_idx_row;
-      wd = probe[idx];
-      t_enter = m;
     }
-    if (done) break;
+    ++nv;
+    if (!more) return true;
+    if (sx) w.tmx += w.tdx;
+    else w.tmy += w.tdy;
+    w.idx += sx ? w.step_col : w.step_row;
+    w.wd = c.probe[w.idx];
+    w.t_enter = m;
   }
-  visits += nv;
-#else
-  unsigned nx = 0, ny = 0;
-  bool exited = false;
-// Unrolled by 2: the compiler renames t_enter / m across the two copies and
-// interleaves them.
-#ifndef RB_P1_UNROLL
-#define RB_P1_UNROLL 2
+  return false;
+}
+
+// The walk, called by all 32 lanes of the warp (walking = false for lanes
+// without one). Runs of RB_P1_RUN cells: the walk (cell sequence and
+// crossing times) does not depend on the probe words, so the next RB_P1_RUN
+// steps are taken with their words loaded back to back (one memory latency
+// per run instead of one per cell), and the run is committed without per-cell
+// work when
+// (a) it is not the ray's last (its last crossing time is < t1, so every
+//     cell of it continues the walk: crossing times are non-decreasing), and
+// (b) no cell of it can pass its gate: every emitted height of the run lies
+//     between fl(oz + t*dz) at the run's first entry and last crossing time
+//     (the height's three correctly rounded operations are monotone in the
+//     two times, which lie in that interval), and the smaller end is >= the
+//     largest F of the run (the max of its words: 0 = no class, border =
+//     NaN, see probeWord) -- so every class cell would be rejected by its
+//     probe filter.
+// A run failing (b) is redone exactly. A lane whose run fails (a) -- its
+// last run -- waits, and all lanes finish their last cells together once
+// every lane of the warp got there (the warp cannot retire before its
+// longest ray anyway; a ray's last run handled when it comes up would be
+// executed by a lone lane, once per lane). A run's lookahead may step past
+// the border into the guard rows (DeviceMap::kProbeGuardRows), hence the
+// signed index. A run holding a candidate cell marks the ray touched even if
+// that cell is not emitted (the endpoint or a zero-length cell): the ray is
+// then queued for pass 2 without reason, which changes nothing (pass 2 only
+// acts on removed cells, all of them candidates the ray would have touched).
+static_assert(RB_P1_RUN > 1 && RB_P1_RUN < DeviceMap::kProbeGuardRows, "pass-1 run length");
+__device__ __forceinline__ void pass1Walk(P1Walk& w, const Pass1Ctx& c, uint32_t W, bool walking,
+                                          bool& touched, unsigned& visits) {
+  unsigned nv = 0;
+  const bool runs = walking && isfinite(c.oz) && isfinite(c.dz);
+  bool ending = !runs;  // lanes without runs do their whole walk in the final exact loop
+  bool finished = !walking;
+#ifdef RB_P1_DIAG
+  unsigned d_fast = 0, d_end = 0, d_gate = 0;
 #endif
-#define RB_PRAGMA_(x) _Pragma(#x)
-#define RB_UNROLL_(n) RB_PRAGMA_(unroll n)
-#define RB_UNROLL(n) RB_UNROLL_(n)
-  RB_UNROLL(RB_P1_UNROLL)
-  while (true) {
-    const bool sx = tmx < tmy;
-    const double m = sx ? tmx : tmy;  // = the reference's min (no NaN here)
-    bool more = m < t1;
-    // Only class / border cells leave the common path; the endpoint and
-    // zero-length tests of the reference's emission (t_next > t_enter) are
-    // made there, on the rare branch.
-    if ((wd & 3u) != 0) {
-      if ((wd & 3u) == 3u) {  // stepped out of the grid: stop before this cell
-        more = false;
-        exited = true;
+  while (!__all_sync(0xffffffffu, ending)) {
+    if (ending) continue;
+    double ax = w.tmx, ay = w.tmy, mlast = 0.0;
+    int j = static_cast<int>(w.idx);
+    uint32_t kmax = w.wd, kor = w.wd, wl = 0;
+#pragma unroll
+    for (int s = 0; s < RB_P1_RUN; ++s) {
+      // m = min, then the axis step (ptxas computes both sums and selects)
+      int dj;
+      asm("{\n\t.reg .pred p;\n\t"
+          "setp.lt.f64 p, %0, %1;\n\t"
+          "selp.f64 %2, %0, %1, p;\n\t"
+          "selp.s32 %3, %6, %7, p;\n\t"
+          "@p add.rn.f64 %0, %0, %4;\n\t"
+          "@!p add.rn.f64 %1, %1, %5;\n\t}"
+          : "+d"(ax), "+d"(ay), "=d"(mlast), "=r"(dj)
+          : "d"(w.tdx), "d"(w.tdy), "r"(w.step_col), "r"(w.step_row));
+      j += dj;
+      const uint32_t wj = c.probe[j];
+      if (s + 1 < RB_P1_RUN) {
+        kmax = max(kmax, wj);
+        kor |= wj;
       } else {
-        const double t_next = more ? m : t1;
-        if (idx != end_idx && t_next > t_enter) {
-          const double h = c.oz + (0.5 * (t_enter + t_next)) * c.dz;
-          const uint8_t tag = static_cast<uint8_t>(wd & 3u);
-          if (tag == kClsCandidate) touched = true;
-          // probe filter: h >= F implies the exact gate rejects (see probeWord)
-          if (!(h >= probeBound(wd))) {
-            const uint32_t pr = idx / Wp;
-            pass1Visit(c, tag, (pr - 1u) * W + (idx - pr * Wp - 1u), h, touched);
-          }
-        }
+        wl = wj;
       }
     }
-    if (!more) break;
-    // (the step counters keep the axis step predicated: two predicated adds
-    // each, rather than both adds and four selects)
-    if (sx) {
-      tmx += tdx;
-      ++nx;
-    } else {
-      tmy += tdy;
-      ++ny;
+    if (!(mlast < w.t1)) {  // the ray's last run: wait for the warp
+      ending = true;
+#ifdef RB_P1_DIAG
+      ++d_end;
+#endif
+      continue;
     }
-    idx += sx ? step_col : step_idx_row;
-    wd = probe[idx];
-    t_enter = m;
+    const double ha = c.oz + w.t_enter * c.dz, hb = c.oz + mlast * c.dz;
+    if (kmax == 0u || (ha < hb ? ha : hb) >= probeBound(kmax)) {
+      w.tmx = ax;
+      w.tmy = ay;
+      w.idx = static_cast<uint32_t>(j);
+      w.wd = wl;
+      w.t_enter = mlast;
+      nv += RB_P1_RUN;
+      if (kor & kClsCandidate) touched = true;
+#ifdef RB_P1_DIAG
+      ++d_fast;
+#endif
+    } else {
+#ifdef RB_P1_DIAG
+      ++d_gate;
+#endif
+      if (pass1Exact(w, c, W, RB_P1_RUN, nv, touched)) ending = finished = true;
+    }
   }
-  // cells iterated = steps taken + 1 (the step onto the border excluded)
-  visits += nx + ny + 1u - (exited ? 1u : 0u);
+  if (!finished) pass1Exact(w, c, W, 0xffffffffu, nv, touched);
+  visits += nv;
+#ifdef RB_P1_DIAG
+  atomicAdd(&g_p1diag[0], d_fast);
+  atomicAdd(&g_p1diag[1], d_end);
+  atomicAdd(&g_p1diag[2], d_gate);
+  atomicAdd(&g_p1diag[3], walking ? 1u : 0u);
+  atomicAdd(&g_p1diag[4], nv);
 #endif
 }
 
@@ -1561,29 +1571,30 @@ __device__ __forceinline__ void pass1Finite(const GridArgs& g, const double o[3]
 #define RB_P1_THREADS 128
 #endif
 constexpr int kP1Threads = RB_P1_THREADS;
-template <bool kStride>
-__global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
-    k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
-                 const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
-                 Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
-                 DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
-                 const uint32_t* __restrict__ pcell) {
-  pdlTrigger();  // the per-ray setup below runs before the wait (inputs from k_ingest)
-  if (retry && !st->respeculate) return;
-  // kStride (the retry launch): grid-stride over ray tiles with a one-wave
-  // grid, so its common no-op case costs one wave of returning blocks. The
-  // main launch has one block per tile (the loop runs once).
-  for (uint32_t k0 = blockIdx.x * kP1Threads; k0 < n;
-       k0 = kStride ? k0 + gridDim.x * kP1Threads : n) {
+// Pass 1 of the rays [k0, k0 + kP1Threads) of a tile, one per thread; every
+// thread of the block calls it (the walk and the queueing are warp-wide).
+template <typename ProbePtr, typename ClsPtr>
+__device__ __forceinline__ void pass1Tile(uint32_t k0, uint32_t n, const uint8_t* __restrict__ kept,
+                                          const double* __restrict__ px,
+                                          const double* __restrict__ py,
+                                          const double* __restrict__ pz, const RayArgs& a,
+                                          const Layers& L, ClsPtr cls, int32_t* kstar,
+                                          uint32_t* raylist, DevStats* st, uint32_t ray_base,
+                                          ProbePtr probe, const uint32_t* __restrict__ pcell) {
   const uint32_t k = k0 + threadIdx.x;
-  bool touched = false;
+  bool touched = false, walking = false;
   unsigned visits = 0;
+  Pass1Ctx c{cls, probe, L, kstar, 0.0, 0.0, 0.0, 0.0, a.alpha_n,
+             static_cast<int32_t>(ray_base + k)};  // global ray id (sharded frames)
+  P1Walk w;
   if (k < n && kept[k]) {
     const double ex = px[k], ey = py[k], ez = pz[k];
-    Pass1Ctx c{cls, probe, L, kstar, a.o[2], ez - a.o[2], ex - a.o[0], ey - a.o[1], a.alpha_n,
-               static_cast<int32_t>(ray_base + k)};  // global ray id (sharded frames)
+    c.oz = a.o[2];
+    c.dz = ez - a.o[2];
+    c.vx = ex - a.o[0];
+    c.vy = ey - a.o[1];
     if (isfinite(c.vx) && isfinite(c.vy)) {
-      pass1Finite(a.g, a.o, ex, ey, c, touched, visits, a, pcell ? pcell[k] : 0xffffffffu);
+      walking = pass1Setup(a.g, a.o, ex, ey, c, touched, visits, a, pcell ? pcell[k] : 0xffffffffu, w);
     } else {
       pdlWait();
       walkRay(a.g, a.o, ex, ey, [&](uint32_t cell, double te, double tn, bool vertical) {
@@ -1593,9 +1604,11 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
       });
     }
   }
-  // Every thread is past the wait before the counters (a retry's k_classify
-  // resets them); rays that needed no class data skipped it so far.
+  // Every thread is past the wait before the walk (class / probe words come
+  // from the classification) and the counters.
   pdlWait();
+  if (walking) w.wd = probe[w.idx];
+  pass1Walk(w, c, static_cast<uint32_t>(a.g.W), walking, touched, visits);
   // Queue rays that crossed a removal candidate for the k* pass (one atomic per warp).
   const unsigned lane = threadIdx.x & 31;
   const unsigned want = __ballot_sync(0xffffffffu, touched && a.bound);
@@ -1608,7 +1621,86 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
   }
   unsigned long long v = warpSum(static_cast<unsigned long long>(visits));
   if (lane == 0 && v) atomicAdd(&st->visits, v);
+}
+
+// kStride (the retry launch of sharded frames): grid-stride over ray tiles
+// with a one-wave grid, so its common no-op case costs one wave of returning
+// blocks. The main launch has one block per tile (the loop runs once).
+template <bool kStride>
+__global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
+    k_rays_pass1(uint32_t n, const uint8_t* __restrict__ kept, const double* __restrict__ px,
+                 const double* __restrict__ py, const double* __restrict__ pz, RayArgs a,
+                 Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
+                 DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
+                 const uint32_t* __restrict__ pcell) {
+  pdlTrigger();  // the per-ray setup runs before the wait (inputs from k_ingest)
+  if (retry && !st->respeculate) return;
+  for (uint32_t k0 = blockIdx.x * kP1Threads; k0 < n;
+       k0 = kStride ? k0 + gridDim.x * kP1Threads : n)
+    pass1Tile(k0, n, kept, px, py, pz, a, L, cls, kstar, raylist, st, ray_base, probe, pcell);
+}
+
+// Grid-wide barrier of a cooperative launch (all blocks co-resident):
+// bar[0] arrivals, bar[1] generation (both zero at the frame's stats reset).
+__device__ __forceinline__ void gridSync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g0 = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(64);
+    }
+    __threadfence();
   }
+  __syncthreads();
+}
+
+template <bool kScratch>
+__device__ __forceinline__ void pass2Rays(unsigned first, unsigned stride, const uint32_t* raylist,
+                                          unsigned total, const double* px, const double* py,
+                                          const double* pz, const RayArgs& a, const Layers& L,
+                                          const uint8_t* cls, const int32_t* kstar,
+                                          uint32_t ray_base, double* ub2);
+
+// The ray phase's tail on single-call frames, one cooperative one-wave
+// launch: (retry) if k_fuse_heavy found a speculated class wrong, the
+// classification and pass 1 again from scratch; then (pass2) the bounds of
+// the removed cells from the queued rays (k_rays_pass2<true>). Both are
+// rare; the common frame pays one launch that reads two flags.
+__global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
+    k_rays_tail(int retry, int pass2, uint32_t n, const uint8_t* __restrict__ kept,
+                const double* __restrict__ px, const double* __restrict__ py,
+                const double* __restrict__ pz, RayArgs a, Layers L, uint8_t* cls,
+                int32_t* kstar, uint32_t* raylist, DevStats* st, ProbeT* probe,
+                const uint32_t* __restrict__ pcell, double* ub2) {
+  pdlWait();
+  pdlTrigger();
+  if (retry && st->respeculate) {
+    // (cls / probe / k* are rewritten inside this kernel: plain loads below)
+    const ClassArgs ca{a.now, a.t_free, a.cleanup, a.bound, a.g.W};
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < static_cast<size_t>(a.g.W) * a.g.H;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+      classifyCell(L, i, false, ca, cls, probe, kstar);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // pass 1 runs again from scratch
+      st->candidate_rays = 0;
+      st->visits = 0;
+    }
+    gridSync(st->grid_bar);
+    for (uint32_t k0 = blockIdx.x * kP1Threads; k0 < n; k0 += gridDim.x * kP1Threads)
+      pass1Tile(k0, n, kept, px, py, pz, a, L, static_cast<const uint8_t*>(cls), kstar, raylist, st,
+                0u, static_cast<const ProbeT*>(probe), pcell);
+    gridSync(st->grid_bar);
+  }
+  if (pass2 && static_cast<volatile int32_t*>(kstar)[-1] != INT_MAX)
+    pass2Rays<true>(blockIdx.x * kP1Threads + threadIdx.x, gridDim.x * kP1Threads, raylist,
+                    static_cast<unsigned>(static_cast<volatile unsigned long long*>(
+                        &st->candidate_rays)[0]),
+                    px, py, pz, a, L, cls, kstar, 0u, ub2);
 }
 
 // Invalidate every cell some ray removed (set is order independent).
@@ -1634,16 +1726,12 @@ __global__ void __launch_bounds__(kThreads) k_remove(Layers L, size_t n, const i
 // removed cells; otherwise (sharded frames) k_remove has run and the bounds go
 // to the map.
 template <bool kScratch>
-__global__ void __launch_bounds__(kThreads)
-    k_rays_pass2(const uint32_t* __restrict__ raylist, const DevStats* st_in,
-                 const double* __restrict__ px, const double* __restrict__ py,
-                 const double* __restrict__ pz, RayArgs a, Layers L,
-                 const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar,
-                 uint32_t ray_base, double* ub2) {
-  pdlEnter();
-  if (kScratch ? kstar[-1] == INT_MAX : st_in->removed == 0) return;
-  const unsigned total = static_cast<unsigned>(st_in->candidate_rays);
-  for (unsigned q = blockIdx.x * kThreads + threadIdx.x; q < total; q += gridDim.x * kThreads) {
+__device__ __forceinline__ void pass2Rays(unsigned first, unsigned stride, const uint32_t* raylist,
+                                          unsigned total, const double* px, const double* py,
+                                          const double* pz, const RayArgs& a, const Layers& L,
+                                          const uint8_t* cls, const int32_t* kstar,
+                                          uint32_t ray_base, double* ub2) {
+  for (unsigned q = first; q < total; q += stride) {
     const uint32_t k = raylist[q];
     const double dz = pz[k] - a.o[2];
     walk(a.g, a.o, px[k], py[k], [&](uint32_t c, double te, double tn, bool vertical) {
@@ -1665,6 +1753,20 @@ __global__ void __launch_bounds__(kThreads)
       }
     });
   }
+}
+
+template <bool kScratch>
+__global__ void __launch_bounds__(kThreads)
+    k_rays_pass2(const uint32_t* __restrict__ raylist, const DevStats* st_in,
+                 const double* __restrict__ px, const double* __restrict__ py,
+                 const double* __restrict__ pz, RayArgs a, Layers L,
+                 const uint8_t* __restrict__ cls, const int32_t* __restrict__ kstar,
+                 uint32_t ray_base, double* ub2) {
+  pdlEnter();
+  if (kScratch ? kstar[-1] == INT_MAX : st_in->removed == 0) return;
+  pass2Rays<kScratch>(blockIdx.x * kThreads + threadIdx.x, gridDim.x * kThreads, raylist,
+                      static_cast<unsigned>(st_in->candidate_rays), px, py, pz, a, L, cls, kstar,
+                      ray_base, ub2);
 }
 
 // ------------------------------------------------------- K7 cell phases
@@ -2221,7 +2323,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
 
 // K5 pass 1 over this process's rays (ids ray_base + k), joined with the
 // long-cell fold (and redone if a speculated class was wrong).
-void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
+void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base, bool tail = false) {
   DeviceMap& m = f.m;
   cudaStream_t s = f.s;
   const RayArgs ra = rayArgs(f);
@@ -2236,9 +2338,12 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
                 m.px + f.ray_at, m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar,
                 m.raylist, m.stats, 0, ray_base, m.probe, f.point_cells);
       ++f.launches;
+#ifdef RB_P1_DIAG
+      k_p1diag<<<1, 1, 0, s>>>();
+#endif
     }
   }
-  if (f.overlap) {
+  if (f.overlap && !tail) {  // (tail: phaseRaysTail joins and retries)
     // Join the long-cell fold; redo the ray pass only if a heavy cell fused
     // nothing (both kernels return immediately otherwise).
     checkCuda(cudaStreamWaitEvent(s, m.ev[11], 0), "stream wait");
@@ -2253,6 +2358,30 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base) {
       ++f.launches;
     }
   }
+}
+
+// Single-call frames: join the long-cell fold, then one cooperative launch
+// for the retry of a failed speculation and pass 2 (k_rays_tail); k_cells
+// removes the k* < inf cells.
+void phaseRaysTail(Frame& f, uint32_t N) {
+  DeviceMap& m = f.m;
+  const RayArgs ra = rayArgs(f);
+  const bool retry = f.overlap && N > 0;
+  const bool pass2 = ra.cleanup && ra.bound;
+  if (ra.cleanup) f.fold_remove = true;
+  if (f.overlap) checkCuda(cudaStreamWaitEvent(f.s, m.ev[11], 0), "stream wait");
+  if (!retry && !pass2) return;
+  static int blocks_per_sm = 0, sms = 0;
+  if (blocks_per_sm == 0) {
+    checkCuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_rays_tail, kP1Threads, 0),
+              "occupancy");
+    checkCuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m.device), "device attribute");
+  }
+  launchCoopPdl(k_rays_tail, static_cast<unsigned>(blocks_per_sm * sms), kP1Threads, 0, f.s,
+                retry ? 1 : 0, pass2 ? 1 : 0, N, m.kept + f.ray_at, m.px + f.ray_at, m.py + f.ray_at,
+                m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar, m.raylist, m.stats, m.probe,
+                f.point_cells, m.ub2);
+  ++f.launches;
 }
 
 // Removal of k* < inf cells, then K6 bounds of removed cells from this
@@ -2481,8 +2610,8 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
-    phaseRaysPass1(f, N, 0);
-    phaseRemovePass2(f, 0);
+    phaseRaysPass1(f, N, 0, true);
+    phaseRaysTail(f, N);
   } else {
     RB_PHASE_EVENT(4, f.s);
     RB_PHASE_EVENT(5, f.s);
@@ -2595,8 +2724,8 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
-    phaseRaysPass1(f, N, 0);
-    phaseRemovePass2(f, 0);
+    phaseRaysPass1(f, N, 0, true);
+    phaseRaysTail(f, N);
   } else {
     RB_PHASE_EVENT(4, f.s);
     RB_PHASE_EVENT(5, f.s);
