@@ -429,6 +429,8 @@ def single_gpu_legs(lib, D, name, steps, warmup, local_rank, want_roofline=True,
         for s in range(warmup):
             for x, c in frames_src[s % nf]:
                 m2.integrate(x, c.pose, 0.1 * s, cfg)
+                if chain:  # (the first chain call allocates its scratch)
+                    m2.smooth_chain_device("elevation", wl.C5_CHAIN, d_vals.data_ptr(), d_ok.data_ptr())
         D.barrier()
         tt, copy = [], 0.0
         for s in range(warmup, warmup + steps):

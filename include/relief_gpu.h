@@ -241,6 +241,23 @@ RELIEF_API relief_status relief_gpu_group_integrate(relief_gpu_group* group,
                                                     int xyz_on_device, uint64_t n_total,
                                                     const double pose[12], double stamp,
                                                     relief_scan_stats* stats_out);
+/* Fusion of the group's frames (set before a frame; every rank the same):
+ *   RELIEF_GPU_GROUP_EXACT (default): the gated, order-dependent fold on every
+ *   rank from the gathered records -- bit-identical to one GPU.
+ *   RELIEF_GPU_GROUP_INFORMATION: ungated fusion in information form -- each
+ *   rank sums p/sigma_p^2 and 1/sigma_p^2 of its own points per cell, the sums
+ *   (and each invalid cell's first point) are all-reduced, and every rank folds
+ *   them into its replica: no point records exchanged and no redundant sort /
+ *   fold. Equal to the reference's sequential Kalman fold up to rounding when
+ *   its gates cannot fire, which the mode requires of the config:
+ *   update.mahalanobis_threshold >= 1e12 and update.wall_count_threshold >=
+ *   2^30 (else the frame fails with RELIEF_ERROR_USAGE). The ray passes and
+ *   cell phases are the exact mode's.
+ * relief_gpu_group_fusion returns the mode (-1 for a null group). */
+#define RELIEF_GPU_GROUP_EXACT 0
+#define RELIEF_GPU_GROUP_INFORMATION 1
+RELIEF_API relief_status relief_gpu_group_set_fusion(relief_gpu_group* group, int mode);
+RELIEF_API int relief_gpu_group_fusion(const relief_gpu_group* group);
 /* Version of the NCCL library the group transport uses (e.g. 22809), or -1. */
 RELIEF_API int relief_gpu_nccl_version(void);
 

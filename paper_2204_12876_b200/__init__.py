@@ -153,6 +153,8 @@ RELIEF_GPU_H_SIGNATURES = {
     "relief_gpu_group_create": (_P, [_P, ctypes.c_void_p, _I, _I]),
     "relief_gpu_group_create_local": (_P, [ctypes.POINTER(_P), _I]),
     "relief_gpu_group_free": (None, [_P]),
+    "relief_gpu_group_set_fusion": (_I, [_P, _I]),
+    "relief_gpu_group_fusion": (_I, [_P]),
     "relief_gpu_group_bounds": (_I, [ctypes.c_uint64, _I, _I, ctypes.POINTER(ctypes.c_uint64),
                                      ctypes.POINTER(ctypes.c_uint64)]),
     "relief_gpu_group_integrate": (_I, [_P, _P, ctypes.c_void_p, _SZ, _I, ctypes.c_uint64, _DP, _D,
@@ -458,6 +460,17 @@ class Group:
         if not h:
             raise ReliefError(1, lib.relief_last_error().decode())
         return cls(lib, h, list(maps), len(maps), 0, True)
+
+    EXACT, INFORMATION = 0, 1
+
+    def set_fusion(self, mode: int) -> None:
+        """relief_gpu_group_set_fusion: Group.EXACT (gated, bit-identical to one GPU) or
+        Group.INFORMATION (ungated information-form partial sums, all-reduced)."""
+        _check(self.lib, self.lib.relief_gpu_group_set_fusion(self.handle, int(mode)))
+
+    @property
+    def fusion(self) -> int:
+        return int(self.lib.relief_gpu_group_fusion(self.handle))
 
     def bounds(self, n_total: int, rank: Optional[int] = None):
         return group_bounds(self.lib, n_total, self.ranks, self.rank if rank is None else rank)

@@ -630,6 +630,15 @@ void relief_gpu_group_free(relief_gpu_group* group) {
   delete group;
 }
 
+relief_status relief_gpu_group_set_fusion(relief_gpu_group* group, int mode) {
+  if (group == nullptr) return usage("null argument");
+  return guard([&] { rb200::groupSetFusion(*group->g, mode); });
+}
+
+int relief_gpu_group_fusion(const relief_gpu_group* group) {
+  return group ? rb200::groupFusion(*group->g) : -1;
+}
+
 relief_status relief_gpu_group_bounds(uint64_t n_total, int n_ranks, int rank, uint64_t* lo,
                                       uint64_t* hi) {
   if (lo == nullptr || hi == nullptr) return usage("null argument");

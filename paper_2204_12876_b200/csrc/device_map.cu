@@ -186,6 +186,7 @@ void destroyDeviceMap(DeviceMap* m) {
   cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   cudaFree(m->slab);
+  cudaFree(m->islab);
   cudaFree(m->pslab);
   cudaFree(m->rslab);
   cudaFree(m->export_buf);

@@ -130,6 +130,12 @@ struct DeviceMap {
   int32_t* kstar = nullptr;
   double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
+  // information-form group frames (allocated on first use, W*H each): the
+  // exchanged per-cell partials (sum p/v, sum 1/v, first point, points, first
+  // rank) and this rank's first point per cell
+  void* islab = nullptr;
+  double *info_a = nullptr, *info_b = nullptr, *info_pf = nullptr, *info_pfl = nullptr;
+  int32_t *info_n = nullptr, *info_first = nullptr;
   // per-point scratch (grown on demand)
   std::size_t cap = 0;
   void* pslab = nullptr;
@@ -304,11 +310,18 @@ struct GroupGeom {
 GroupGeom groupGeom(uint64_t n_total, int ranks, int rank);
 struct GroupFrame;
 GroupFrame* groupBegin(DeviceMap& m, const PipelineParams& P, const GroupGeom& g, const Pose& pose,
-                       double stamp, double dt);
+                       double stamp, double dt, bool info = false);
 void groupEnd(GroupFrame* gf);
 void groupPhaseIngest(GroupFrame& gf, const double* xyz, bool on_device,
                       std::vector<XBuf>& gathers);
 void groupPhaseUpdate(GroupFrame& gf, std::vector<XBuf>& reduces);
+// Information-form variant of the update (ungated fusion only):
+// local per-cell partials (reduces: first rank), then the first points
+// (reduces: the partials), then the fold of the merged partials + ray pass 1
+// (reduces: k*, bounds, as groupPhaseUpdate).
+void groupPhaseInfoPartials(GroupFrame& gf, std::vector<XBuf>& reduces);
+void groupPhaseInfoFirst(GroupFrame& gf, std::vector<XBuf>& reduces);
+void groupPhaseInfoApply(GroupFrame& gf, std::vector<XBuf>& reduces);
 void groupPhaseRemove(GroupFrame& gf, std::vector<XBuf>& reduces);
 void groupPhaseCells(GroupFrame& gf, std::vector<XBuf>& reduces);
 ScanResult groupFinish(GroupFrame& gf);
@@ -322,6 +335,11 @@ void groupDestroy(Group* g);
 int groupRanks(const Group& g);
 int groupRank(const Group& g);
 bool groupIsLocal(const Group& g);
+// Fusion of group frames: 0 exact (gated, bit-identical to one GPU), 1
+// information form (ungated partial sums + all-reduce; needs gates that
+// cannot fire: mahalanobis_threshold >= 1e12, wall_count_threshold >= 2^30).
+void groupSetFusion(Group& g, int mode);
+int groupFusion(const Group& g);
 const std::vector<DeviceMap*>& groupMaps(const Group& g);
 ScanResult groupIntegrate(Group& g, const PipelineParams& P, const double* xyz, std::size_t n,
                           bool on_device, uint64_t n_total, const Pose& pose, double stamp,

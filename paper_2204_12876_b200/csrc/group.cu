@@ -1,5 +1,6 @@
-// Group frames: one frame split across GPUs (exact variant;
-// DESIGN.md §7), and the transports that run its exchanges.
+// Group frames: one frame split across GPUs (exact and
+// information-form variants), and the transports that run its
+// exchanges.
 //
 // The frame's phases live in pipeline.cu (groupPhase*): each enqueues its
 // kernels on the map's stream and names the buffers to exchange next. Two
@@ -319,6 +320,7 @@ struct LocalTransport : Transport {
 
 struct Group {
   bool local = false;
+  int fusion = 0;  // 0 exact, 1 information form
   std::vector<DeviceMap*> maps;  // NCCL: this rank's map; local: every rank's, in rank order
   std::unique_ptr<NcclTransport> nccl;
   std::unique_ptr<LocalTransport> loc;
@@ -377,6 +379,11 @@ void groupDestroy(Group* g) { delete g; }
 int groupRanks(const Group& g) { return g.ranks; }
 int groupRank(const Group& g) { return g.rank; }
 bool groupIsLocal(const Group& g) { return g.local; }
+void groupSetFusion(Group& g, int mode) {
+  if (mode != 0 && mode != 1) fail(Err::kUsage, "group fusion mode must be 0 (exact) or 1 (information form)");
+  g.fusion = mode;
+}
+int groupFusion(const Group& g) { return g.fusion; }
 const std::vector<DeviceMap*>& groupMaps(const Group& g) { return g.maps; }
 
 // One frame through a group (both transports). xyz: NCCL -- this rank's batch;
@@ -398,7 +405,9 @@ ScanResult groupIntegrate(Group& g, const PipelineParams& P, const double* xyz, 
   if (!g.local && n != geo[0].n_local)
     fail(Err::kUsage, "batch size differs from relief_gpu_group_bounds for this rank");
   if (g.local && n != n_total) fail(Err::kUsage, "a local group takes the whole frame");
-  for (int r = 0; r < G; ++r) frames[r] = groupBegin(*g.maps[r], P, geo[r], pose, stamp, dts[r]);
+  const bool info = g.fusion == 1;
+  for (int r = 0; r < G; ++r)
+    frames[r] = groupBegin(*g.maps[r], P, geo[r], pose, stamp, dts[r], info);
   std::vector<std::vector<XBuf>> x(G);
   auto exchange = [&](bool is_gather) {
     if (g.local) {
@@ -416,7 +425,15 @@ ScanResult groupIntegrate(Group& g, const PipelineParams& P, const double* xyz, 
     groupPhaseIngest(*frames[r], mine, on_device, x[r]);
   }
   exchange(true);
-  for (int r = 0; r < G; ++r) groupPhaseUpdate(*frames[r], x[r]);
+  if (info) {
+    for (int r = 0; r < G; ++r) groupPhaseInfoPartials(*frames[r], x[r]);
+    exchange(false);
+    for (int r = 0; r < G; ++r) groupPhaseInfoFirst(*frames[r], x[r]);
+    exchange(false);
+    for (int r = 0; r < G; ++r) groupPhaseInfoApply(*frames[r], x[r]);
+  } else {
+    for (int r = 0; r < G; ++r) groupPhaseUpdate(*frames[r], x[r]);
+  }
   exchange(false);
   for (int r = 0; r < G; ++r) groupPhaseRemove(*frames[r], x[r]);
   exchange(false);

@@ -154,3 +154,106 @@ def test_shard_api_exchange_written_late_on_torch_stream(gpu, reference, tmp_pat
         for st, m in zip(got, reps):
             assert_stats_match(st, want, context=f"frame {f}")
             assert_layers_match(m.layers(), single.layers(), context=f"frame {f}")
+
+
+# ------------------------------------------------ information-form group frames
+# relief_gpu_group_set_fusion(RELIEF_GPU_GROUP_INFORMATION): each rank sums its own points per cell
+# in information form and the sums are all-reduced. Checked against the
+# reference's sequential Kalman fold run with its gates disabled (integration.cpp:40-55: the
+# outlier gate cannot fire under mahalanobis_threshold = 1e12, the wall gate under 2^30 points),
+# the configuration the mode requires; heights equal up to rounding (1e-9 relative here).
+UNGATED = "update.mahalanobis_threshold = 1e12\nupdate.wall_count_threshold = 1073741824\n"
+
+
+def _info_run(gpu, reference, tmp_path, text, res, W, H, G, frames, context):
+    cfg_path = tmp_path / "info.config"
+    cfg_path.write_text(text)
+    cfg, cfg_ref = pk.Config.load(gpu, cfg_path), pk.Config.load(reference, cfg_path)
+    ref_map = pk.ReliefMap.create(reference, res, W, H)
+    reps = [pk.ReliefMap.create(gpu, res, W, H) for _ in range(G)]
+    group = pk.Group.local(gpu, reps)
+    group.set_fusion(pk.Group.INFORMATION)
+    assert group.fusion == pk.Group.INFORMATION
+    totals = {"points_fused": 0, "cells_removed_by_cleanup": 0}
+    for f, (xyz, pose, stamp) in enumerate(frames(cfg_path)):
+        want = ref_map.integrate(xyz, pose, stamp, cfg_ref)
+        got = group.integrate(xyz, len(xyz), pose, stamp, cfg)
+        ctx = f"{context} G={G} frame {f}"
+        assert_stats_match(got, want, drift_tol=1e-12, context=ctx)
+        for k in totals:
+            totals[k] += getattr(got, k)
+        ref_layers = ref_map.layers()
+        for g, m in enumerate(reps):
+            assert m.center() == ref_map.center()
+            assert_layers_match(m.layers(), ref_layers, height_tol=1e-9, tol_trav=1e-9,
+                                context=f"{ctx} rank {g}")
+    group.close()
+    return totals
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_group_information_form_vs_reference_ungated(gpu, reference, tmp_path, G):
+    """Recenter every frame, drift compensation, cleanup + bounds (reference defaults otherwise)."""
+    text = wl._map(0.04, 300, 300) + "noise.alpha_d = 0.0002\n" + wl.lidar(512, rings=64) + \
+        wl.SCENE_S0 + UNGATED
+
+    def frames(cfg_path):
+        for f in range(6):
+            pose = wl.pose34(np.eye(3), (0.04 * f + 0.013, -0.021 * f, 1.0 + 0.01 * f))
+            yield ref_render(reference, cfg_path, pose, 0.1 * f, 3, f), pose, 0.15 * f
+
+    t = _info_run(gpu, reference, tmp_path, text, 0.04, 300, 300, G, frames, "lidar")
+    assert t["points_fused"] > 0
+
+
+def test_group_information_form_removals(gpu, reference, tmp_path):
+    """Removals fire under the information form (4 ranks): a box seen by beams 25-35 degrees
+    down vanishes at 2.95 s; the beams then pass below its stale top cells to the ground behind
+    (ungated fusion would average any point landing in them, so none may land there)."""
+    text = (wl._map(0.04, 120, 120) +
+            "noise.alpha_d = 0.005\nupdate.sigma_outlier2 = 0.0001\ndrift.enabled = false\n"
+            "overlap.enabled = false\nexclusion.enabled = false\ncleanup.t_free = 0.3\n"
+            "sensor.pattern = grid\nsensor.h_fov_deg = 70\nsensor.v_fov_deg = 10\n"
+            "sensor.cols = 160\nsensor.rows = 30\nsensor.max_range = 10\n"
+            "scene.ground = 0.0\nscene.moving_box = 1.2 0.0 0.3 0.8 0.8 0.6 0 0 0 -1 2.95\n" + UNGATED)
+    pose = wl.pose34(wl.rot_y(math.radians(30.0)), (0.0, 0.0, 1.2))
+
+    def frames(cfg_path):
+        for s in range(60):
+            yield ref_render(reference, cfg_path, pose, s * 0.1, 4, s), pose, s * 0.1
+
+    t = _info_run(gpu, reference, tmp_path, text, 0.04, 120, 120, 4, frames, "moving box")
+    assert t["cells_removed_by_cleanup"] > 50, t
+
+
+def test_group_information_form_c4_full_size(gpu, reference, tmp_path):
+    """The configured C4 split (1,000,064 points -> 1000x1000) over 4 ranks, information form."""
+    w = wl.c4()
+
+    def frames(cfg_path):
+        for f in range(2):
+            for c in w.calls(f):
+                yield ref_render(reference, cfg_path, c.pose, c.time, c.seed, c.scan_index), c.pose, c.stamp
+
+    t = _info_run(gpu, reference, tmp_path, w.config_text + UNGATED, w.resolution, w.width, w.height, 4,
+                  frames, "C4")
+    assert t["points_fused"] > 1_000_000
+
+
+def test_group_information_form_needs_ungated_config(gpu, tmp_path):
+    """The mode refuses a config whose gates can fire (RELIEF_ERROR_USAGE), and unknown modes."""
+    cfg_path = tmp_path / "gated.config"
+    cfg_path.write_text(wl._map(0.04, 60, 60))
+    cfg = pk.Config.load(gpu, cfg_path)
+    reps = [pk.ReliefMap.create(gpu, 0.04, 60, 60) for _ in range(2)]
+    group = pk.Group.local(gpu, reps)
+    with pytest.raises(pk.ReliefError):
+        group.set_fusion(7)
+    group.set_fusion(pk.Group.INFORMATION)
+    xyz = np.stack([np.zeros(10), np.zeros(10), -np.ones(10)], axis=1)
+    with pytest.raises(pk.ReliefError) as e:
+        group.integrate(xyz, 10, wl.pose34(np.eye(3), (0.0, 0.0, 1.0)), 0.0, cfg)
+    assert "information-form" in str(e.value)
+    group.set_fusion(pk.Group.EXACT)
+    group.integrate(xyz, 10, wl.pose34(np.eye(3), (0.0, 0.0, 1.0)), 0.0, cfg)
+    group.close()
