@@ -58,6 +58,8 @@ REF_LIB = ROOT / "oracle" / "_ref" / "librelief_ref.so"
 L2_FLUSH_BYTES = 256 << 20
 DEVSTATS_BYTES = 128  # DevStats read back per scan (device_map.hpp)
 N_FRAMES = 8          # distinct frames cycled by both arms
+# gates that cannot fire: the configuration the information-form group mode requires
+UNGATED = "update.mahalanobis_threshold = 1e12\nupdate.wall_count_threshold = 1073741824\n"
 CONFIG_NAMES = ("C1", "C2", "C3", "headline", "C4", "C5")
 LAYERS = ("elevation", "variance", "last_update", "upper_bound", "upper_bound_valid", "traversability",
           "normal_x", "normal_y", "normal_z", "valid")
@@ -546,6 +548,35 @@ def sharded_legs(lib, D, args, rank, world, local_rank, dist):
     grp2.close()
     m2.close()
 
+    # information-form group frames (relief_gpu_group_set_fusion): the same split with ungated
+    # fusion -- per-cell partial sums all-reduced instead of the records gathered and the whole
+    # frame sorted and folded on every rank; needs a config whose gates cannot fire
+    import tempfile
+    from pathlib import Path
+    up = Path(tempfile.mkdtemp()) / "ungated.config"
+    up.write_text(w.config_text + UNGATED)
+    cfg_u = pk.Config.load(lib, up)
+    m3 = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
+    grp3 = mg.create_nccl_group(lib, m3, dist)
+    grp3.set_fusion(pk.Group.INFORMATION)
+    for s in range(warmup):
+        grp3.integrate_device(my_dev[s % nf].data_ptr(), hi - lo, n_total, frames[s % nf][0][1].pose, 0.1 * s,
+                              cfg_u)
+    D.barrier()
+    info_t = []
+    for s in range(warmup, warmup + steps):
+        D.flush_l2()
+        grp3.integrate_device(my_dev[s % nf].data_ptr(), hi - lo, n_total, frames[s % nf][0][1].pose, 0.1 * s,
+                              cfg_u)
+        info_t.append(m3.kernel_seconds()[7])
+    D.barrier()
+    info_total = D.max(sum(info_t))
+    info_digests = [None] * world
+    dist.all_gather_object(info_digests, layer_digest(m3))
+    info_elev = m3.layers()["elevation"] if rank == 0 else None
+    grp3.close()
+    m3.close()
+
     # replicas: an independent map per GPU (weak scaling)
     _, rep, _ = single_gpu_legs(lib, D, args.workload, steps, warmup, local_rank, want_roofline=False)
     rep_max_ms = D.max(rep["ms_per_frame"])
@@ -557,11 +588,28 @@ def sharded_legs(lib, D, args, rank, world, local_rank, dist):
             t, c = dev_frames[s % nf][0]
             ms.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
         want = layer_digest(ms)
+        mu = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
+        for s in range(warmup + steps):  # the ungated sequential fold on one GPU
+            t, c = dev_frames[s % nf][0]
+            mu.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg_u)
+        ue = mu.layers()["elevation"]
+        fin = np.isfinite(ue) & np.isfinite(info_elev)
+        same_mask = bool((np.isnan(ue) == np.isnan(info_elev)).all())
+        rel = float((np.abs(info_elev[fin] - ue[fin]) / np.maximum(1.0, np.abs(ue[fin]))).max()) if fin.any() else 0.0
+        mu.close()
         parity = {"parity_hash_ok": all(d == want for d in digests),
                   "replicas_consistent": len(set(digests)) == 1,
                   "layer_sha256": want[:16],
                   "check": "sha256 of all 10 layers after the warm-up + timed frames, every rank vs a "
-                           "single-GPU map fed the whole frames"}
+                           "single-GPU map fed the whole frames",
+                  "information_form": {
+                      "value": n_total * steps / info_total, "unit": "points/s",
+                      "ms_per_step": info_total / steps * 1e3,
+                      "replicas_consistent": len(set(info_digests)) == 1,
+                      "elevation_max_rel_diff_vs_sequential": rel, "valid_mask_equal": same_mask,
+                      "parity_ok": same_mask and rel <= 1e-9 and len(set(info_digests)) == 1,
+                      "config": "workload config + " + UNGATED.replace(chr(10), "; ").strip("; "),
+                      "api": "relief_gpu_group_set_fusion(RELIEF_GPU_GROUP_INFORMATION), device batches"}}
     grp.close()
     m.close()
     out = {"value": n_total * steps / dev_total, "ms_per_step": dev_total / steps * 1e3,
@@ -608,6 +656,7 @@ def run_b200(args, rank, world, local_rank):
                 "config": config_dict(w, args.workload, main["points_per_frame"], 1, nf, world),
                 "e2e": main["e2e"], "gpu_launches": main["gpu_launches"], "clocks": main["clocks"],
                 "replicas": main["replicas"], "parity_hash_ok": main.get("parity_hash_ok"),
+                "information_form": main.get("information_form"),
                 "replicas_consistent": main.get("replicas_consistent"),
                 "parity_check": main.get("check"), "layer_sha256": main.get("layer_sha256"),
                 "nccl_version": main["nccl_version"], "cpu_baseline": None,

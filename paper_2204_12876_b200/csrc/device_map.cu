@@ -133,7 +133,16 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
   m->grid = grid;
   try {
     checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
-    checkCuda(cudaStreamCreateWithFlags(&m->stream2, cudaStreamNonBlocking), "stream create");
+    // (RB_STREAM2_PRIO: the long-cell fold's stream at the highest priority, so
+    // its blocks take SM slots as the ray pass's retire)
+    int prio_lo = 0, prio_hi = 0;
+    checkCuda(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
+#ifndef RB_STREAM2_PRIO
+#define RB_STREAM2_PRIO 0  // measured slower
+#endif
+    checkCuda(cudaStreamCreateWithPriority(&m->stream2, cudaStreamNonBlocking,
+                                           RB_STREAM2_PRIO ? prio_hi : prio_lo),
+              "stream create");
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_after, cudaEventDisableTiming), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "event create");

@@ -902,6 +902,25 @@ __device__ __forceinline__ void flushCounts(FoldCounts k, DevStats* st) {
   }
 }
 
+// Before the fold (RB_SPLIT_CLASSIFY): the drift offset (as k_apply_offset)
+// and the ray class of every cell without points this scan -- its post-fusion
+// state is its current one -- so the classification sweep after the fold
+// shrinks to the cells k_fuse folds (which it classifies itself).
+__global__ void __launch_bounds__(kThreads)
+    k_prep(Layers L, size_t n, const double* off_p, const int32_t* __restrict__ count, ClassArgs ca,
+           uint8_t* cls, ProbeT* probe, int32_t* kstar) {
+  pdlEnter();
+  const double off = off_p != nullptr ? *off_p : 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (off != 0.0) {
+      if (L.valid[i]) L.elev[i] += off;
+      if (L.ubv[i]) L.ub[i] += off;
+    }
+    if (count[i] == 0) classifyCell(L, i, false, ca, cls, probe, kstar);
+  }
+}
+
 // Cells with at most `heavy` points are folded here, one thread per cell;
 // longer cells are queued for k_fuse_heavy, which runs on a second stream
 // concurrently with the ray pass: cells
@@ -920,9 +939,12 @@ __global__ void __launch_bounds__(kThreads)
            int classify, ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
            int32_t* __restrict__ kstar) {
   // wait first: the ray pass launched on our trigger may then read anything
-  // older than this kernel before its own wait
+  // older than this kernel before its own wait. When the ray pass follows
+  // directly (classify 2), trigger only once the fold is done: resident
+  // pass-1 blocks waiting for us would take the registers this low-occupancy
+  // fold needs.
   pdlWait();
-  pdlTrigger();
+  if (classify != 2) pdlTrigger();
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const int cnt = i < ncell ? count[i] : 0;
   if (off_p != nullptr && i < ncell) {
@@ -953,8 +975,11 @@ __global__ void __launch_bounds__(kThreads)
   }
   FoldCounts k;
   if (cnt > 0 && !is_heavy) foldCell(L, i, cnt, start, spz, spv, a, st, k);
-  if (classify && i < ncell) classifyCell(L, i, is_heavy, ca, cls, probe, kstar);
+  // classify 1: every cell; 2: the cells with points (k_prep classified the rest)
+  if (i < ncell && (classify == 1 || (classify == 2 && cnt > 0)))
+    classifyCell(L, i, is_heavy, ca, cls, probe, kstar);
   flushCounts(k, st);
+  if (classify == 2) pdlTrigger();
 }
 
 // Post-fusion ray class of a cell the concurrent ray pass treated as "none";
@@ -2308,19 +2333,33 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
 #ifndef RB_FUSE_CLASSIFY
 #define RB_FUSE_CLASSIFY 0
 #endif
-  if (!RB_FUSE_OFFSET && f.fuse_offset != nullptr) {
-    launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, f.fuse_offset);
+#ifndef RB_SPLIT_CLASSIFY
+#define RB_SPLIT_CLASSIFY 0  // measured slower
+#endif
+  const RayArgs ra = rayArgs(f);
+  const ClassArgs ca{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W};
+  int classify = 0;
+  if (RB_SPLIT_CLASSIFY && (ra.cleanup || ra.bound)) {
+    launchPdl(k_prep, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell,
+              static_cast<const double*>(f.fuse_offset), static_cast<const int32_t*>(m.count), ca,
+              m.cls, m.probe, m.kstar);
     ++f.launches;
     f.fuse_offset = nullptr;
+    classify = 2;
+  } else {
+    if (!RB_FUSE_OFFSET && f.fuse_offset != nullptr) {
+      launchPdl(k_apply_offset, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell, f.fuse_offset);
+      ++f.launches;
+      f.fuse_offset = nullptr;
+    }
+    classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound) ? 1 : 0;
   }
-  const RayArgs ra = rayArgs(f);
-  const bool classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound);
   launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv,
-            fa, m.stats, f.heavy, m.heavy, m.heavy + f.ncell, f.fuse_offset, classify ? 1 : 0,
-            ClassArgs{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W}, m.cls, m.probe, m.kstar);
+            fa, m.stats, f.heavy, m.heavy, m.heavy + f.ncell, f.fuse_offset, classify, ca, m.cls,
+            m.probe, m.kstar);
   ++f.launches;
   f.fuse_offset = nullptr;
-  f.classified = classify;
+  f.classified = classify != 0;
   f.fa = fa;
   // (Launching it after k_classify instead, to keep that kernel boundary programmatic, made
   // the frame 15 % slower: the side-stream blocks then queue behind the ray pass.)

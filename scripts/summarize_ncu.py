@@ -20,7 +20,7 @@ ROOT = Path(__file__).resolve().parent.parent
 # kernel -> bench.py kernel group (the event-timed phases of integrateScanDevice)
 GROUP = {"k_ingest": "ingest", "k_drift_finalize": "drift", "k_apply_offset": "drift",
          "k_sort_rowscan": "sort", "k_sort_scatter": "sort", "k_fuse": "fusion", "k_fuse_heavy": "rays",
-         "k_classify": "rays", "k_rays_pass1": "rays", "k_remove": "rays", "k_rays_pass2": "rays",
+         "k_classify": "rays", "k_rays_pass1": "rays", "k_remove": "rays", "k_rays_pass2": "rays", "k_rays_tail": "rays",
          "k_cells": "cells", "k_shift": "shift"}
 
 
