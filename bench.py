@@ -365,38 +365,44 @@ def single_gpu_legs(lib, D, name, steps, warmup, local_rank, want_roofline=True,
     d_ok = torch.empty(cells, dtype=torch.uint8, device=D.dev)
 
     def run_device(m, s):
-        """(device seconds, host wall seconds of the library calls) of one step."""
-        dev = wall = 0.0
+        """(device seconds, wall seconds inside the library calls, wall seconds of the Python
+        calls) of one step. The library's in-call time is its own clock around the C call
+        (ScanStats.total_seconds); the Python time adds the ctypes marshalling."""
+        dev = wall = pywall = 0.0
         for t, c in dev_frames[s % nf]:
             t0 = time.perf_counter()
-            m.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
-            wall += time.perf_counter() - t0
+            st = m.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
+            pywall += time.perf_counter() - t0
+            wall += st.total_seconds
             dev += m.kernel_seconds()[7]  # device time, events at the frame ends only
         if chain:
             t0 = time.perf_counter()
             dev += m.smooth_chain_device("elevation", wl.C5_CHAIN, d_vals.data_ptr(), d_ok.data_ptr())
             wall += time.perf_counter() - t0
-        return dev, wall
+            pywall += time.perf_counter() - t0
+        return dev, wall, pywall
 
     # value: device-resident input
     m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
     for s in range(warmup):
         run_device(m, s)
     D.barrier()
-    dev_t, wall_t, launches = [], [], 0
+    dev_t, wall_t, pywall_t, launches = [], [], [], 0
     cm = clocks if clocks is not None else _Null()
     with cm:
         for s in range(warmup, warmup + steps):
             D.flush_l2()
-            dv, wv = run_device(m, s)
+            dv, wv, pv = run_device(m, s)
             dev_t.append(dv)
             wall_t.append(wv)
+            pywall_t.append(pv)
             launches += m.last_launches() * calls
     D.barrier()
     dev_total = D.max(sum(dev_t))
     out = {"value": pts * steps / dev_total, "unit": "points/s", "ms_per_frame": dev_total / steps * 1e3,
            "wall_ms_per_frame": statistics.mean(wall_t) * 1e3,
            "host_overhead_us_per_call": (statistics.mean(wall_t) - statistics.mean(dev_t)) / calls * 1e6,
+           "python_call_us_per_call": (statistics.mean(pywall_t) - statistics.mean(wall_t)) / calls * 1e6,
            "points_per_frame": pts, "calls_per_frame": calls, "gpu_launches": int(launches),
            "graphs": {"instantiated": m.graph_stats()[0], "updated": m.graph_stats()[1]},
            "frame_device_ms": [round(x * 1e3, 4) for x in dev_t]}
@@ -700,6 +706,10 @@ def run_b200(args, rank, world, local_rank):
         "config": config_dict(w, args.workload, main["points_per_frame"], main["calls_per_frame"], nf, 1),
         "wall_ms_per_step": main["wall_ms_per_frame"],
         "host_overhead_us_per_call": main["host_overhead_us_per_call"],
+        "python_call_us_per_call": main["python_call_us_per_call"],
+        "host_overhead_note": "wall time inside the library's synchronous call (its own clock) minus the "
+                              "frame's device time; python_call_us_per_call is the ctypes marshalling of the "
+                              "bench driver on top",
         "kernel_ms": main.get("kernel_ms"),
         "phase_split_note": "kernel_ms / roofline.duration_us come from a separate pass with phase events "
                             "on (they end the programmatic overlap at the phase boundaries); value and "

@@ -176,6 +176,8 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
+    checkCuda(cudaMallocHost(&m->h_seq, sizeof(unsigned long long)), "pinned stats");
+    *m->h_seq = 0;
     fillFresh(*m);
     k_probe_border<<<static_cast<unsigned>((np + 255) / 256), 256, 0, m->stream>>>(m->probe - guard,
                                                                                   np);
@@ -208,6 +210,7 @@ void destroyDeviceMap(DeviceMap* m) {
   cudaFree(m->stats);
   cudaFree(m->drift_offset);
   if (m->h_stats) cudaFreeHost(m->h_stats);
+  if (m->h_seq) cudaFreeHost(m->h_seq);
   for (int k = 0; k < DeviceMap::kSlots; ++k) {
     if (m->h_slot[k]) cudaFreeHost(m->h_slot[k]);
     if (m->ev_copied[k]) cudaEventDestroy(m->ev_copied[k]);

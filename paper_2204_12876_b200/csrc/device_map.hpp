@@ -56,6 +56,7 @@ struct DevStats {
   int respeculate;                    // a heavy cell fused nothing: redo the ray pass
   unsigned int ingest_done;           // ingest blocks finished (the last one reduces the drift vote)
   unsigned int grid_bar[2];           // k_rays_tail's grid barrier (arrivals, generation)
+  unsigned int cells_done;            // k_cells blocks finished (the last one hands the stats over)
 };
 
 // Geometry + parameters passed by value to kernels.
@@ -167,6 +168,12 @@ struct DeviceMap {
   std::size_t hist_cap = 0;
   DevStats* stats = nullptr;     // device
   DevStats* h_stats = nullptr;   // pinned host mirror
+  // Synchronous frames hand their stats over through pinned host memory: the
+  // last block of the frame's last kernel copies them into h_stats and then
+  // writes the frame's sequence number into *h_seq, which the host polls
+  // (no D2H copy, no stream synchronisation on the common path).
+  unsigned long long* h_seq = nullptr;
+  unsigned long long frame_seq = 0;
   double* drift_offset = nullptr;  // device scalar
   // host-side bookkeeping
   double last_stamp = 0.0;

@@ -21,10 +21,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstddef>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -37,6 +39,9 @@ namespace rb200 {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef RB_STATS_HANDOVER
+#define RB_STATS_HANDOVER 1  // synchronous frames: stats through pinned memory (DeviceMap::h_seq)
+#endif
 
 constexpr double kInf = __builtin_huge_val();
 
@@ -1816,7 +1821,40 @@ struct CellArgs {
   int fold_remove;
   const int32_t* kstar;
   double* ub2;
+  // Stats hand-over of a synchronous frame (DeviceMap::h_seq; null: none):
+  // the last of the nblocks blocks copies the stats to hstats, then writes seq.
+  DevStats* hstats;
+  unsigned long long* hseq;
+  unsigned long long seq;
+  unsigned nblocks;
 };
+
+// End of a k_cells block: the last block to finish copies the frame's stats
+// (final: every earlier kernel of the frame has completed, and every block's
+// counter atomics precede its ticket) to pinned host memory, fences, and
+// publishes the frame's sequence number.
+__device__ __forceinline__ void handOverStats(const CellArgs& a, DevStats* st, unsigned tid) {
+  if (a.hseq == nullptr) return;
+  __syncthreads();
+  if (tid >= 32) return;
+  unsigned ticket = 0;
+  if (tid == 0) {
+    __threadfence();
+    ticket = atomicAdd(&st->cells_done, 1u);
+  }
+  if (__shfl_sync(0xffffffffu, ticket, 0) != a.nblocks - 1) return;
+  // the last block's first warp: one stats word per lane, each lane fencing
+  // its own store before lane 0 publishes the sequence number
+  __threadfence();
+  static_assert(sizeof(DevStats) % 8 == 0 && sizeof(DevStats) / 8 <= 32, "stats words");
+  if (tid < sizeof(DevStats) / 8) {
+    reinterpret_cast<unsigned long long*>(a.hstats)[tid] =
+        reinterpret_cast<const volatile unsigned long long*>(st)[tid];
+    __threadfence_system();
+  }
+  __syncwarp();
+  if (tid == 0) *reinterpret_cast<volatile unsigned long long*>(a.hseq) = a.seq;
+}
 
 constexpr int kTileX = 32, kTileY = 8;
 constexpr std::size_t kCellsMaxSmem = 200 * 1024;
@@ -1995,6 +2033,7 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   removed = warpSum(removed);
   if ((tid & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
   if ((tid & 31) == 0 && removed) atomicAdd(&st->removed, removed);
+  handOverStats(a, st, static_cast<unsigned>(tid));
 }
 
 // Same cell phases without the tile, for traversability windows too large to
@@ -2010,6 +2049,7 @@ __global__ void __launch_bounds__(256)
   removed = warpSum(removed);
   if ((threadIdx.x & 31) == 0 && cleared) atomicAdd(&st->overlap_cleared, cleared);
   if ((threadIdx.x & 31) == 0 && removed) atomicAdd(&st->removed, removed);
+  handOverStats(a, st, threadIdx.x);
 }
 
 
@@ -2076,6 +2116,10 @@ struct Frame {
   // (explicit_remove: sharded frames, whose host exchanges the bounds after it).
   bool fold_remove = false;
   bool explicit_remove = false;
+  // Stats handed over by k_cells through pinned memory (DeviceMap::h_seq)
+  // instead of a D2H copy + stream synchronisation (synchronous frames whose
+  // last kernel is k_cells).
+  bool handover = false;
   int heavy = INT_MAX;
   Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
       : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
@@ -2483,13 +2527,25 @@ void phaseCells(Frame& f) {
   ca.fold_remove = f.fold_remove ? 1 : 0;
   ca.kstar = m.kstar;
   ca.ub2 = m.ub2;
+  ca.hstats = nullptr;
+  ca.hseq = nullptr;
+  ca.seq = 0;
+  ca.nblocks = 0;
+  f.handover = f.handover && !f.P.use_convnet_traversability;
+  if (f.handover) {
+    ca.hstats = m.h_stats;
+    ca.hseq = m.h_seq;
+    ca.seq = ++m.frame_seq;
+  }
   const int halo = std::max(1, ca.radius);
   const std::size_t sm = static_cast<std::size_t>(kTileX + 2 * halo) * (kTileY + 2 * halo) * 9 + 16;
   if (sm > kCellsMaxSmem) {  // window too large for a shared-memory tile
+    ca.nblocks = static_cast<unsigned>((f.g.W + 255) / 256) * static_cast<unsigned>(f.g.H);
     launchPdl(k_cells_global, dim3((f.g.W + 255) / 256, f.g.H), 256, 0, f.s, m.cur, m.count,
               m.start, ca, m.stats);
   } else {
     const dim3 grid((f.g.W + kTileX - 1) / kTileX, (f.g.H + kTileY - 1) / kTileY);
+    ca.nblocks = grid.x * grid.y;
     auto* kern = ca.radius == 2 ? k_cells<2> : (ca.radius == 1 ? k_cells<1> : k_cells<0>);
     if (sm > 48 * 1024)
       checkCuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2513,12 +2569,29 @@ void phaseCells(Frame& f) {
 // Stats to the host (one sync).
 void phaseStatsEnqueue(Frame& f) {
   DeviceMap& m = f.m;
-  checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, f.s), "stats");
+  if (!f.handover)
+    checkCuda(cudaMemcpyAsync(m.h_stats, m.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, f.s), "stats");
   checkCuda(cudaGetLastError(), "kernel launch");
 }
 const DevStats& phaseStatsWait(Frame& f) {
   DeviceMap& m = f.m;
-  checkCuda(cudaStreamSynchronize(f.s), "integrate");
+  if (f.handover) {
+    // Poll the sequence number k_cells publishes; every 1024 polls ask the
+    // stream, so a failed frame (or a finished one whose write this thread
+    // has not yet seen) ends the wait with the stream's status.
+    const volatile unsigned long long* seq = m.h_seq;
+    for (unsigned k = 1; *seq != m.frame_seq; ++k) {
+      if ((k & 1023u) == 0) {
+        const cudaError_t e = cudaStreamQuery(f.s);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) checkCuda(e, "integrate");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (*seq != m.frame_seq) fail(Err::kDevice, "frame stats were not handed over");
+  } else {
+    checkCuda(cudaStreamSynchronize(f.s), "integrate");
+  }
   if (m.h_stats->error_code == 1) fail(Err::kInvalidVariance, "variances must be positive");
   return *m.h_stats;
 }
@@ -2664,11 +2737,30 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     RB_PHASE_EVENT(5, f.s);
   }
   RB_PHASE_EVENT(6, f.s);  // rays done
+  f.handover = RB_STATS_HANDOVER != 0;
   phaseCells(f);
   phaseStatsEnqueue(f);
   cap.launch();
+#ifdef RB_HOST_DIAG
+  const auto t_sub = std::chrono::steady_clock::now();
+#endif
   const DevStats& d = phaseStatsWait(f);
   ScanResult out = resultFrom(d, n);
+#ifdef RB_HOST_DIAG
+  {  // host-side split of the call: submission, wait (averages every 200 calls)
+    static double s_sub = 0, s_wait = 0;
+    static int s_n = 0;
+    const auto t_end = std::chrono::steady_clock::now();
+    s_sub += std::chrono::duration<double>(t_sub - t_call).count();
+    s_wait += std::chrono::duration<double>(t_end - t_sub).count();
+    if (++s_n == 200) {
+      fprintf(stderr, "HOSTDIAG n=%zu submit %.2f us wait %.2f us launches %lld\n", n, s_sub / s_n * 1e6,
+              s_wait / s_n * 1e6, f.launches);
+      s_sub = s_wait = 0;
+      s_n = 0;
+    }
+  }
+#endif
 
   // Per-phase device times are read from the events only when asked for
   // (resolveTiming): nine event queries cost ~30 us of host time per call.
@@ -2688,6 +2780,8 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
 void resolveTiming(DeviceMap& m) {
   if (!m.timing_pending) return;
   m.timing_pending = false;
+  // (a frame whose stats were handed over may still be recording its last event)
+  checkCuda(cudaEventSynchronize(m.ev[12]), "timing");
   if (!m.timing_phases) {  // only the upload and the device total were recorded
     float ms_copy = 0.0f, ms_total = 0.0f;
     checkCuda(cudaEventElapsedTime(&ms_copy, m.ev[0], m.ev[13]), "timing");

@@ -59,6 +59,9 @@ def main():
                 env["RELIEF_B200_LIB"] = os.path.join(ROOT, v, "librelief_b200.so")
             code = CHILD.replace("ROOT", repr(ROOT), 1).replace("WL", repr(wl.split(",")), 1)
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
+            if os.environ.get("AB_DUMP"):  # keep the child's output (e.g. a diag build's counters)
+                with open(os.environ["AB_DUMP"], "a") as fh:
+                    fh.write(f"== {v} round {rnd}\n" + r.stdout)
             line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")]
             if not line:
                 print(v, "FAILED", r.stderr[-2000:])
