@@ -58,13 +58,16 @@ RELIEF_API relief_status relief_gpu_map_kernel_seconds(const relief_map* map, do
  * also ends their programmatic (overlapped) launch. The runners turn it on. */
 RELIEF_API relief_status relief_gpu_map_set_phase_timing(relief_map* map, int on);
 
-/* CUDA graphs for synchronous frames (default off): each relief_map_integrate /
+/* CUDA graphs for synchronous frames. on = 1: each relief_map_integrate /
  * relief_gpu_map_integrate_device call captures its launches and replays them
- * as one graph launch, updating a cached executable graph in place. Off: the
- * same launches are issued one by one, chained by programmatic dependent
- * launch, which measured as fast on the device and cheaper on the host
- * (DESIGN.md §5.0b). Results are identical either way. graph_stats: out[0]
- * graphs instantiated, out[1] frames that updated a cached graph. */
+ * as one graph launch, updating a cached executable graph in place (frames of
+ * >= 512Ki points launch their head -- upload, resets, ingest -- directly and
+ * capture the rest while it runs). on = 0: the launches are issued one by one,
+ * chained by programmatic dependent launch. on = 2 (default): graphs for
+ * frames of >= 32Ki points, direct launches below (where the capture costs
+ * more than it saves). Results are identical either way; any
+ * other value: RELIEF_ERROR_USAGE. graph_stats: out[0] graphs instantiated,
+ * out[1] frames that updated a cached graph. */
 RELIEF_API relief_status relief_gpu_map_set_graphs(relief_map* map, int on);
 RELIEF_API relief_status relief_gpu_map_graph_stats(const relief_map* map, int64_t out[2]);
 

@@ -391,9 +391,10 @@ class ReliefMap:
             ctypes.c_void_p(d_valid)))
         return float(self.lib.relief_gpu_map_chain_seconds(self.handle))
 
-    def set_graphs(self, on: bool) -> None:
-        """relief_gpu_map_set_graphs: one CUDA graph per synchronous frame (default) or direct launches."""
-        _check(self.lib, self.lib.relief_gpu_map_set_graphs(self.handle, 1 if on else 0))
+    def set_graphs(self, on) -> None:
+        """relief_gpu_map_set_graphs: True / 1 one CUDA graph per synchronous frame, False / 0 direct
+        launches, 2 (the default) graphs for frames of at least 32Ki points."""
+        _check(self.lib, self.lib.relief_gpu_map_set_graphs(self.handle, int(on)))
 
     def graph_stats(self):
         """(graphs instantiated, frames that updated a cached graph)."""

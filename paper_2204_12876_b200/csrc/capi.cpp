@@ -548,7 +548,8 @@ relief_status relief_gpu_shard_finish(relief_map* map, const int64_t counters_to
 
 relief_status relief_gpu_map_set_graphs(relief_map* map, int on) {
   if (map == nullptr) return usage("null argument");
-  map->dev->use_graphs = on != 0;
+  if (on < 0 || on > 2) return usage("graph mode must be 0, 1 or 2");
+  map->dev->graph_mode = on;
   return RELIEF_OK;
 }
 

@@ -211,7 +211,7 @@ struct DeviceMap {
   long long graph_instantiations = 0, graph_updates = 0;
   // Off by default: measured no device-time gain over PDL-chained direct
   // launches and more host time per call (profiles/r2_host_overhead.txt).
-  bool use_graphs = false;
+  int graph_mode = 2;  // 0 direct launches, 1 graphs, 2 graphs for frames >= kGraphMinPoints
   // Synchronous host-input frames: the upload is split into kChunks copies on
   // copy_stream and each chunk is ingested as soon as it lands.
   static constexpr int kChunks = 2;  // 2 and 4 measured alike; 8 slower

@@ -39,6 +39,17 @@ namespace rb200 {
 namespace {
 
 constexpr int kThreads = 256;
+// Graph frames of at least kGraphMinPoints points (graph_mode 2); from
+// kGraphHeadPoints on, the frame's head is launched directly and only the
+// rest captured (its ingest then covers the capture and graph update).
+#ifndef RB_GRAPH_MIN_POINTS
+#define RB_GRAPH_MIN_POINTS 32768
+#endif
+#ifndef RB_GRAPH_HEAD_POINTS
+#define RB_GRAPH_HEAD_POINTS 524288
+#endif
+constexpr uint32_t kGraphMinPoints = RB_GRAPH_MIN_POINTS;
+constexpr uint32_t kGraphHeadPoints = RB_GRAPH_HEAD_POINTS;
 #ifndef RB_STATS_HANDOVER
 #define RB_STATS_HANDOVER 1  // synchronous frames: stats through pinned memory (DeviceMap::h_seq)
 #endif
@@ -2611,8 +2622,12 @@ struct FrameCapture {
   DeviceMap& m;
   cudaStream_t s;
   bool on;
-  FrameCapture(DeviceMap& map, cudaStream_t st, bool enable) : m(map), s(st), on(enable) {
-    if (on) checkCuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+  FrameCapture(DeviceMap& map, cudaStream_t st, bool enable) : m(map), s(st), on(false) {
+    if (enable) begin();
+  }
+  void begin() {
+    checkCuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+    on = true;
   }
   ~FrameCapture() {  // an exception mid-frame: end (and drop) the capture
     if (on) {
@@ -2703,7 +2718,12 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // Pageable host input cannot be a graph's copy source: it is uploaded
   // before the capture (the frame then reads it like device input).
   const bool pageable = !xyz_on_device && n > 0 && !hostPinned(xyz);
-  const bool graph = m.use_graphs && !P.use_convnet_traversability;
+  // Graph frames (DeviceMap::graph_mode): with direct launches the device
+  // outruns the host's submission on mid-size frames; on tiny frames the
+  // capture + update costs more than it saves.
+  const bool graph = !P.use_convnet_traversability &&
+                     (m.graph_mode == 1 || (m.graph_mode == 2 && N >= kGraphMinPoints));
+  const bool graph_head = graph && N >= kGraphHeadPoints;
   // ev0 -> ev13: the input copy (host input only); everything after it is the
   // frame's device time (stats / count / tile-count resets, recenter, kernels).
   const double* d_xyz = xyz;
@@ -2712,7 +2732,11 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     d_xyz = phaseUpload(f, xyz, n, false);
     recordTiming(m.ev[13], f.s);
   }
-  FrameCapture cap(m, f.s, graph);
+  // Graph frames: the head of the frame (upload, resets, recenter, ingest,
+  // drift) is launched directly, so the device starts at once; the rest is
+  // captured and its graph updated while the ingest runs (RB_GRAPH_HEAD 0:
+  // the whole frame is captured).
+  FrameCapture cap(m, f.s, graph && !graph_head);
   const bool chunked = !xyz_on_device && !pageable && N >= 2 * kTile;
   if (!pageable) {
     recordTiming(m.ev[0], f.s);
@@ -2727,6 +2751,7 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   RB_PHASE_EVENT(2, f.s);  // ingest done
   phaseDrift(f, N);
   RB_PHASE_EVENT(3, f.s);  // drift done
+  if (graph_head) cap.begin();
   if (n > 0) {
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0

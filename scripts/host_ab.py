@@ -1,6 +1,7 @@
 """Host overhead of synchronous frames across library builds.
 
-Usage (GPU box): python scripts/host_ab.py default ab/NAME ... [--workloads=C1,C4]
+Usage (GPU box): python scripts/host_ab.py default ab/NAME default:g ... [--workloads=C1,C4]
+(suffix ":g" = relief_gpu_map_set_graphs(1), ":d" = (0) direct launches; none = the default mode)
 Per build and workload, over 200 frames after 20 warm-up frames (no L2 flush): the
 library's in-call wall time (ScanStats.total_seconds, its own clock around the C call),
 the device time of the frame (kernel_seconds()[7], events on the library stream) and
@@ -35,6 +36,8 @@ for name in WL:
     res = {}
     for leg in ("device", "pinned"):
         m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height)
+        if GRAPHS is not None:
+            m.set_graphs(GRAPHS)
         inc, devt, wall = [], [], []
         for s in range(220):
             t0 = time.perf_counter()
@@ -65,9 +68,11 @@ def main():
     for rnd in range(2):
         for v in args:
             env = dict(os.environ)
-            if v != "default":
-                env["RELIEF_B200_LIB"] = os.path.join(ROOT, v, "librelief_b200.so")
+            lib, _, opt = v.partition(":")
+            if lib != "default":
+                env["RELIEF_B200_LIB"] = os.path.join(ROOT, lib, "librelief_b200.so")
             code = CHILD.replace("ROOT", repr(ROOT), 1).replace("WL", repr(wl.split(",")), 1)
+            code = code.replace("GRAPHS", {"g": "1", "d": "0"}.get(opt, "None"))
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
             diag = [l for l in r.stderr.splitlines() if l.startswith("HOSTDIAG")]
             line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")]

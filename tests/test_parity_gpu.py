@@ -368,7 +368,8 @@ def test_graph_and_direct_launches_identical(gpu, reference, tmp_path):
     text = wl._map(0.04, 200, 200) + "noise.alpha_d = 0.0002\n" + wl.lidar(300, rings=48) + wl.SCENE_S0
     pair = Pair(gpu, reference, tmp_path, text, 0.04, 200, 200)
     pair.maps[0].set_graphs(True)
-    direct = pk.ReliefMap.create(gpu, 0.04, 200, 200)  # direct launches (the default)
+    direct = pk.ReliefMap.create(gpu, 0.04, 200, 200)
+    direct.set_graphs(False)  # direct launches
     cfg = pair.cfgs[0]
     for f in range(12):
         pose = wl.pose34(np.eye(3), (0.05 * (f // 3), 0.0, 1.0))  # recenter on every third frame
@@ -391,4 +392,34 @@ def test_graph_and_direct_launches_identical(gpu, reference, tmp_path):
         pair.compare(height_tol=1e-9, context=f"frame {f}")
     inst, upd = pair.maps[0].graph_stats()
     assert inst >= 2 and upd >= 6, (inst, upd)
+    assert direct.graph_stats() == (0, 0)
+
+
+def test_graph_modes_large_frames(gpu, reference, tmp_path):
+    """Graph mode 2 (the default) on frames above both thresholds (the head launched directly,
+    the rest captured), mode 1 and direct launches agree bit for bit, and with the reference."""
+    text = wl._map(0.04, 400, 400) + "noise.alpha_d = 0.0002\n" + wl.lidar(4400, rings=128) + wl.SCENE_S0
+    pair = Pair(gpu, reference, tmp_path, text, 0.04, 400, 400)   # default mode 2
+    forced = pk.ReliefMap.create(gpu, 0.04, 400, 400)
+    forced.set_graphs(1)
+    direct = pk.ReliefMap.create(gpu, 0.04, 400, 400)
+    direct.set_graphs(0)
+    cfg = pair.cfgs[0]
+    with pytest.raises(pk.ReliefError):
+        direct.set_graphs(3)
+    for f in range(4):
+        pose = wl.pose34(np.eye(3), (0.05 * f, 0.0, 1.0))
+        xyz = ref_render(reference, pair.cfg_path, pose, 0.1 * f, 9, f)
+        xyz = xyz[: len(xyz) - 40000 * (f % 2)]            # above / below 512Ki points
+        got = pair.maps[0].integrate(xyz, pose, 0.1 * f, cfg)
+        want = pair.maps[1].integrate(xyz, pose, 0.1 * f, pair.cfgs[1])
+        a = forced.integrate(xyz, pose, 0.1 * f, cfg)
+        d = direct.integrate(xyz, pose, 0.1 * f, cfg)
+        assert_stats_match(got, want, drift_tol=1e-12, context=f"frame {f}")
+        assert_stats_match(a, got, context=f"mode 1 frame {f}")
+        assert_stats_match(d, got, context=f"direct frame {f}")
+        assert_layers_match(forced.layers(), pair.maps[0].layers(), tol_trav=0.0, context=f"mode 1 {f}")
+        assert_layers_match(direct.layers(), pair.maps[0].layers(), tol_trav=0.0, context=f"direct {f}")
+        pair.compare(height_tol=1e-9, context=f"frame {f}")
+    assert pair.maps[0].graph_stats()[0] >= 1 and forced.graph_stats()[0] >= 1
     assert direct.graph_stats() == (0, 0)
