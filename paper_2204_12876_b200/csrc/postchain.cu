@@ -19,6 +19,7 @@
 #include "device_map.hpp"
 #include "fp_exact.cuh"
 #include "launch.cuh"
+#include "stl_sort.cuh"
 #include "runners.hpp"
 #include "snapshot.hpp"
 
@@ -27,6 +28,9 @@ namespace rb200 {
 namespace {
 
 constexpr int kT = 256;
+#ifndef RB_MEDIAN3
+#define RB_MEDIAN3 1  // tiled 3x3 median with a median-of-9 network (k_median3)
+#endif
 constexpr int kMaxWindow = 121;  // radius <= 5
 
 struct Weights {
@@ -86,15 +90,10 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
       if (cc < 0 || cc >= W) continue;
       const int j = rr * W + cc;
       if (!ok[j]) continue;
-      const double x = v[j];  // insertion keeps the window sorted ascending
-      int p = n++;
-      while (p > 0 && x < win[p - 1]) {
-        win[p] = win[p - 1];
-        --p;
-      }
-      win[p] = x;
+      win[n++] = v[j];
     }
   }
+  stl::sort(win, n);  // the reference's std::sort, move for move (stl_sort.cuh)
   out[i] = (n % 2 == 1) ? win[n / 2] : 0.5 * (win[n / 2 - 1] + win[n / 2]);
 }
 
@@ -103,6 +102,80 @@ __global__ void __launch_bounds__(kT) k_median(const double* __restrict__ v,
 // skips (outside the grid or invalid) as k_linear. (A tiled median was not
 // faster: its cost is the per-cell insertion sort, not the loads.)
 constexpr int kSX = 32, kSY = 8;
+// 3x3 median (radius 1), 32 x 8 cells per block with the halo staged in
+// shared memory. A cell whose nine window cells are all valid, non-zero and
+// not NaN takes the rank-4 value from a median-of-9 exchange network (nine
+// distinct-or-identical values: the rank-4 value is the same bits whatever
+// sorts them); any other cell (fewer values, or a +-0 / NaN whose final place
+// the reference's std::sort decides) sorts its window with stl::sort, as
+// k_median.
+__device__ __forceinline__ void cmpSwap(double& a, double& b) {
+  const double lo = b < a ? b : a, hi = b < a ? a : b;
+  a = lo;
+  b = hi;
+}
+__global__ void __launch_bounds__(kSX* kSY) k_median3(const double* __restrict__ v,
+                                                      const uint8_t* __restrict__ ok, int W, int H,
+                                                      double* __restrict__ out,
+                                                      uint8_t* __restrict__ ok_out) {
+  pdlEnter();
+  constexpr int TW = kSX + 2, TH = kSY + 2;
+  __shared__ double sv[TH * TW];
+  __shared__ uint8_t so[TH * TW];
+  const int c0 = blockIdx.x * kSX - 1, r0 = blockIdx.y * kSY - 1;
+  const int tid = threadIdx.y * kSX + threadIdx.x;
+  for (int q = tid; q < TW * TH; q += kSX * kSY) {
+    const int rr = r0 + q / TW, cc = c0 + q % TW;
+    uint8_t o = 0;
+    double x = 0.0;
+    if (rr >= 0 && rr < H && cc >= 0 && cc < W) {
+      const int j = rr * W + cc;
+      o = ok[j];
+      if (o) x = v[j];
+    }
+    so[q] = o;
+    sv[q] = x;
+  }
+  __syncthreads();
+  const int r = blockIdx.y * kSY + threadIdx.y, c = blockIdx.x * kSX + threadIdx.x;
+  if (r >= H || c >= W) return;
+  const int i = r * W + c;
+  const int base = threadIdx.y * TW + threadIdx.x;  // window's top-left in the tile
+  const uint8_t oi = so[base + TW + 1];
+  ok_out[i] = oi;
+  if (!oi) {
+    out[i] = v[i];
+    return;
+  }
+  double p[9];
+  bool plain = true;  // nine valid, non-zero, non-NaN values
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int q = base + (k / 3) * TW + (k % 3);
+    p[k] = sv[q];
+    plain = plain && so[q] && p[k] != 0.0 && p[k] == p[k];
+  }
+  if (plain) {
+    cmpSwap(p[1], p[2]); cmpSwap(p[4], p[5]); cmpSwap(p[7], p[8]);
+    cmpSwap(p[0], p[1]); cmpSwap(p[3], p[4]); cmpSwap(p[6], p[7]);
+    cmpSwap(p[1], p[2]); cmpSwap(p[4], p[5]); cmpSwap(p[7], p[8]);
+    cmpSwap(p[0], p[3]); cmpSwap(p[5], p[8]); cmpSwap(p[4], p[7]);
+    cmpSwap(p[3], p[6]); cmpSwap(p[1], p[4]); cmpSwap(p[2], p[5]);
+    cmpSwap(p[4], p[7]); cmpSwap(p[4], p[2]); cmpSwap(p[6], p[4]);
+    cmpSwap(p[4], p[2]);
+    out[i] = p[4];
+    return;
+  }
+  double win[9];
+  int n = 0;
+  for (int k = 0; k < 9; ++k) {
+    const int q = base + (k / 3) * TW + (k % 3);
+    if (so[q]) win[n++] = sv[q];
+  }
+  stl::sort(win, n);  // n <= 9: the library's insertion sort
+  out[i] = (n % 2 == 1) ? win[n / 2] : 0.5 * (win[n / 2 - 1] + win[n / 2]);
+}
+
 template <int R, int KIND>
 __global__ void __launch_bounds__(kSX* kSY) k_stencil_tile(const double* __restrict__ v,
                                                            const uint8_t* __restrict__ ok, int W,
@@ -241,29 +314,39 @@ __global__ void __launch_bounds__(kTileCC* kTileCC)
     if (ok[i]) *any_valid = 1;
     else fg = true;
   }
-  // Tile-local labels by min-propagation with pointer jumping: every cell
-  // takes the smallest label among itself, its 4-neighbours in the tile and
-  // the label its label points at, until no label changes (labels only
-  // decrease and always name a cell of the same component, so the in-place
-  // races are benign). The fixed point is the component's smallest index.
+  // Tile-local labels: each warp is one tile row, so a row's runs of invalid
+  // cells come from one ballot (every cell points at its run's first cell);
+  // runs touching across rows are then joined by a shared-memory union-find
+  // whose hooks always point the larger root at the smaller one, so a
+  // component's root is its smallest index (the first cell of its first
+  // run), as before.
   constexpr int kNone = 1 << 30;
-  lab[t] = fg ? t : kNone;
+  static_assert(kTileCC == 32, "one warp per tile row");
+  const unsigned row = __ballot_sync(0xffffffffu, fg);
+  const unsigned below = tx == 31 ? 0xffffffffu : ((2u << tx) - 1u);  // lanes <= tx
+  const unsigned gaps = ~row & below;
+  const int run = ty * kTileCC + (gaps ? 32 - __clz(gaps) : 0);
+  lab[t] = fg ? run : kNone;
   __syncthreads();
-  while (true) {
-    int changed = 0;
-    if (fg) {
-      int m = lab[t];
-      if (tx > 0) m = min(m, lab[t - 1]);
-      if (tx < kTileCC - 1) m = min(m, lab[t + 1]);
-      if (ty > 0) m = min(m, lab[t - kTileCC]);
-      if (ty < kTileCC - 1) m = min(m, lab[t + kTileCC]);
-      m = min(m, lab[m]);
-      if (m < lab[t]) {
-        lab[t] = m;
-        changed = 1;
-      }
+  // one union per stretch of vertical contact between two runs
+  if (fg && ty > 0 && lab[t - kTileCC] != kNone &&
+      !(tx > 0 && lab[t - 1] != kNone && lab[t - kTileCC - 1] != kNone)) {
+    int a = run, b = lab[t - kTileCC];
+    while (true) {
+      while (lab[a] != a) a = lab[a];
+      while (lab[b] != b) b = lab[b];
+      if (a == b) break;
+      const int hi = a > b ? a : b, lo = a ^ b ^ hi;
+      if (atomicCAS(&lab[hi], hi, lo) == hi) break;
+      a = hi;  // hi was hooked meanwhile: retry from it
+      b = lo;
     }
-    if (!__syncthreads_or(changed)) break;
+  }
+  __syncthreads();
+  if (fg) {
+    int x = run;
+    while (lab[x] != x) x = lab[x];
+    lab[t] = x;  // (only the run starts are roots; other cells are never read above)
   }
   if (!in) return;
   if (!fg) {
@@ -440,7 +523,11 @@ int smoothChainEnqueue(cudaStream_t s, ChainScratch& sc, const double* d_values,
         launchPdl(k_linear, grid, kT, 0, s, cv, co, W, H, st.radius, wt, nv, no);
       ++launches;
     } else if (st.kind == 2) {
-      launchPdl(k_median, grid, kT, 0, s, cv, co, W, H, st.radius, nv, no);
+      if (st.radius == 1 && RB_MEDIAN3)
+        launchPdl(k_median3, dim3((W + kSX - 1) / kSX, (H + kSY - 1) / kSY), dim3(kSX, kSY), 0, s, cv, co,
+                  W, H, nv, no);
+      else
+        launchPdl(k_median, grid, kT, 0, s, cv, co, W, H, st.radius, nv, no);
       ++launches;
     } else {
       const dim3 tiles((W + kTileCC - 1) / kTileCC, (H + kTileCC - 1) / kTileCC);

@@ -13,6 +13,8 @@ m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height)
 for f in range(2):
     for c in w.calls(f):
         m.integrate(pk.sim_render(lib, p, c.pose, c.time, c.seed, c.scan_index), c.pose, 0.1 * f, cfg)
-for i in range(3):
+ts = []
+for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     v, ok = m.smooth_chain("elevation", wl.C5_CHAIN)
-    print("chain ms", lib.relief_gpu_map_chain_seconds(m.handle) * 1e3)
+    ts.append(lib.relief_gpu_map_chain_seconds(m.handle) * 1e3)
+print("chain ms", " ".join(f"{t:.4f}" for t in ts[:3]), "median", f"{np.median(ts[1:] or ts):.4f}")

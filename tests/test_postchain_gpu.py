@@ -61,6 +61,31 @@ def test_chain_matches_reference_random(gpu, reference, steps):
         assert bits_equal(got_v, want_v).all(), np.nanmax(np.abs(got_v - want_v))
 
 
+@pytest.mark.parametrize("radius", [1, 2])
+def test_median_ties_zeros_and_nan(gpu, reference, radius):
+    """Median windows with repeated values, +0 / -0 and NaN among the valid values: which of two
+    equal-comparing values lands on the median rank is decided by the reference's stable insertion
+    sort (std::sort on < 16 elements); the device's 3x3 network path defers such windows to the same
+    insertion order, so values stay bit-exact."""
+    rng = np.random.default_rng(7 + radius)
+    H, W = 40, 70
+    values = rng.integers(-3, 4, (H, W)).astype(np.float64) * 0.25   # many exact ties
+    values[rng.random((H, W)) < 0.15] = -0.0
+    values[rng.random((H, W)) < 0.02] = np.nan
+    valid = (rng.random((H, W)) < 0.85).astype(np.uint8)
+    steps = [(2, radius, 1.0)]
+    got_v, got_ok = pk.smooth_chain(gpu, values, valid, steps)
+    want_v, want_ok = ref_chain(reference, values, valid, steps)
+    assert np.array_equal(got_ok, want_ok)
+    assert bits_equal(got_v, want_v).all()
+    # all-valid smooth layer: the network path on every interior cell
+    smooth = rng.normal(1.0, 0.2, (H, W)).cumsum(axis=0)
+    full = np.ones((H, W), dtype=np.uint8)
+    got_v, _ = pk.smooth_chain(gpu, smooth, full, steps)
+    want_v, _ = ref_chain(reference, smooth, full, steps)
+    assert bits_equal(got_v, want_v).all()
+
+
 def test_nothing_to_inpaint_status(gpu, reference):
     values = np.full((8, 9), np.nan)
     valid = np.zeros((8, 9), dtype=np.uint8)
