@@ -2721,7 +2721,9 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // Graph frames (DeviceMap::graph_mode): with direct launches the device
   // outruns the host's submission on mid-size frames; on tiny frames the
   // capture + update costs more than it saves.
-  const bool graph = !P.use_convnet_traversability &&
+  // (Phase timing: direct launches, so no phase absorbs the wait for the
+  // graph launch of a head-split frame.)
+  const bool graph = !P.use_convnet_traversability && !m.phase_events &&
                      (m.graph_mode == 1 || (m.graph_mode == 2 && N >= kGraphMinPoints));
   const bool graph_head = graph && N >= kGraphHeadPoints;
   // ev0 -> ev13: the input copy (host input only); everything after it is the
