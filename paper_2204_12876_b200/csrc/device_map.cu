@@ -173,6 +173,9 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     m->cls = c.take<uint8_t>(n);
     m->probe = c.take<uint16_t>(np) + guard;
     m->ub2 = c.take<double>(n);
+    m->jw = (grid.width + 7) / 8;  // sized for the smallest jump block (pipeline.cu kJumpBlk)
+    m->jh = (grid.height + 7) / 8;
+    checkCuda(cudaMalloc(&m->jgrid, static_cast<std::size_t>(m->jw) * m->jh * sizeof(uint16_t)), "jump grid");
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");
@@ -197,6 +200,7 @@ void destroyDeviceMap(DeviceMap* m) {
   cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   cudaFree(m->slab);
+  cudaFree(m->jgrid);
   cudaFree(m->islab);
   cudaFree(m->pslab);
   cudaFree(m->rslab);

@@ -127,9 +127,12 @@ struct DeviceMap {
   // kProbeGuardRows padded rows of border words before and after the grid
   // (pass 1's run lookahead may step that far past the border)
   uint16_t* probe = nullptr;
-  static constexpr int kProbeGuardRows = 16;
+  static constexpr int kProbeGuardRows = 40;  // (also the jump grid's rings below the last rows)
   int32_t* kstar = nullptr;
   double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)
+  // pass-1 jump grid (pipeline.cu k_jump_grid): one word per 16 x 16 cells
+  uint16_t* jgrid = nullptr;
+  int jw = 0, jh = 0;
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
   // information-form group frames (allocated on first use, W*H each): the
   // exchanged per-cell partials (sum p/v, sum 1/v, first point, points, first
@@ -277,8 +280,7 @@ struct ShardIO {
   uint32_t* rec_cell = nullptr;     // device, n_records (scan order)
   double* rec_z = nullptr;
   double* rec_var = nullptr;
-  int32_t* kstar = nullptr;
-  double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)   // device, cells: first removing ray per cell
+  int32_t* kstar = nullptr;    // device, cells: first removing ray per cell
   double* ub = nullptr;       // device, cells: upper-bound layer
   uint8_t* ubv = nullptr;     // device, cells: upper-bound validity
   std::size_t cells = 0;

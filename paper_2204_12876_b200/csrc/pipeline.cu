@@ -42,6 +42,9 @@ constexpr int kThreads = 256;
 // Graph frames of at least kGraphMinPoints points (graph_mode 2); from
 // kGraphHeadPoints on, the frame's head is launched directly and only the
 // rest captured (its ingest then covers the capture and graph update).
+#ifndef RB_P1_JUMP
+#define RB_P1_JUMP 1  // pass-1 rays jump over the blocks their heights clear (pass1Jump)
+#endif
 #ifndef RB_GRAPH_MIN_POINTS
 #define RB_GRAPH_MIN_POINTS 32768
 #endif
@@ -702,6 +705,11 @@ struct RayArgs {
   // Per-frame ray constants: the origin lies in the closed map extent, and its
   // cell (the start cell of every ray that is not clipped at its start).
   int origin_in, ocol, orow;
+  // Pass-1 jump grid (k_jump_grid; null: no jumps): one probe word per
+  // kJumpBlk x kJumpBlk block of cells, jw x jh blocks of side jres metres.
+  const uint16_t* jgrid;
+  int jw, jh;
+  double jres;
 };
 
 // Post-fusion ray class per cell; also resets k* (reference raycast.cpp:
@@ -713,6 +721,13 @@ struct RayArgs {
 // those cells are classified "none" up front; k_fuse_heavy flags any heavy
 // cell that fused nothing and the ray pass is then redone (retry = 1: this
 // kernel and pass 1 run only if the flag is set).
+#ifndef RB_P1_JBLK
+#define RB_P1_JBLK 16
+#endif
+constexpr int kJumpBlk = RB_P1_JBLK;  // cells per side of a pass-1 jump block
+constexpr int kJumpShift = kJumpBlk == 8 ? 3 : (kJumpBlk == 16 ? 4 : 5);
+static_assert(kJumpBlk == 8 || kJumpBlk == 16 || kJumpBlk == 32, "jump block");
+
 // Pass-1 probe word of a cell (16 bits): the ray class in the low 2 bits and,
 // above it, an order-preserving key of an f16 bound F >= T of the cell's gate
 // threshold T (T = upper_bound for a bound cell, elevation - sqrt(variance)
@@ -1111,6 +1126,38 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
     classifyCell(L, i, heavy >= 0 && count[i] > heavy, ca, cls, probe, kstar);
 }
 
+// Pass-1 jump grid: per kJumpBlk x kJumpBlk block of cells, the largest probe
+// word over the block and a one-cell ring around it (so a cell the exact walk
+// reaches while the real line runs through a neighbouring block, by rounding
+// at a block edge, is covered), 0xffff (bound NaN: never jumped) when any of
+// those cells is a removal candidate (its rays must be queued, exactly) or
+// the border. One warp per block: lanes 0-17 take the 18 ring columns.
+__global__ void __launch_bounds__(kThreads) k_jump_grid(const ProbeT* __restrict__ probe, int W, int H,
+                                                        uint16_t* __restrict__ jg, int jw, int jh) {
+  pdlWait();
+  pdlTrigger();
+  const int warp = static_cast<int>((blockIdx.x * static_cast<unsigned>(kThreads) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp >= jw * jh) return;
+  const int by = warp / jw, bx = warp - by * jw;
+  uint32_t mx = 0, cand = 0;
+  for (int q = lane; q < kJumpBlk + 2; q += 32) {
+    const int pc = kJumpBlk * bx + q;  // padded column (the ring starts one cell left)
+    if (pc > W + 1) break;
+    // padded rows kJumpBlk*by .. +kJumpBlk+1 (past H + 1: the border guard rows)
+    const ProbeT* p = probe + static_cast<size_t>(kJumpBlk * by) * (W + 2) + pc;
+#pragma unroll 6
+    for (int r = 0; r < kJumpBlk + 2; ++r) {
+      const uint32_t wd = p[static_cast<size_t>(r) * (W + 2)];
+      mx = max(mx, wd);
+      cand |= (wd & 3u) == kClsCandidate ? 1u : 0u;
+    }
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  cand = __reduce_or_sync(0xffffffffu, cand);
+  if (lane == 0) jg[warp] = static_cast<uint16_t>(cand ? 0xffffu : mx);
+}
+
 // Liang-Barsky slab clip (reference raycast.cpp:30-42).
 __device__ __forceinline__ bool clipAxis(double p, double q, double& t0, double& t1) {
   if (p == 0.0) return q >= 0.0;
@@ -1358,11 +1405,11 @@ __device__ __forceinline__ void pass1Visit(const Pass1Ctx& c, uint8_t cl, uint32
 }
 
 #ifdef RB_P1_DIAG
-__device__ unsigned long long g_p1diag[5];
+__device__ unsigned long long g_p1diag[7];
 __global__ void k_p1diag() {
-  printf("P1DIAG fast_runs %llu end_runs %llu gate_runs %llu rays %llu cells %llu\n", g_p1diag[0],
-         g_p1diag[1], g_p1diag[2], g_p1diag[3], g_p1diag[4]);
-  for (int i = 0; i < 5; ++i) g_p1diag[i] = 0;
+  printf("P1DIAG fast_runs %llu end_runs %llu gate_runs %llu rays %llu cells %llu jumped_cells %llu jumps %llu\n",
+         g_p1diag[0], g_p1diag[1], g_p1diag[2], g_p1diag[3], g_p1diag[4], g_p1diag[5], g_p1diag[6]);
+  for (int i = 0; i < 7; ++i) g_p1diag[i] = 0;
 }
 #endif
 #ifndef RB_P1_RUN
@@ -1387,6 +1434,7 @@ struct P1Walk {
   double tmx, tmy, tdx, tdy, t_enter, t1;
   uint32_t idx, end_idx, wd;  // padded cell index, the endpoint's, the cell's probe word
   int step_col, step_row;     // index steps (step_row = +-(W+2))
+  int col, row;               // the cell (pass1Jump only; the walk keeps idx)
 };
 
 // Returns true when the ray has a walk left (the vertical and clipped-out
@@ -1461,6 +1509,8 @@ __device__ __forceinline__ bool pass1Setup(const GridArgs& g, const double o[3],
   w.end_idx = end_idx;
   w.step_col = step_col;
   w.step_row = step_row * static_cast<int>(Wp);
+  w.col = col;
+  w.row = row;
   return true;
 }
 
@@ -1603,6 +1653,118 @@ __device__ __forceinline__ void pass1Walk(P1Walk& w, const Pass1Ctx& c, uint32_t
 #endif
 }
 
+// Jump ahead (RayArgs::jgrid): before its walk, a ray follows its real line
+// through the jump grid (plain fp64, approximate) from the walk's entry time
+// and stops at the first block whose word's bound F is not below the ray's
+// height over the block's time range (less a margin far above any rounding
+// of the walk's crossing times); the cells the exact walk passes before that
+// time lie in the passed blocks or their one-cell rings, so none of them can
+// pass its gate and no candidate is among them. The walk's state is then
+// moved to the last state it enters before that time, exactly: along its
+// primary axis (the smaller t_delta) the reference's running sums
+// t_max += t_delta up to the last crossing before the target, along the
+// other axis the sums that the reference's merge order takes first (ties
+// step y, raycast.cpp:120) -- the state the reference's loop is in when it
+// enters that cell. No compare / select chain per step, no probe loads.
+__device__ __forceinline__ void pass1Jump(P1Walk& w, const Pass1Ctx& c, const RayArgs& a,
+                                          unsigned& visits) {
+  if (!isfinite(c.oz) || !isfinite(c.dz)) return;
+  const int sx = w.step_col, sy = w.step_row > 0 ? 1 : (w.step_row < 0 ? -1 : 0);
+  // The real line's block crossings, from the walk's own cell and crossing
+  // times (blocks are whole cells): the next block face along x is crossed
+  // with the column crossing (bx+1)*B-1-col (resp. col-bx*B) steps after
+  // t_max_x; approximate sums are enough here (see the one-cell rings).
+  int bx = w.col >> kJumpShift, by = w.row >> kJumpShift;
+  double tbx = kInf, tby = kInf, dtbx = kInf, dtby = kInf;
+  if (sx != 0) {
+    tbx = w.tmx + (sx > 0 ? (bx + 1) * kJumpBlk - 1 - w.col : w.col - bx * kJumpBlk) * w.tdx;
+    dtbx = kJumpBlk * w.tdx;
+  }
+  if (sy != 0) {
+    tby = w.tmy + (sy > 0 ? (by + 1) * kJumpBlk - 1 - w.row : w.row - by * kJumpBlk) * w.tdy;
+    dtby = kJumpBlk * w.tdy;
+  }
+  const double t1 = w.t1;
+  const double hm = 1e-9 * (fabs(c.oz) + fabs(c.dz)) + 1e-12;
+  double ha = c.oz + w.t_enter * c.dz, t_stop = w.t_enter;
+#pragma unroll 1
+  for (int k = 0; k < 512; ++k) {
+    const double tb = fmin(fmin(tbx, tby), t1);
+    const double hb = c.oz + tb * c.dz;
+    const uint32_t wd = a.jgrid[by * a.jw + bx];
+    if (wd != 0u && !((ha < hb ? ha : hb) - hm >= probeBound(wd))) break;
+    t_stop = tb;
+    if (!(tb < t1)) break;
+    if (tbx < tby) {
+      bx += sx;
+      tbx += dtbx;
+      if (static_cast<unsigned>(bx) >= static_cast<unsigned>(a.jw)) break;
+    } else {
+      by += sy;
+      tby += dtby;
+      if (static_cast<unsigned>(by) >= static_cast<unsigned>(a.jh)) break;
+    }
+    ha = hb;
+  }
+  const double tt = t_stop - 1e-9;  // states entered before tt are skipped
+  if (!(tt > w.t_enter)) return;
+  // The running sums: a blind stretch two steps shorter than the real-valued
+  // count (whose error is far below one step), no compares, then the exact
+  // stop by comparison.
+  const int lim_x = a.g.W + 2, lim_y = a.g.H + 2;  // the walk stays in the grid: fewer steps
+  double tmx = w.tmx, tmy = w.tmy, last = w.t_enter;
+  int di = 0, dj = 0;
+  const bool xp = w.tdx <= w.tdy;
+  {
+    double& tp = xp ? tmx : tmy;
+    const double tdp = xp ? w.tdx : w.tdy;
+    int& np = xp ? di : dj;
+    const int lim = xp ? lim_x : lim_y;
+    int blind = static_cast<int>(fmin((tt - tp) * (1.0 / tdp), static_cast<double>(lim))) - 2;
+#pragma unroll 4
+    for (int k = 0; k < blind; ++k) tp += tdp;
+    np = blind > 0 ? blind : 0;
+    while (tp < tt && np < lim) {
+      last = tp;
+      tp += tdp;
+      ++np;
+    }
+    if (np == 0 || np >= lim) return;
+  }
+  {
+    double& ts = xp ? tmy : tmx;
+    const double tds = xp ? w.tdy : w.tdx;
+    int& ns = xp ? dj : di;
+    const int lim = xp ? lim_y : lim_x;
+    int blind = static_cast<int>(fmin((last - ts) * (1.0 / tds), static_cast<double>(lim))) - 2;
+#pragma unroll 4
+    for (int k = 0; k < blind; ++k) ts += tds;
+    ns = blind > 0 ? blind : 0;
+    // x steps before a y crossing only if strictly earlier (ties step y)
+    if (xp) {
+      while (ts <= last && ns < lim) {
+        ts += tds;
+        ++ns;
+      }
+    } else {
+      while (ts < last && ns < lim) {
+        ts += tds;
+        ++ns;
+      }
+    }
+    if (ns >= lim) return;
+  }
+  w.tmx = tmx;
+  w.tmy = tmy;
+  w.t_enter = last;
+  w.idx = static_cast<uint32_t>(static_cast<int>(w.idx) + di * w.step_col + dj * w.step_row);
+  visits += static_cast<unsigned>(di + dj);
+#ifdef RB_P1_DIAG
+  atomicAdd(&g_p1diag[5], static_cast<unsigned long long>(di + dj));
+  atomicAdd(&g_p1diag[6], 1ull);
+#endif
+}
+
 // 128-thread blocks, 9 per SM: 56 registers (no spills in the DDA loop) at 36
 // resident warps (256 x 5 at 48 registers spilled the step increments).
 #ifndef RB_PASS1_MIN_BLOCKS
@@ -1648,6 +1810,7 @@ __device__ __forceinline__ void pass1Tile(uint32_t k0, uint32_t n, const uint8_t
   // Every thread is past the wait before the walk (class / probe words come
   // from the classification) and the counters.
   pdlWait();
+  if (walking && a.jgrid != nullptr) pass1Jump(w, c, a, visits);
   if (walking) w.wd = probe[w.idx];
   pass1Walk(w, c, static_cast<uint32_t>(a.g.W), walking, touched, visits);
   // Queue rays that crossed a removal candidate for the k* pass (one atomic per warp).
@@ -2299,6 +2462,9 @@ RayArgs rayArgs(const Frame& f) {
   ra.bound = f.P.cleanup.upper_bound_enabled;
   const GridArgs& g = f.g;
   ra.origin_in = ra.o[0] >= g.ox && ra.o[0] <= g.xmax && ra.o[1] >= g.oy && ra.o[1] <= g.ymax;
+  ra.jgrid = nullptr;
+  ra.jw = ra.jh = 0;
+  ra.jres = 0.0;
   auto clampc = [](int v, int n) { return v < 0 ? 0 : (v > n - 1 ? n - 1 : v); };
   ra.ocol = clampc(x86_to_int(std::floor((ra.o[0] - g.ox) / g.res)), g.W);
   ra.orow = clampc(x86_to_int(std::floor((ra.o[1] - g.oy) / g.res)), g.H);
@@ -2436,8 +2602,19 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base, bool tail = false) 
       ++f.launches;
     }
     if (N > 0) {
+      RayArgs rj = ra;
+      if (RB_P1_JUMP) {  // the jump grid of this frame's probe words (pass1Jump)
+        const int jw = (f.g.W + kJumpBlk - 1) / kJumpBlk, jh = (f.g.H + kJumpBlk - 1) / kJumpBlk;
+        launchPdl(k_jump_grid, static_cast<unsigned>((static_cast<std::size_t>(jw) * jh * 32 + kThreads - 1) / kThreads),
+                  kThreads, 0, s, static_cast<const ProbeT*>(m.probe), f.g.W, f.g.H, m.jgrid, jw, jh);
+        ++f.launches;
+        rj.jgrid = m.jgrid;
+        rj.jw = jw;
+        rj.jh = jh;
+        rj.jres = kJumpBlk * f.g.res;
+      }
       launchPdl(k_rays_pass1<false>, gridFor(N, kP1Threads), kP1Threads, 0, s, N, m.kept + f.ray_at,
-                m.px + f.ray_at, m.py + f.ray_at, m.pz + f.ray_at, ra, m.cur, m.cls, m.kstar,
+                m.px + f.ray_at, m.py + f.ray_at, m.pz + f.ray_at, rj, m.cur, m.cls, m.kstar,
                 m.raylist, m.stats, 0, ray_base, m.probe, f.point_cells);
       ++f.launches;
 #ifdef RB_P1_DIAG

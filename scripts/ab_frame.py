@@ -1,8 +1,8 @@
 """A/B of whole-frame device time across library builds (no phase events, L2 flushed per frame).
 
 Usage (GPU box): python scripts/ab_frame.py default ab/NAME ... [--workloads C4,headline,C3,C1]
-Prints, per build and workload, the median device ms per frame over 20 frames (after 5 warm-up
-frames) and the stats of the last frame (which must agree across builds).
+Prints, per build and workload, the median device ms per frame over the last 20 of AB_FRAMES
+frames (default 25) and the stats of the last frame (which must agree across builds).
 """
 import os
 import statistics
@@ -31,13 +31,13 @@ for name in WL:
     torch.cuda.synchronize()
     m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height)
     ts = []
-    for s in range(25):
+    for s in range(NFR):
         flush.zero_(); torch.cuda.synchronize()
         dev = 0.0
         for t, c in frames[s % 8]:
             st = m.integrate_device(t.data_ptr(), t.shape[0], c.pose, 0.1 * s, cfg)
             dev += m.kernel_seconds()[7]
-        if s >= 5:
+        if s >= NFR - 20:
             ts.append(dev)
     out[name] = {"ms": statistics.median(ts) * 1e3, "min": min(ts) * 1e3,
                  "stats": [st.points_fused, st.cells_updated, st.cells_removed_by_cleanup, st.points_rejected_outlier]}
@@ -58,6 +58,7 @@ def main():
             if v != "default":
                 env["RELIEF_B200_LIB"] = os.path.join(ROOT, v, "librelief_b200.so")
             code = CHILD.replace("ROOT", repr(ROOT), 1).replace("WL", repr(wl.split(",")), 1)
+            code = code.replace("NFR", os.environ.get("AB_FRAMES", "25"))  # median over the last 20
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env)
             if os.environ.get("AB_DUMP"):  # keep the child's output (e.g. a diag build's counters)
                 with open(os.environ["AB_DUMP"], "a") as fh:
