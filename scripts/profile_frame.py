@@ -11,7 +11,7 @@ import paper_2204_12876_b200 as pk  # noqa: E402
 from paper_2204_12876_b200 import workloads as wl  # noqa: E402
 
 
-def main(name: str = "headline", warm: int = 3, frames: int = 1) -> None:
+def main(name: str = "headline", warm: int = 3, frames: int = 1, distinct: int = 2) -> None:
     lib = pk.load_library()
     w = wl.ALL[name]()
     d = Path(tempfile.mkdtemp())
@@ -20,13 +20,14 @@ def main(name: str = "headline", warm: int = 3, frames: int = 1) -> None:
     cfg = pk.Config.load(lib, cfgp)
     m = pk.ReliefMap.create(lib, w.resolution, w.width, w.height)
     clouds = [[(pk.sim_render(lib, cfgp, c.pose, c.time, c.seed, c.scan_index), c) for c in w.calls(f)]
-              for f in range(2)]
+              for f in range(distinct)]
     for f in range(warm + frames):
-        for xyz, c in clouds[f % 2]:
+        for xyz, c in clouds[f % distinct]:
             m.integrate(xyz, c.pose, 0.1 * f, cfg)
     print("launches/frame", m.last_launches(), "kernel_seconds", list(m.kernel_seconds()))
 
 
 if __name__ == "__main__":
     a = sys.argv[1:]
-    main(a[0] if a else "headline", int(a[1]) if len(a) > 1 else 3, int(a[2]) if len(a) > 2 else 1)
+    main(a[0] if a else "headline", int(a[1]) if len(a) > 1 else 3, int(a[2]) if len(a) > 2 else 1,
+         int(a[3]) if len(a) > 3 else 2)
