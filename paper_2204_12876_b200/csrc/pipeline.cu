@@ -1090,8 +1090,16 @@ __global__ void __launch_bounds__(32)
       checkSpeculation(L, i, a, t_free, cleanup, bound, st);
     }
   }
+  // The other long cells, one per lane, on the blocks that had no very long
+  // cell (a very long cell's fold is the kernel's critical path: its block
+  // takes no further work unless every block had one).
   const unsigned total = static_cast<unsigned>(st_in->heavy_cells);
-  for (unsigned q = blockIdx.x * 32 + lane; q < total; q += gridDim.x * 32) {
+  const unsigned busy = nv < gridDim.x ? nv : 0u;
+  if (blockIdx.x < busy) {
+    flushCounts(k, st);
+    return;
+  }
+  for (unsigned q = (blockIdx.x - busy) * 32 + lane; q < total; q += (gridDim.x - busy) * 32) {
     const uint32_t i = list[q];
     foldCell(L, i, count[i], start, spz, spv, a, st, k);
     checkSpeculation(L, i, a, t_free, cleanup, bound, st);
