@@ -59,6 +59,7 @@ L2_FLUSH_BYTES = 256 << 20
 DEVSTATS_BYTES = 128  # DevStats read back per scan (device_map.hpp)
 N_FRAMES = 8          # distinct frames cycled by both arms
 # gates that cannot fire: the configuration the information-form group mode requires
+PRE_FRAMES = 40  # steady-state leg: frames integrated before its warm-up (untimed)
 UNGATED = "update.mahalanobis_threshold = 1e12\nupdate.wall_count_threshold = 1073741824\n"
 CONFIG_NAMES = ("C1", "C2", "C3", "headline", "C4", "C5")
 LAYERS = ("elevation", "variance", "last_update", "upper_bound", "upper_bound_valid", "traversability",
@@ -431,6 +432,26 @@ def single_gpu_legs(lib, D, name, steps, warmup, local_rank, want_roofline=True,
         out["post_chain_ms"] = statistics.median(ct[1:]) * 1e3
     m.close()
 
+    # steady state: the same timed protocol on a map that has already integrated PRE_FRAMES frames
+    # (untimed), as a mapper that has been running for a few seconds; pass 1's jumps clear most of
+    # the rays' cells only once the map's bounds have settled
+    if want_stream:
+        m4 = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
+        for s in range(PRE_FRAMES + warmup):
+            run_device(m4, s)
+        D.barrier()
+        st_t = []
+        for s in range(PRE_FRAMES + warmup, PRE_FRAMES + warmup + steps):
+            D.flush_l2()
+            st_t.append(run_device(m4, s)[0])
+        D.barrier()
+        st_total = D.max(sum(st_t))
+        out["steady_state"] = {"value": pts * steps / st_total, "unit": "points/s",
+                               "ms_per_frame": st_total / steps * 1e3, "pre_frames": PRE_FRAMES,
+                               "note": f"same steps / warm-up / L2 flush as value, on a map that integrated "
+                                       f"{PRE_FRAMES} earlier frames of the same sequence (untimed)"}
+        m4.close()
+
     # e2e: drop-in C ABI, pinned host input (and pageable)
     def e2e(frames_src, label):
         m2 = pk.ReliefMap.create(lib, w.resolution, w.width, w.height, device=local_rank)
@@ -715,6 +736,7 @@ def run_b200(args, rank, world, local_rank):
                             "on (they end the programmatic overlap at the phase boundaries); value and "
                             "ms_per_step are timed without them",
         "e2e": main["e2e"], "e2e_pageable": main["e2e_pageable"], "e2e_streaming": main.get("e2e_streaming"),
+        "steady_state": main.get("steady_state"),
         "gpu_launches": main["gpu_launches"], "roofline": main.get("roofline"),
         "cpu_baseline": cpu, "clocks": clocks.summary(), "configs": configs,
     }
