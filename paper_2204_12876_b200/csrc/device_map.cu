@@ -175,7 +175,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     m->ub2 = c.take<double>(n);
     m->jw = (grid.width + 7) / 8;  // sized for the smallest jump block (pipeline.cu kJumpBlk)
     m->jh = (grid.height + 7) / 8;
-    checkCuda(cudaMalloc(&m->jgrid, static_cast<std::size_t>(m->jw) * m->jh * sizeof(uint16_t)), "jump grid");
+    checkCuda(cudaMalloc(&m->jgrid, static_cast<std::size_t>(m->jw) * m->jh * sizeof(float)), "jump grid");
     checkCuda(cudaMalloc(&m->stats, sizeof(DevStats)), "stats allocation");
     checkCuda(cudaMalloc(&m->drift_offset, sizeof(double)), "offset allocation");
     checkCuda(cudaMallocHost(&m->h_stats, sizeof(DevStats)), "pinned stats");

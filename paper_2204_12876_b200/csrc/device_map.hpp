@@ -131,7 +131,7 @@ struct DeviceMap {
   int32_t* kstar = nullptr;
   double* ub2 = nullptr;      // upper bounds of cells removed this frame (+inf between frames)
   // pass-1 jump grid (pipeline.cu k_jump_grid): one word per 16 x 16 cells
-  uint16_t* jgrid = nullptr;
+  float* jgrid = nullptr;
   int jw = 0, jh = 0;
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
   // information-form group frames (allocated on first use, W*H each): the

@@ -707,7 +707,7 @@ struct RayArgs {
   int origin_in, ocol, orow;
   // Pass-1 jump grid (k_jump_grid; null: no jumps): one probe word per
   // kJumpBlk x kJumpBlk block of cells, jw x jh blocks of side jres metres.
-  const uint16_t* jgrid;
+  const float* jgrid;
   int jw, jh;
   double jres;
 };
@@ -1141,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
 // those cells is a removal candidate (its rays must be queued, exactly) or
 // the border. One warp per block: lanes 0-17 take the 18 ring columns.
 __global__ void __launch_bounds__(kThreads) k_jump_grid(const ProbeT* __restrict__ probe, int W, int H,
-                                                        uint16_t* __restrict__ jg, int jw, int jh) {
+                                                        float* __restrict__ jg, int jw, int jh) {
   pdlWait();
   pdlTrigger();
   const int warp = static_cast<int>((blockIdx.x * static_cast<unsigned>(kThreads) + threadIdx.x) >> 5);
@@ -1163,7 +1163,14 @@ __global__ void __launch_bounds__(kThreads) k_jump_grid(const ProbeT* __restrict
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   cand = __reduce_or_sync(0xffffffffu, cand);
-  if (lane == 0) jg[warp] = static_cast<uint16_t>(cand ? 0xffffu : mx);
+  // the block's bound as f32: -inf (no class cell), F of the largest word
+  // (an f16 value, exact in f32), +inf for a candidate / the border / NaN
+  if (lane == 0) {
+    float b = -__int_as_float(0x7f800000);
+    if (cand || mx == 0xffffu) b = __int_as_float(0x7f800000);
+    else if (mx != 0u) b = static_cast<float>(probeBound(mx));
+    jg[warp] = b == b ? b : __int_as_float(0x7f800000);
+  }
 }
 
 // Liang-Barsky slab clip (reference raycast.cpp:30-42).
@@ -1699,8 +1706,10 @@ __device__ __forceinline__ void pass1Jump(P1Walk& w, const Pass1Ctx& c, const Ra
   for (int k = 0; k < 512; ++k) {
     const double tb = fmin(fmin(tbx, tby), t1);
     const double hb = c.oz + tb * c.dz;
-    const uint32_t wd = a.jgrid[by * a.jw + bx];
-    if (wd != 0u && !((ha < hb ? ha : hb) - hm >= probeBound(wd))) break;
+    // the block's smallest height less the margin, rounded down to f32, must
+    // reach the block's bound (an f32 value)
+    const float fb = __ldg(a.jgrid + by * a.jw + bx);
+    if (!(__double2float_rd((ha < hb ? ha : hb) - hm) >= fb)) break;
     t_stop = tb;
     if (!(tb < t1)) break;
     if (tbx < tby) {
@@ -1718,50 +1727,52 @@ __device__ __forceinline__ void pass1Jump(P1Walk& w, const Pass1Ctx& c, const Ra
   if (!(tt > w.t_enter)) return;
   // The running sums: a blind stretch two steps shorter than the real-valued
   // count (whose error is far below one step), no compares, then the exact
-  // stop by comparison.
+  // stop by comparison. Primary axis = the one with more crossings (smaller
+  // t_delta); each axis' code is written out (no per-step select between them).
   const int lim_x = a.g.W + 2, lim_y = a.g.H + 2;  // the walk stays in the grid: fewer steps
   double tmx = w.tmx, tmy = w.tmy, last = w.t_enter;
   int di = 0, dj = 0;
-  const bool xp = w.tdx <= w.tdy;
-  {
-    double& tp = xp ? tmx : tmy;
-    const double tdp = xp ? w.tdx : w.tdy;
-    int& np = xp ? di : dj;
-    const int lim = xp ? lim_x : lim_y;
-    int blind = static_cast<int>(fmin((tt - tp) * (1.0 / tdp), static_cast<double>(lim))) - 2;
+  const double tdx = w.tdx, tdy = w.tdy;
+  if (tdx <= tdy) {
+    const int bx0 = static_cast<int>(fmin((tt - tmx) * (1.0 / tdx), static_cast<double>(lim_x))) - 2;
 #pragma unroll 4
-    for (int k = 0; k < blind; ++k) tp += tdp;
-    np = blind > 0 ? blind : 0;
-    while (tp < tt && np < lim) {
-      last = tp;
-      tp += tdp;
-      ++np;
+    for (int k = 0; k < bx0; ++k) tmx += tdx;
+    di = bx0 > 0 ? bx0 : 0;
+    while (tmx < tt && di < lim_x) {
+      last = tmx;
+      tmx += tdx;
+      ++di;
     }
-    if (np == 0 || np >= lim) return;
-  }
-  {
-    double& ts = xp ? tmy : tmx;
-    const double tds = xp ? w.tdy : w.tdx;
-    int& ns = xp ? dj : di;
-    const int lim = xp ? lim_y : lim_x;
-    int blind = static_cast<int>(fmin((last - ts) * (1.0 / tds), static_cast<double>(lim))) - 2;
+    if (di == 0 || di >= lim_x) return;
+    const int by0 = static_cast<int>(fmin((last - tmy) * (1.0 / tdy), static_cast<double>(lim_y))) - 2;
 #pragma unroll 4
-    for (int k = 0; k < blind; ++k) ts += tds;
-    ns = blind > 0 ? blind : 0;
-    // x steps before a y crossing only if strictly earlier (ties step y)
-    if (xp) {
-      while (ts <= last && ns < lim) {
-        ts += tds;
-        ++ns;
-      }
-    } else {
-      while (ts < last && ns < lim) {
-        ts += tds;
-        ++ns;
-      }
+    for (int k = 0; k < by0; ++k) tmy += tdy;
+    dj = by0 > 0 ? by0 : 0;
+    while (tmy <= last && dj < lim_y) {  // ties step y first
+      tmy += tdy;
+      ++dj;
     }
-    if (ns >= lim) return;
+  } else {
+    const int by0 = static_cast<int>(fmin((tt - tmy) * (1.0 / tdy), static_cast<double>(lim_y))) - 2;
+#pragma unroll 4
+    for (int k = 0; k < by0; ++k) tmy += tdy;
+    dj = by0 > 0 ? by0 : 0;
+    while (tmy < tt && dj < lim_y) {
+      last = tmy;
+      tmy += tdy;
+      ++dj;
+    }
+    if (dj == 0 || dj >= lim_y) return;
+    const int bx0 = static_cast<int>(fmin((last - tmx) * (1.0 / tdx), static_cast<double>(lim_x))) - 2;
+#pragma unroll 4
+    for (int k = 0; k < bx0; ++k) tmx += tdx;
+    di = bx0 > 0 ? bx0 : 0;
+    while (tmx < last && di < lim_x) {  // x steps first only if strictly earlier
+      tmx += tdx;
+      ++di;
+    }
   }
+  if (di >= lim_x || dj >= lim_y) return;  // (absorbed increments: leave it to the walk)
   w.tmx = tmx;
   w.tmy = tmy;
   w.t_enter = last;
