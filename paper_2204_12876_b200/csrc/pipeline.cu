@@ -1701,24 +1701,31 @@ __device__ __forceinline__ void pass1Jump(P1Walk& w, const Pass1Ctx& c, const Ra
   }
   const double t1 = w.t1;
   const double hm = 1e-9 * (fabs(c.oz) + fabs(c.dz)) + 1e-12;
+  // the block's smallest height: at its exit when the ray falls, its entry
+  // when it rises (the computed height is monotone in t)
+  const bool down = c.dz < 0.0;
   double ha = c.oz + w.t_enter * c.dz, t_stop = w.t_enter;
+  const float* jp = a.jgrid + by * a.jw + bx;
+  const int jstep = sy * a.jw;
 #pragma unroll 1
-  for (int k = 0; k < 512; ++k) {
-    const double tb = fmin(fmin(tbx, tby), t1);
+  while (true) {
+    const double tm = tbx < tby ? tbx : tby;
+    const double tb = tm < t1 ? tm : t1;
     const double hb = c.oz + tb * c.dz;
-    // the block's smallest height less the margin, rounded down to f32, must
-    // reach the block's bound (an f32 value)
-    const float fb = __ldg(a.jgrid + by * a.jw + bx);
-    if (!(__double2float_rd((ha < hb ? ha : hb) - hm) >= fb)) break;
+    // the smallest height less the margin, rounded down to f32, must reach
+    // the block's bound (an f32 value)
+    if (!(__double2float_rd((down ? hb : ha) - hm) >= __ldg(jp))) break;
     t_stop = tb;
     if (!(tb < t1)) break;
     if (tbx < tby) {
       bx += sx;
       tbx += dtbx;
+      jp += sx;
       if (static_cast<unsigned>(bx) >= static_cast<unsigned>(a.jw)) break;
     } else {
       by += sy;
       tby += dtby;
+      jp += jstep;
       if (static_cast<unsigned>(by) >= static_cast<unsigned>(a.jh)) break;
     }
     ha = hb;
