@@ -666,12 +666,15 @@ def run_b200(args, rank, world, local_rank):
         raise RuntimeError(f"rank {rank}: CUDA device {local_rank} not visible (no CPU fallback)")
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    # RB_BENCH_GROUP=1: the N > 1 legs (group frames over NCCL) even on one rank -- a smoke run of
+    # that code path on a single GPU (torchrun --nproc-per-node 1)
+    group = world > 1 or os.environ.get("RB_BENCH_GROUP") == "1"
+    if group:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     D = Device(local_rank, dist)
 
-    if world > 1:
+    if group:
         w, main, nf = sharded_legs(lib, D, args, rank, world, local_rank, dist)
         result = None
         if rank == 0:
