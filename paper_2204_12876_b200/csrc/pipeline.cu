@@ -72,6 +72,14 @@ __device__ __forceinline__ T warpSum(T v) {
 // Radix-sort tile geometry (K2): kTile consecutive keys per tile.
 constexpr int kSortItems = 8;
 constexpr int kTile = kThreads * kSortItems;
+static_assert(kTile == 2048, "tshift 11");
+// Small frames (RB_SMALL_TILE_N keys or fewer, single-map frames): 512-key tiles.
+#ifndef RB_SMALL_TILE_N
+#define RB_SMALL_TILE_N 600000
+#endif
+constexpr uint32_t kSmallTileN = RB_SMALL_TILE_N;
+constexpr int kSmallTile = 512;
+constexpr uint32_t kSmallTileShift = 9;
 
 // Tile digit count tc[d * pitch + tile] += 1 for every lane with ok, one
 // atomic per (digit, tile) run in the warp; every lane must call.
@@ -260,6 +268,7 @@ struct IngestArgs {
   int drift_min_points;
   double drift_max_off;
   double* drift_offset;
+  uint32_t tshift;  // log2 of the sort tile (SortGeom::tshift)
 };
 
 // Per point (reference integration.cpp:85-113,134-140; sensing.cpp:32-41;
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(kThreads)
   if (count_cells) {
     const unsigned peers = __match_any_sync(0xffffffffu, cell);
     if (cell < WH && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&count[cell], __popc(peers));
-    countTileDigit(tc0, pitch, cell & dmask, k / kTile, cell < WH);
+    countTileDigit(tc0, pitch, cell & dmask, k >> a.tshift, cell < WH);
   }
 
   // Fixed-shape block reduction: deterministic drift partial per block.
@@ -563,6 +572,7 @@ __global__ void __launch_bounds__(kThreads)
 struct SortGeom {
   int passes = 0, dbits = 0;
   uint32_t ntiles = 0;  // tiles of the N input keys (bounds every pass)
+  uint32_t tshift = 11; // log2 of the tile (kTile keys, or kSmallTile for small frames)
   uint32_t pitch = 0;   // row pitch of tc (ntiles rounded up to 4)
   uint32_t* tc = nullptr;      // [passes][buckets][pitch]
   uint32_t* rowsum = nullptr;  // [passes][buckets]
@@ -598,6 +608,7 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) rowsum[blockIdx.x] = carry;
 }
 
+template <int kItems>
 __global__ void __launch_bounds__(kThreads)
     k_sort_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                    uint32_t n_in, int pass, SortGeom sg, uint32_t sentinel,
@@ -640,11 +651,12 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   uint16_t* my = wcnt + warp * buckets;
   const unsigned lt = (1u << lane) - 1u;
-  const uint32_t wbase = tile * kTile + warp * (kTile / 8);
-  uint32_t key[kSortItems], val[kSortItems];
-  uint16_t rank[kSortItems];
+  constexpr uint32_t kT = kThreads * kItems;  // this instantiation's tile (1 << sg.tshift)
+  const uint32_t wbase = tile * kT + warp * (kT / 8);
+  uint32_t key[kItems], val[kItems];
+  uint16_t rank[kItems];
 #pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
+  for (int r = 0; r < kItems; ++r) {
     const uint32_t idx = wbase + r * 32 + lane;
     key[r] = idx < n ? keys_in[idx] : sentinel;
     const bool ok = key[r] < sentinel;
@@ -671,7 +683,7 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   uint32_t* tc_next = last ? nullptr : sg.counts(pass + 1);
 #pragma unroll
-  for (int r = 0; r < kSortItems; ++r) {
+  for (int r = 0; r < kItems; ++r) {
     const bool ok = key[r] < sentinel;
     const uint32_t d = (key[r] >> shift) & mask;
     const uint32_t pos = ok ? offs[d] + my[d] + rank[r] : 0u;
@@ -680,7 +692,7 @@ __global__ void __launch_bounds__(kThreads)
         keys_out[pos] = key[r];
         vals_out[pos] = val[r];
       }
-      countTileDigit(tc_next, sg.pitch, (key[r] >> (shift + dbits)) & mask, pos / kTile, ok);
+      countTileDigit(tc_next, sg.pitch, (key[r] >> (shift + dbits)) & mask, pos >> sg.tshift, ok);
     } else {
       if (ok) {
         // Final pass: the fusion payload in (cell, scan order) order.
@@ -2320,6 +2332,7 @@ struct Frame {
   // instead of a D2H copy + stream synchronisation (synchronous frames whose
   // last kernel is k_cells).
   bool handover = false;
+  bool small_tiles = false;  // sortGeometry's small-frame tiles (single-map frames)
   int heavy = INT_MAX;
   Frame(DeviceMap& map, const PipelineParams& params, const Pose& p, double st, double d)
       : m(map), P(params), pose(p), stamp(st), dt(d), s(map.stream), ncell(map.grid.cells()),
@@ -2408,13 +2421,17 @@ const double* phaseUploadChunked(Frame& f, const double* xyz, uint32_t N) {
 
 // K2 geometry for N keys: 1-3 LSD passes over the bits of the cell id. The
 // tile digit counts are accumulated upstream, so they are zeroed here.
-SortGeom sortGeometry(DeviceMap& m, uint32_t WH, uint32_t N) {
+// small: a single-map frame of fewer than kSmallTileN keys sorts in tiles of
+// kSmallTile keys (more blocks for the GPU's SMs; the per-tile ranking chain
+// is 4x shorter).
+SortGeom sortGeometry(DeviceMap& m, uint32_t WH, uint32_t N, bool small = false) {
   SortGeom sg;
   if (N == 0) return sg;
   const int bits = 32 - __builtin_clz(WH);
   sg.passes = bits <= 11 ? 1 : (bits <= 22 ? 2 : 3);
   sg.dbits = (bits + sg.passes - 1) / sg.passes;
-  sg.ntiles = (N + kTile - 1) / kTile;
+  sg.tshift = (small && N < kSmallTileN) ? kSmallTileShift : 11u;
+  sg.ntiles = (N + (1u << sg.tshift) - 1) >> sg.tshift;
   sg.pitch = (sg.ntiles + 3) & ~3u;
   const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
   const std::size_t need = tcn + static_cast<std::size_t>(sg.passes) * sg.buckets();
@@ -2430,7 +2447,7 @@ SortGeom sortGeometry(DeviceMap& m, uint32_t WH, uint32_t N) {
 }
 
 SortGeom phaseSortGeometry(Frame& f, uint32_t N) {
-  const SortGeom sg = sortGeometry(f.m, f.WH, N);
+  const SortGeom sg = sortGeometry(f.m, f.WH, N, f.small_tiles);
   if (N == 0) return sg;
   const std::size_t tcn = static_cast<std::size_t>(sg.passes) * sg.buckets() * sg.pitch;
   checkCuda(cudaMemsetAsync(sg.tc, 0, tcn * sizeof(uint32_t), f.s), "memset");
@@ -2465,6 +2482,7 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   ia.drift_min_points = f.P.drift.min_points;
   ia.drift_max_off = f.P.drift.max_offset_per_scan;
   ia.drift_offset = m.drift_offset;
+  ia.tshift = sg.tshift;
   if (ia.drift_blocks) f.fuse_offset = m.drift_offset;  // applied by k_fuse (phaseSortFuse)
   const uint32_t chunk = chunked ? chunkPoints(N) : N;
   for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
@@ -2540,8 +2558,9 @@ void phaseSort(Frame& f, const uint32_t* keys, uint32_t N, const double* z, cons
   for (int p = 0; p < sg.passes; ++p) {
     launchPdl(k_sort_rowscan, sg.buckets(), kThreads, 0, s, sg.counts(p), sg.pitch,
                                                      sg.rowsum + p * sg.buckets());
-    launchPdl(k_sort_scatter, sg.ntiles, kThreads, sc_smem, s, kin, vin, N, p, sg, f.WH, kout, vout, z, var,
-                                                        m.spz, m.spv, m.start);
+    launchPdl(sg.tshift == kSmallTileShift ? k_sort_scatter<kSmallTile / kThreads> : k_sort_scatter<kSortItems>,
+              sg.ntiles, kThreads, sc_smem, s, kin, vin, N, p, sg, f.WH, kout, vout, z, var, m.spz, m.spv,
+              m.start);
     f.launches += 2;
     // ping-pong between key1 and key0 (key0 is free once pass 0 has read it)
     const uint32_t* next_in = kout;
@@ -2916,7 +2935,8 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   // Scratch first: nothing may allocate inside a graph capture.
   if (n > 0) {
     phaseScratch(f, n);
-    sortGeometry(m, f.WH, N);
+    f.small_tiles = RB_SMALL_TILE_N > 0;
+    sortGeometry(m, f.WH, N, f.small_tiles);
   }
   // Pageable host input cannot be a graph's copy source: it is uploaded
   // before the capture (the frame then reads it like device input).
@@ -3073,6 +3093,7 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   }
   Frame f(m, P, pose, stamp, dt);
   const uint32_t N = static_cast<uint32_t>(n);
+  f.small_tiles = RB_SMALL_TILE_N > 0;
   phaseBegin(f);
   phaseScratch(f, n);
   double* d_xyz = m.xyz_slot[slot];
