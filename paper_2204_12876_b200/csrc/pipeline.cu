@@ -80,6 +80,14 @@ static_assert(kTile == 2048, "tshift 11");
 constexpr uint32_t kSmallTileN = RB_SMALL_TILE_N;
 constexpr int kSmallTile = 512;
 constexpr uint32_t kSmallTileShift = 9;
+// Sorts of at most kFusedTiles tiles scan the tile counts inside the scatter.
+#ifndef RB_FUSED_ROWSCAN
+#define RB_FUSED_ROWSCAN 1
+#endif
+#ifndef RB_FUSED_TILES
+#define RB_FUSED_TILES 48
+#endif
+constexpr uint32_t kFusedTiles = RB_FUSED_TILES;
 
 // Tile digit count tc[d * pitch + tile] += 1 for every lane with ok, one
 // atomic per (digit, tile) run in the warp; every lane must call.
@@ -608,7 +616,10 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) rowsum[blockIdx.x] = carry;
 }
 
-template <int kItems>
+// kFused: the row scans are done here (frames of at most kFusedTiles tiles):
+// each block sums its digits' rows itself, which saves the k_sort_rowscan
+// launch of every pass.
+template <int kItems, bool kFused = false>
 __global__ void __launch_bounds__(kThreads)
     k_sort_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                    uint32_t n_in, int pass, SortGeom sg, uint32_t sentinel,
@@ -633,17 +644,39 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t nkeys;
   {
     const int per = (buckets + kThreads - 1) / kThreads;
+    constexpr int kMaxPer = 8;  // buckets <= 2048 (11-bit digits)
+    uint32_t row_total[kMaxPer], before[kMaxPer];
     uint32_t loc = 0;
     for (int j = 0; j < per; ++j) {
       const int d = threadIdx.x * per + j;
-      if (d < buckets) loc += rowsum[d];
+      uint32_t t = 0, b = 0;
+      if (d < buckets) {
+        if (kFused) {  // the digit's row: counts of all tiles, and of the tiles before this one
+          const uint4* row = reinterpret_cast<const uint4*>(tc + static_cast<size_t>(d) * sg.pitch);
+          for (uint32_t q = 0; q < sg.pitch / 4; ++q) {
+            const uint4 v = row[q];
+            const uint32_t t0 = 4 * q;
+            b += (t0 < tile ? v.x : 0u) + (t0 + 1 < tile ? v.y : 0u) + (t0 + 2 < tile ? v.z : 0u) +
+                 (t0 + 3 < tile ? v.w : 0u);
+            t += v.x + v.y + v.z + v.w;
+          }
+        } else {
+          t = rowsum[d];
+          b = tc[static_cast<size_t>(d) * sg.pitch + tile];
+        }
+      }
+      if (j < kMaxPer) {
+        row_total[j] = t;
+        before[j] = b;
+      }
+      loc += t;
     }
     uint32_t run = blockExclusiveScan(loc, &nkeys);
-    for (int j = 0; j < per; ++j) {
+    for (int j = 0; j < per && j < kMaxPer; ++j) {
       const int d = threadIdx.x * per + j;
       if (d < buckets) {
-        offs[d] = run + tc[static_cast<size_t>(d) * sg.pitch + tile];
-        run += rowsum[d];
+        offs[d] = run + before[j];
+        run += row_total[j];
       }
     }
   }
@@ -2556,12 +2589,19 @@ void phaseSort(Frame& f, const uint32_t* keys, uint32_t N, const double* z, cons
   const uint32_t* kin = keys;
   uint32_t *kout = m.key1, *vin = m.val0, *vout = m.val1;
   for (int p = 0; p < sg.passes; ++p) {
-    launchPdl(k_sort_rowscan, sg.buckets(), kThreads, 0, s, sg.counts(p), sg.pitch,
-                                                     sg.rowsum + p * sg.buckets());
-    launchPdl(sg.tshift == kSmallTileShift ? k_sort_scatter<kSmallTile / kThreads> : k_sort_scatter<kSortItems>,
+    const bool fused = RB_FUSED_ROWSCAN && sg.ntiles <= kFusedTiles;
+    if (!fused) {
+      launchPdl(k_sort_rowscan, sg.buckets(), kThreads, 0, s, sg.counts(p), sg.pitch,
+                sg.rowsum + p * sg.buckets());
+      ++f.launches;
+    }
+    launchPdl(fused ? (sg.tshift == kSmallTileShift ? k_sort_scatter<kSmallTile / kThreads, true>
+                                                     : k_sort_scatter<kSortItems, true>)
+                    : (sg.tshift == kSmallTileShift ? k_sort_scatter<kSmallTile / kThreads>
+                                                     : k_sort_scatter<kSortItems>),
               sg.ntiles, kThreads, sc_smem, s, kin, vin, N, p, sg, f.WH, kout, vout, z, var, m.spz, m.spv,
               m.start);
-    f.launches += 2;
+    ++f.launches;
     // ping-pong between key1 and key0 (key0 is free once pass 0 has read it)
     const uint32_t* next_in = kout;
     kout = (kout == m.key1) ? m.key0 : m.key1;
