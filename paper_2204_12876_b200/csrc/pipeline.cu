@@ -1796,7 +1796,9 @@ __device__ __forceinline__ void pass1Jump(P1Walk& w, const Pass1Ctx& c, const Ra
       ++di;
     }
     if (di == 0 || di >= lim_x) return;
-    const int by0 = static_cast<int>(fmin((last - tmy) * (1.0 / tdy), static_cast<double>(lim_y))) - 2;
+    // (an axis that never steps has t_max = t_delta = inf: the estimate is NaN, no blind steps)
+    const double ey = (last - tmy) * (1.0 / tdy);
+    const int by0 = ey == ey ? static_cast<int>(fmin(ey, static_cast<double>(lim_y))) - 2 : 0;
 #pragma unroll 4
     for (int k = 0; k < by0; ++k) tmy += tdy;
     dj = by0 > 0 ? by0 : 0;
@@ -1815,7 +1817,8 @@ __device__ __forceinline__ void pass1Jump(P1Walk& w, const Pass1Ctx& c, const Ra
       ++dj;
     }
     if (dj == 0 || dj >= lim_y) return;
-    const int bx0 = static_cast<int>(fmin((last - tmx) * (1.0 / tdx), static_cast<double>(lim_x))) - 2;
+    const double ex = (last - tmx) * (1.0 / tdx);
+    const int bx0 = ex == ex ? static_cast<int>(fmin(ex, static_cast<double>(lim_x))) - 2 : 0;
 #pragma unroll 4
     for (int k = 0; k < bx0; ++k) tmx += tdx;
     di = bx0 > 0 ? bx0 : 0;
