@@ -858,7 +858,10 @@ constexpr int kFoldBatch = 8;
 #define RB_HEAVY_CELL 64
 #endif
 constexpr int kHeavyCell = RB_HEAVY_CELL;
-constexpr int kHeavyBlocks = 256;  // one warp each
+#ifndef RB_HEAVY_BLOCKS
+#define RB_HEAVY_BLOCKS 256
+#endif
+constexpr int kHeavyBlocks = RB_HEAVY_BLOCKS;  // one warp each
 
 struct FoldCounts {
   unsigned long long nf = 0, no = 0, ni = 0, upd = 0;
@@ -1001,7 +1004,10 @@ __global__ void __launch_bounds__(kThreads)
 // longer cells are queued for k_fuse_heavy, which runs on a second stream
 // concurrently with the ray pass: cells
 // with more than kVeryHeavyCell points on their own list (one warp each there).
-constexpr int kVeryHeavyCell = 256;
+#ifndef RB_VHEAVY_CELL
+#define RB_VHEAVY_CELL 256  // (64 / 96 / 128 measured slower)
+#endif
+constexpr int kVeryHeavyCell = RB_VHEAVY_CELL;
 //
 // Every cell also gets the frame's drift offset first (reference drift.cpp:
 // 44-55, off_p: device scalar from the ingest's drift reduction; null = none)
