@@ -109,6 +109,43 @@ def test_randomised_scenarios_match_reference(gpu, reference, tmp_path, seed):
                             context=ctx)
 
 
+# Long sequences: the ray pass's jumps engage once the map's cells have been
+# observed and their bounds settled, so these scenarios run 24 frames of a slowly moving sensor
+# over the same ground (every 6th frame with a stamp gap that makes cells stale) and compare
+# every frame. RELIEF_SOAK_LONG_SEEDS=N widens the sweep.
+LONG_SEEDS = list(range(int(os.environ.get("RELIEF_SOAK_LONG_SEEDS", "6"))))
+
+
+@pytest.mark.parametrize("seed", LONG_SEEDS)
+def test_randomised_long_sequences_match_reference(gpu, reference, tmp_path, seed):
+    rng = np.random.default_rng(7000 + seed)
+    res = float(rng.choice([0.02, 0.04, 0.05]))
+    W, H = int(rng.integers(60, 260)), int(rng.integers(60, 260))
+    text, drift = _config(rng)
+    cfg_path = tmp_path / "soak_long.config"
+    cfg_path.write_text(wl._map(res, W, H) + text)
+    libs = (gpu, reference)
+    cfgs = [pk.Config.load(lib, cfg_path) for lib in libs]
+    maps = [pk.ReliefMap.create(lib, res, W, H) for lib in libs]
+    pos = np.array([0.0, 0.0, rng.uniform(0.5, 1.5)])
+    base = _cloud(rng, res, False, int(rng.integers(2000, 8000)))
+    stamp = 0.0
+    for f in range(24):
+        yaw = rng.uniform(-0.2, 0.2)
+        R = wl.rot_z(yaw) @ wl.rot_y(rng.uniform(-0.05, 0.05))
+        pos = pos + np.array([rng.normal(0, 0.5 * res), rng.normal(0, 0.5 * res), 0.0])
+        pose = wl.pose34(R, tuple(pos))
+        stamp += 1.5 if f % 6 == 5 else 0.1
+        jitter = base + rng.normal(0, 0.3 * res, base.shape)  # the same scene, re-sampled
+        xyz = np.concatenate([jitter, _cloud(rng, res, False, int(rng.integers(100, 600)))])
+        got = maps[0].integrate(xyz, pose, stamp, cfgs[0])
+        want = maps[1].integrate(xyz, pose, stamp, cfgs[1])
+        ctx = f"long seed {seed} frame {f} ({W}x{H}@{res}, drift={drift})"
+        assert_stats_match(got, want, drift_tol=1e-12 if drift else 0.0, context=ctx)
+        assert_layers_match(maps[0].layers(), maps[1].layers(), height_tol=1e-9 if drift else 0.0,
+                            context=ctx)
+
+
 def _frames(rng, res, cell_aligned, n_frames):
     pos, stamp, out = np.zeros(3), 0.0, []
     for _ in range(n_frames):
