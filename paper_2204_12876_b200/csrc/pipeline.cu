@@ -9,14 +9,18 @@
 //                        (+ drift vote mean, fixed-order, in the last block)
 //   K2  radix sort       stable LSD sort of (cell, point) -> per-cell segments
 //                        in scan order; exclusive scan count -> segment start
-//   K3  k_fuse           drift offset + gated Kalman fold + ray class, one
+//   K3  k_fuse           drift offset (k_apply_offset) + gated Kalman fold, one
 //                        thread per cell (long cells: k_fuse_heavy, side stream)
-//   K5  k_rays_pass1     exact 2-D DDA per kept point: bounds of invalid cells,
-//                        k* = first removing ray per candidate cell
-//   K6  k_rays_pass2     bounds of removed cells from rays k >= k* (scratch)
+//   K5  k_classify       ray class + probe word per cell; k_jump_grid: the
+//                        16x16-block bounds the rays jump over
+//       k_rays_pass1     exact 2-D DDA per kept point (jumping over cleared
+//                        blocks): bounds of invalid cells, k* = first removing
+//                        ray per candidate cell
+//   K6  k_rays_tail      retry of a failed speculation + bounds of removed cells
+//                        from rays k >= k* (scratch), one cooperative launch
 //   K7  k_cells          removal (k* < inf) + overlap clearance + normals +
 //                        traversability + time variance, one shared-memory
-//                        tile with a halo
+//                        tile with a halo; its last block hands the stats over
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
