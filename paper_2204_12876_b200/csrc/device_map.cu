@@ -128,6 +128,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
   }
   if (device < 0 || device >= count) fail(Err::kUsage, "CUDA device ordinal out of range");
   checkCuda(cudaSetDevice(device), "cudaSetDevice");
+  preloadFrameKernels(device);
   auto* m = new DeviceMap();
   m->device = device;
   m->grid = grid;

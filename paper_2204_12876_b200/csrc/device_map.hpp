@@ -236,6 +236,7 @@ GridArgs gridArgs(const Grid& g);
 
 // Lifecycle (device_map.cu).
 DeviceMap* createDeviceMap(int device, const Grid& grid);
+void preloadFrameKernels(int device);  // (pipeline.cu) module loading at map creation
 void destroyDeviceMap(DeviceMap* m);
 void ensurePointCapacity(DeviceMap& m, std::size_t n);
 void fillFresh(DeviceMap& m);  // reference grid.cpp:24-39 fill values

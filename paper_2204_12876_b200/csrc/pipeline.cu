@@ -2975,6 +2975,32 @@ ScanResult resultFrom(const DevStats& d, std::size_t n) {
 
 }  // namespace
 
+// Loads the frame kernels' code on this device now (map creation) rather than
+// at their first launch: with the runtime's lazy module loading the first
+// frame of a process otherwise pays ~10 ms on the device.
+void preloadFrameKernels(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  done[device] = true;
+  cudaFuncAttributes fa;
+  const void* kernels[] = {
+      reinterpret_cast<const void*>(k_shift), reinterpret_cast<const void*>(k_ingest),
+      reinterpret_cast<const void*>(k_drift_finalize), reinterpret_cast<const void*>(k_apply_offset),
+      reinterpret_cast<const void*>(k_sort_rowscan),
+      reinterpret_cast<const void*>(k_sort_scatter<kSortItems>),
+      reinterpret_cast<const void*>(k_sort_scatter<kSortItems, true>),
+      reinterpret_cast<const void*>(k_sort_scatter<kSmallTile / kThreads>),
+      reinterpret_cast<const void*>(k_sort_scatter<kSmallTile / kThreads, true>),
+      reinterpret_cast<const void*>(k_fuse), reinterpret_cast<const void*>(k_fuse_heavy),
+      reinterpret_cast<const void*>(k_classify), reinterpret_cast<const void*>(k_jump_grid),
+      reinterpret_cast<const void*>(k_rays_pass1<false>), reinterpret_cast<const void*>(k_rays_pass1<true>),
+      reinterpret_cast<const void*>(k_rays_tail), reinterpret_cast<const void*>(k_cells<0>),
+      reinterpret_cast<const void*>(k_cells<1>), reinterpret_cast<const void*>(k_cells<2>),
+      reinterpret_cast<const void*>(k_cells_global)};
+  for (const void* k : kernels) cudaFuncGetAttributes(&fa, k);
+  cudaGetLastError();
+}
+
 ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const double* xyz,
                                std::size_t n, bool xyz_on_device, const Pose& pose,
                                double stamp, double dt) {
