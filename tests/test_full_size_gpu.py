@@ -9,6 +9,8 @@ path of the ray pass runs at full size too.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -97,3 +99,27 @@ def test_overlap_clearance_fires_full_size(gpu, reference, tmp_path):
         assert_layers_match(maps[0].layers(), maps[1].layers(), context=f"frame {f}")
         cleared += got.cells_cleared_by_overlap
     assert cleared > 100, cleared
+
+
+# Steady state at full size: the bench's C4 sequence (stamps 0.1 s apart) for 40 frames, where
+# the ray pass's jumps clear most of the DDA cells; every frame's counters and every 8th frame's
+# layers against the reference (~30 s per config: the reference's frames take ~0.7 s each).
+# RELIEF_FULL_STEADY=0 skips them.
+@pytest.mark.skipif(os.environ.get("RELIEF_FULL_STEADY") == "0", reason="RELIEF_FULL_STEADY=0")
+@pytest.mark.parametrize("name", ["C4", "headline"])
+def test_full_size_steady_state(gpu, reference, tmp_path, name):
+    w = wl.ALL[name]()
+    cfg_path = tmp_path / f"{w.name}.config"
+    cfg_path.write_text(w.config_text + "drift.enabled = false\n")
+    libs = (gpu, reference)
+    cfgs = [pk.Config.load(lib, cfg_path) for lib in libs]
+    maps = [pk.ReliefMap.create(lib, w.resolution, w.width, w.height) for lib in libs]
+    clouds = [[(ref_render(reference, cfg_path, c.pose, c.time, c.seed, c.scan_index), c) for c in w.calls(f)]
+              for f in range(8)]
+    for s in range(40):
+        for xyz, c in clouds[s % 8]:
+            got = maps[0].integrate(xyz, c.pose, 0.1 * s, cfgs[0])
+            want = maps[1].integrate(xyz, c.pose, 0.1 * s, cfgs[1])
+            assert_stats_match(got, want, context=f"{name} step {s}")
+        if s % 8 == 7:
+            assert_layers_match(maps[0].layers(), maps[1].layers(), context=f"{name} after step {s}")
