@@ -49,6 +49,12 @@ constexpr int kThreads = 256;
 #ifndef RB_P1_JUMP
 #define RB_P1_JUMP 1  // pass-1 rays jump over the blocks their heights clear (pass1Jump)
 #endif
+#ifndef RB_INGEST_TMA
+#define RB_INGEST_TMA 1  // persistent ingest fed by TMA bulk copies (k_ingest_tma)
+#endif
+#ifndef RB_INGEST_TMA_BLOCKS
+#define RB_INGEST_TMA_BLOCKS 5  // k_ingest_tma grid: blocks per SM (48 registers: 5 resident)
+#endif
 #ifndef RB_GRAPH_MIN_POINTS
 #define RB_GRAPH_MIN_POINTS 32768
 #endif
@@ -286,46 +292,27 @@ struct IngestArgs {
 // Per point (reference integration.cpp:85-113,134-140; sensing.cpp:32-41;
 // drift.cpp:24-42; grid.cpp:41-47): fate, map-frame point, sigma_p^2, cell,
 // drift vote against the pre-fusion map, per-cell point count.
-__global__ void __launch_bounds__(kThreads)
-    k_ingest(const double* __restrict__ xyz, uint32_t n, IngestArgs a, Layers L,
-             int32_t* __restrict__ count, double* __restrict__ px, double* __restrict__ py,
-             double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
-             uint8_t* __restrict__ kept, double* __restrict__ drift_part,
-             int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
-             uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base, uint32_t in_base) {
-  pdlEnter();
+// One 256-point tile of the ingest: the points k = k_base + tile * 256 + thread,
+// read from the staged copy `sx` in shared memory (null: from xyz directly).
+__device__ __forceinline__ void ingestTile(const double* __restrict__ xyz, uint32_t n, const IngestArgs& a,
+                                           const Layers& L, int32_t* __restrict__ count,
+                                           double* __restrict__ px, double* __restrict__ py,
+                                           double* __restrict__ pz, double* __restrict__ pvar,
+                                           uint32_t* __restrict__ key, uint8_t* __restrict__ kept,
+                                           double* __restrict__ drift_part, int* __restrict__ drift_npart,
+                                           uint32_t* __restrict__ tc0, uint32_t pitch, uint32_t dmask,
+                                           int count_cells, DevStats* st, uint32_t k_base,
+                                           uint32_t in_base, uint32_t tile, const double* sx) {
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
-  // k_base: first point of this launch (a chunk of a frame whose upload is
-  // split); block partials are indexed by the frame-wide block k / kThreads.
-  // in_base: frame index of xyz[0] (0, or a group rank's first point, whose
-  // outputs land at their frame-wide indices).
-  const uint32_t k = k_base + blockIdx.x * kThreads + threadIdx.x;
+  const uint32_t k = k_base + tile * kThreads + threadIdx.x;
   int oor = 0, exc = 0, oom = 0, dn = 0;
   double ds = 0.0;
   uint32_t cell = WH;
-  // The block's 256 points (6 KB of x y z) come in as 16-byte vector loads
-  // into shared memory (every byte fetched once, full sectors), then each
-  // thread reads its own triple; a misaligned caller pointer reads directly.
-  __shared__ double2 s_xyz[3 * kThreads / 2];
-  const uint32_t k0 = k_base + blockIdx.x * kThreads;
-  const double* blk = xyz + 3 * static_cast<size_t>(k0 - in_base);
-  const bool staged = (reinterpret_cast<uintptr_t>(blk) & 15u) == 0;
-  if (staged) {
-    const uint32_t nb = k0 < n ? min(static_cast<uint32_t>(kThreads), n - k0) : 0u;
-    const double2* src = reinterpret_cast<const double2*>(blk);
-    for (uint32_t q = threadIdx.x; 2 * q < 3 * nb; q += kThreads) {
-      if (2 * q + 1 < 3 * nb) {
-        s_xyz[q] = __ldcs(src + q);
-      } else {
-        s_xyz[q].x = __ldcs(blk + 2 * q);  // odd tail: the last double alone
-      }
-    }
-    __syncthreads();
-  }
+  const bool staged = sx != nullptr;
   if (k < n) {
     double x, y, z;
     if (staged) {
-      const double* sp = reinterpret_cast<const double*>(s_xyz) + 3 * threadIdx.x;
+      const double* sp = sx + 3 * threadIdx.x;
       x = sp[0];
       y = sp[1];
       z = sp[2];
@@ -415,12 +402,49 @@ __global__ void __launch_bounds__(kThreads)
       c2 += s_cnt[2][w];
       c3 += s_cnt[3][w];
     }
-    drift_part[k_base / kThreads + blockIdx.x] = bs;
-    drift_npart[k_base / kThreads + blockIdx.x] = c0;
+    drift_part[k_base / kThreads + tile] = bs;
+    drift_npart[k_base / kThreads + tile] = c0;
     if (c1) atomicAdd(&st->out_of_range, static_cast<unsigned long long>(c1));
     if (c2) atomicAdd(&st->excluded, static_cast<unsigned long long>(c2));
     if (c3) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c3));
   }
+  __syncthreads();  // (the block's reduction arrays are reused by its next tile)
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_ingest(const double* __restrict__ xyz, uint32_t n, IngestArgs a, Layers L,
+             int32_t* __restrict__ count, double* __restrict__ px, double* __restrict__ py,
+             double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
+             uint8_t* __restrict__ kept, double* __restrict__ drift_part,
+             int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
+             uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base, uint32_t in_base) {
+  pdlEnter();
+  // k_base: first point of this launch (a chunk of a frame whose upload is
+  // split); block partials are indexed by the frame-wide block k / kThreads.
+  // in_base: frame index of xyz[0] (0, or a group rank's first point, whose
+  // outputs land at their frame-wide indices).
+  // The block's 256 points (6 KB of x y z) come in as 16-byte vector loads
+  // into shared memory (every byte fetched once, full sectors), then each
+  // thread reads its own triple; a misaligned caller pointer reads directly.
+  __shared__ double2 s_xyz[3 * kThreads / 2];
+  const uint32_t k0 = k_base + blockIdx.x * kThreads;
+  const double* blk = xyz + 3 * static_cast<size_t>(k0 - in_base);
+  const bool staged = (reinterpret_cast<uintptr_t>(blk) & 15u) == 0;
+  if (staged) {
+    const uint32_t nb = k0 < n ? min(static_cast<uint32_t>(kThreads), n - k0) : 0u;
+    const double2* src = reinterpret_cast<const double2*>(blk);
+    for (uint32_t q = threadIdx.x; 2 * q < 3 * nb; q += kThreads) {
+      if (2 * q + 1 < 3 * nb) {
+        s_xyz[q] = __ldcs(src + q);
+      } else {
+        s_xyz[q].x = __ldcs(blk + 2 * q);  // odd tail: the last double alone
+      }
+    }
+    __syncthreads();
+  }
+  ingestTile(xyz, n, a, L, count, px, py, pz, pvar, key, kept, drift_part, drift_npart, tc0, pitch,
+             dmask, count_cells, st, k_base, in_base, blockIdx.x,
+             staged ? reinterpret_cast<const double*>(s_xyz) : nullptr);
 #if RB_INGEST_FINALIZE
   if (a.drift_blocks == 0) return;
   // The last block of the frame's ingest (over all chunk launches) reduces the
@@ -436,6 +460,73 @@ __global__ void __launch_bounds__(kThreads)
   driftFinalizeBlock(drift_part, drift_npart, static_cast<int>(a.drift_blocks), a.drift_min_points,
                      a.drift_max_off, a.drift_offset, st);
 #endif
+}
+
+// Persistent ingest with the input brought in by the TMA engine: each block
+// takes the tiles blockIdx.x, + gridDim.x, ... of this launch (ntl tiles), and
+// while it processes one tile the next tile's 6 KB of x y z lands in the other
+// half of a double buffer by a bulk asynchronous copy (cp.async.bulk, mbarrier
+// completion). A partial last tile (or a caller pointer not 16-B aligned) is
+// read directly. Outputs, drift partials (per tile) and counts are those of
+// k_ingest.
+__device__ __forceinline__ uint32_t smemAddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__global__ void __launch_bounds__(kThreads)
+    k_ingest_tma(const double* __restrict__ xyz, uint32_t n, IngestArgs a, Layers L,
+                 int32_t* __restrict__ count, double* __restrict__ px, double* __restrict__ py,
+                 double* __restrict__ pz, double* __restrict__ pvar, uint32_t* __restrict__ key,
+                 uint8_t* __restrict__ kept, double* __restrict__ drift_part,
+                 int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
+                 uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base, uint32_t in_base,
+                 uint32_t ntl) {
+  pdlEnter();
+  constexpr uint32_t kTileBytes = 3 * kThreads * sizeof(double);  // 6 KB
+  __shared__ alignas(128) double s_buf[2][3 * kThreads];
+  __shared__ alignas(8) unsigned long long s_bar[2];
+  const double* base = xyz + 3 * static_cast<size_t>(k_base - in_base);
+  const bool tma = (reinterpret_cast<uintptr_t>(base) & 15u) == 0;
+  auto full = [&](uint32_t t) { return k_base + (t + 1) * kThreads <= n; };
+  auto issue = [&](uint32_t t, int b) {  // thread 0: tile t into buffer b
+    if (!tma || !full(t)) return;
+    const uint32_t bar = smemAddr(&s_bar[b]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's last reads first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kTileBytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smemAddr(s_buf[b])),
+        "l"(base + 3 * static_cast<size_t>(t) * kThreads), "r"(kTileBytes), "r"(bar)
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemAddr(&s_bar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemAddr(&s_bar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < ntl) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (uint32_t t = blockIdx.x; t < ntl; t += gridDim.x, ++it) {
+    const int b = static_cast<int>(it & 1u);
+    // the other buffer is free: every thread finished the previous tile (the
+    // barrier at the end of ingestTile)
+    if (threadIdx.x == 0 && t + gridDim.x < ntl) issue(t + gridDim.x, b ^ 1);
+    const double* sx = nullptr;
+    if (tma && full(t)) {
+      const uint32_t bar = smemAddr(&s_bar[b]), parity = (it >> 1) & 1u;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "WAIT_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+          "r"(parity)
+          : "memory");
+      sx = s_buf[b];
+    }
+    ingestTile(xyz, n, a, L, count, px, py, pz, pvar, key, kept, drift_part, drift_npart, tc0, pitch,
+               dmask, count_cells, st, k_base, in_base, t, sx);
+  }
 }
 
 // ------------------------------------------------------ drift (one block)
@@ -2533,10 +2624,16 @@ void phaseIngest(Frame& f, const double* d_xyz, uint32_t N, const SortGeom& sg, 
   const uint32_t chunk = chunked ? chunkPoints(N) : N;
   for (uint32_t base = 0, c = 0; base < N; base += chunk, ++c) {
     if (chunked) checkCuda(cudaStreamWaitEvent(f.s, m.ev_chunk[c], 0), "stream wait");
-    launchPdl(k_ingest, gridFor(std::min(chunk, N - base)), kThreads, 0, f.s, d_xyz, lo + N, ia,
-              m.cur, m.count, m.px, m.py, m.pz, m.pvar, m.key0, m.kept, m.drift_sum_part,
-              m.drift_n_part, sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0, m.stats,
-              lo + base, lo);
+    const unsigned ntl = gridFor(std::min(chunk, N - base));
+    if (RB_INGEST_TMA && !RB_INGEST_FINALIZE)
+      launchPdl(k_ingest_tma, std::min(ntl, 148u * RB_INGEST_TMA_BLOCKS), kThreads, 0, f.s, d_xyz, lo + N,
+                ia, m.cur, m.count, m.px, m.py, m.pz, m.pvar, m.key0, m.kept, m.drift_sum_part,
+                m.drift_n_part, sg.tc, sg.pitch, sg.buckets() - 1, count_cells ? 1 : 0, m.stats,
+                lo + base, lo, ntl);
+    else
+      launchPdl(k_ingest, ntl, kThreads, 0, f.s, d_xyz, lo + N, ia, m.cur, m.count, m.px, m.py, m.pz,
+                m.pvar, m.key0, m.kept, m.drift_sum_part, m.drift_n_part, sg.tc, sg.pitch,
+                sg.buckets() - 1, count_cells ? 1 : 0, m.stats, lo + base, lo);
     ++f.launches;
   }
 }
