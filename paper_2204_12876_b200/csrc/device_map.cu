@@ -147,6 +147,8 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     for (auto& e : m->ev) checkCuda(cudaEventCreate(&e), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_after, cudaEventDisableTiming), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "event create");
+    checkCuda(cudaEventCreateWithFlags(&m->ev_dfork, cudaEventDisableTiming), "event create");
+    checkCuda(cudaEventCreateWithFlags(&m->ev_djoin, cudaEventDisableTiming), "event create");
     checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev_chunk)
       checkCuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
@@ -232,6 +234,8 @@ void destroyDeviceMap(DeviceMap* m) {
     if (e) cudaEventDestroy(e);
   if (m->ev_after) cudaEventDestroy(m->ev_after);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+  if (m->ev_dfork) cudaEventDestroy(m->ev_dfork);
+  if (m->ev_djoin) cudaEventDestroy(m->ev_djoin);
   for (int k = 0; k < m->graph_count; ++k) cudaGraphExecDestroy(m->graphs[k]);
   for (auto& e : m->ev_chunk)
     if (e) cudaEventDestroy(e);

@@ -206,6 +206,7 @@ struct DeviceMap {
   cudaEvent_t ev[14] = {};
   cudaEvent_t ev_after = nullptr;  // relief_gpu_map_after_stream
   cudaEvent_t ev_fork = nullptr;   // frame stream -> copy stream (chunked upload)
+  cudaEvent_t ev_dfork = nullptr, ev_djoin = nullptr;  // drift on stream2 (phaseDrift side)
   // Executable graphs of recent synchronous-frame topologies, most recent
   // first (pipeline.cu FrameCapture); off: direct launches.
   static constexpr int kGraphs = 4;

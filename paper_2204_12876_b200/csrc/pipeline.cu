@@ -2460,6 +2460,7 @@ struct Frame {
   // none, or applied already -- the sharded path's k_apply_offset_value).
   const double* fuse_offset = nullptr;
   bool classified = false;  // k_fuse wrote this frame's ray classes
+  bool drift_join = false;  // phaseDrift(side) ran on stream2: join before the fold
   // Removal of k* < inf cells: in k_cells (fold_remove, set when the ray pass
   // ran with cleanup on), or by k_remove right after the ray pass
   // (explicit_remove: sharded frames, whose host exchanges the bounds after it).
@@ -2660,14 +2661,38 @@ RayArgs rayArgs(const Frame& f) {
 
 // Drift vote mean of a single-GPU frame (unless the ingest's last block
 // reduced it); the offset itself is applied before the fold (phaseSortFuse).
-void phaseDrift(Frame& f, uint32_t N) {
+// side (RB_SIDE_DRIFT): the vote mean and the offset sweep run on stream2,
+// forked from the frame stream after the ingest, so both overlap the radix
+// sort (which touches no layer); phaseSortFuse joins before the fold.
+#ifndef RB_SIDE_DRIFT
+#define RB_SIDE_DRIFT 1
+#endif
+void phaseDrift(Frame& f, uint32_t N, bool side = false) {
   DeviceMap& m = f.m;
   if (N == 0 || !f.P.drift.enabled || f.fuse_offset != nullptr) return;
+  if (RB_SIDE_DRIFT && side) {
+    checkCuda(cudaEventRecord(m.ev_dfork, f.s), "event");
+    checkCuda(cudaStreamWaitEvent(m.stream2, m.ev_dfork, 0), "stream wait");
+    k_drift_finalize<<<1, 1024, 0, m.stream2>>>(m.drift_sum_part, m.drift_n_part,
+                                                 static_cast<int>(gridFor(N)), f.P.drift.min_points,
+                                                 f.P.drift.max_offset_per_scan, m.drift_offset, m.stats);
+    k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
+    checkCuda(cudaEventRecord(m.ev_djoin, m.stream2), "event");
+    f.launches += 2;
+    f.drift_join = true;
+    return;
+  }
   launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part,
             static_cast<int>(gridFor(N)), f.P.drift.min_points, f.P.drift.max_offset_per_scan,
             m.drift_offset, m.stats);
   ++f.launches;
   f.fuse_offset = m.drift_offset;
+}
+
+void joinDrift(Frame& f) {
+  if (!f.drift_join) return;
+  checkCuda(cudaStreamWaitEvent(f.s, f.m.ev_djoin, 0), "stream wait");
+  f.drift_join = false;
 }
 
 // K2 over N keys (cells; >= WH = not sorted) with payload (z, var) indexed
@@ -2752,6 +2777,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
 #ifndef RB_SPLIT_CLASSIFY
 #define RB_SPLIT_CLASSIFY 0  // measured slower
 #endif
+  joinDrift(f);
   const RayArgs ra = rayArgs(f);
   const ClassArgs ca{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W};
   int classify = 0;
@@ -2884,6 +2910,7 @@ void phaseRemovePass2(Frame& f, uint32_t ray_base) {
 
 // K7 cell phases + update_variance, then the conv-net filter when selected.
 void phaseCells(Frame& f) {
+  joinDrift(f);
   DeviceMap& m = f.m;
   const UpdateParams& U = f.P.update;
   CellArgs ca;
@@ -3150,10 +3177,11 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   RB_PHASE_EVENT(1, f.s);  // resets done
   phaseIngest(f, d_xyz, N, sg, true, chunked, 0, true);
   RB_PHASE_EVENT(2, f.s);  // ingest done
-  phaseDrift(f, N);
+  if (!RB_SIDE_DRIFT || n == 0) phaseDrift(f, N);
   RB_PHASE_EVENT(3, f.s);  // drift done
   if (graph_head) cap.begin();
   if (n > 0) {
+    phaseDrift(f, N, true);
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
     phaseRaysPass1(f, N, 0, true);
@@ -3287,9 +3315,10 @@ void integrateScanAsync(DeviceMap& m, const PipelineParams& P, const double* xyz
   phaseIngest(f, d_xyz, N, sg, true, false, 0, true);
   checkCuda(cudaEventRecord(m.ev_consumed[slot], f.s), "event");
   RB_PHASE_EVENT(2, f.s);
-  phaseDrift(f, N);
+  if (!RB_SIDE_DRIFT || n == 0) phaseDrift(f, N);
   RB_PHASE_EVENT(3, f.s);
   if (n > 0) {
+    phaseDrift(f, N, true);
     phaseSortFuse(f, m.key0, N, m.pz, m.pvar, sg);
     f.point_cells = sg.passes <= 2 ? m.key0 : nullptr;  // a 3rd pass reuses key0
     phaseRaysPass1(f, N, 0, true);
