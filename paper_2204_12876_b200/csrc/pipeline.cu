@@ -1095,14 +1095,62 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Cells with at most `heavy` points are folded here, one thread per cell;
-// longer cells are queued for k_fuse_heavy, which runs on a second stream
-// concurrently with the ray pass (DESIGN.md "Fusion / ray overlap"): cells
-// with more than kVeryHeavyCell points on their own list (one warp each there).
 #ifndef RB_VHEAVY_CELL
 #define RB_VHEAVY_CELL 256  // (64 / 96 / 128 measured slower)
 #endif
 constexpr int kVeryHeavyCell = RB_VHEAVY_CELL;
+
+// Queues a warp's long cells (more than `heavy` points) for k_fuse_heavy:
+// more than kVeryHeavyCell points on the warp-per-cell list, the others on
+// the lane-per-cell list. All 32 lanes call it.
+__device__ __forceinline__ void appendHeavy(int cnt, int heavy, size_t i, uint32_t* heavy_list,
+                                            uint32_t* vheavy_list, DevStats* st) {
+  const bool is_heavy = cnt > heavy;
+  const bool is_vheavy = is_heavy && cnt > kVeryHeavyCell;
+  const int lane = threadIdx.x & 31;
+  const unsigned hv = __ballot_sync(0xffffffffu, is_heavy && !is_vheavy);
+  if (hv) {
+    unsigned base = 0;
+    if (lane == __ffs(hv) - 1)
+      base = static_cast<unsigned>(atomicAdd(&st->heavy_cells, static_cast<unsigned long long>(__popc(hv))));
+    base = __shfl_sync(0xffffffffu, base, __ffs(hv) - 1);
+    if (is_heavy && !is_vheavy) heavy_list[base + __popc(hv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+  }
+  const unsigned vv = __ballot_sync(0xffffffffu, is_vheavy);
+  if (vv) {
+    unsigned base = 0;
+    if (lane == __ffs(vv) - 1)
+      base = static_cast<unsigned>(atomicAdd(&st->vheavy_cells, static_cast<unsigned long long>(__popc(vv))));
+    base = __shfl_sync(0xffffffffu, base, __ffs(vv) - 1);
+    if (is_vheavy) vheavy_list[base + __popc(vv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+  }
+}
+
+// Second-stream sweep after the ingest (RB_EARLY_HEAVY): the drift offset
+// (off_p null: none) and the long-cell lists from the per-cell counts, so the
+// long-cell fold can start as soon as the sort is done, beside k_fuse (which
+// then builds no lists).
+__global__ void __launch_bounds__(kThreads)
+    k_side_prep(Layers L, size_t n, const double* off_p, const int32_t* __restrict__ count, int heavy,
+                uint32_t* heavy_list, uint32_t* vheavy_list, DevStats* st) {
+  const double off = off_p != nullptr ? *off_p : 0.0;
+  const int lane = threadIdx.x & 31;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t b = blockIdx.x * static_cast<size_t>(blockDim.x) + (threadIdx.x & ~31u); b < n; b += stride) {
+    const size_t i = b + lane;
+    const bool in = i < n;
+    if (in && off != 0.0) {
+      if (L.valid[i]) L.elev[i] += off;
+      if (L.ubv[i]) L.ub[i] += off;
+    }
+    if (heavy_list != nullptr) appendHeavy(in ? count[i] : 0, heavy, i, heavy_list, vheavy_list, st);
+  }
+}
+
+// Cells with at most `heavy` points are folded here, one thread per cell;
+// longer cells are queued for k_fuse_heavy, which runs on a second stream
+// concurrently with the ray pass (DESIGN.md "Fusion / ray overlap"): cells
+// with more than kVeryHeavyCell points on their own list (one warp each there).
 //
 // Every cell also gets the frame's drift offset first (reference drift.cpp:
 // 44-55, off_p: device scalar from the ingest's drift reduction; null = none)
@@ -1132,24 +1180,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   const bool is_heavy = cnt > heavy;
-  const bool is_vheavy = is_heavy && cnt > kVeryHeavyCell;
-  const int lane = threadIdx.x & 31;
-  const unsigned hv = __ballot_sync(0xffffffffu, is_heavy && !is_vheavy);
-  if (hv) {
-    unsigned base = 0;
-    if (lane == __ffs(hv) - 1)
-      base = static_cast<unsigned>(atomicAdd(&st->heavy_cells, static_cast<unsigned long long>(__popc(hv))));
-    base = __shfl_sync(0xffffffffu, base, __ffs(hv) - 1);
-    if (is_heavy && !is_vheavy) heavy_list[base + __popc(hv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
-  }
-  const unsigned vv = __ballot_sync(0xffffffffu, is_vheavy);
-  if (vv) {
-    unsigned base = 0;
-    if (lane == __ffs(vv) - 1)
-      base = static_cast<unsigned>(atomicAdd(&st->vheavy_cells, static_cast<unsigned long long>(__popc(vv))));
-    base = __shfl_sync(0xffffffffu, base, __ffs(vv) - 1);
-    if (is_vheavy) vheavy_list[base + __popc(vv & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
-  }
+  if (heavy_list != nullptr) appendHeavy(cnt, heavy, i, heavy_list, vheavy_list, st);
   FoldCounts k;
   if (cnt > 0 && !is_heavy) foldCell(L, i, cnt, start, spz, spv, a, st, k);
   // classify 1: every cell; 2: the cells with points (k_prep classified the rest)
@@ -2461,6 +2492,7 @@ struct Frame {
   const double* fuse_offset = nullptr;
   bool classified = false;  // k_fuse wrote this frame's ray classes
   bool drift_join = false;  // phaseDrift(side) ran on stream2: join before the fold
+  bool lists_built = false; // k_side_prep queued the long cells (the long fold starts after the sort)
   // Removal of k* < inf cells: in k_cells (fold_remove, set when the ray pass
   // ran with cleanup on), or by k_remove right after the ray pass
   // (explicit_remove: sharded frames, whose host exchanges the bounds after it).
@@ -2667,21 +2699,43 @@ RayArgs rayArgs(const Frame& f) {
 #ifndef RB_SIDE_DRIFT
 #define RB_SIDE_DRIFT 1
 #endif
+#ifndef RB_EARLY_HEAVY
+#define RB_EARLY_HEAVY 1
+#endif
+void setOverlap(Frame& f) {
+  const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
+  f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
+  f.heavy = f.overlap ? kHeavyCell : INT_MAX;
+}
+
 void phaseDrift(Frame& f, uint32_t N, bool side = false) {
   DeviceMap& m = f.m;
-  if (N == 0 || !f.P.drift.enabled || f.fuse_offset != nullptr) return;
+  const bool drift = N > 0 && f.P.drift.enabled && f.fuse_offset == nullptr;
   if (RB_SIDE_DRIFT && side) {
+    setOverlap(f);
+    const bool lists = RB_EARLY_HEAVY && N > 0 && f.overlap;
+    if (!drift && !lists) return;
     checkCuda(cudaEventRecord(m.ev_dfork, f.s), "event");
     checkCuda(cudaStreamWaitEvent(m.stream2, m.ev_dfork, 0), "stream wait");
-    k_drift_finalize<<<1, 1024, 0, m.stream2>>>(m.drift_sum_part, m.drift_n_part,
-                                                 static_cast<int>(gridFor(N)), f.P.drift.min_points,
-                                                 f.P.drift.max_offset_per_scan, m.drift_offset, m.stats);
-    k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
+    if (drift) {
+      k_drift_finalize<<<1, 1024, 0, m.stream2>>>(m.drift_sum_part, m.drift_n_part,
+                                                   static_cast<int>(gridFor(N)), f.P.drift.min_points,
+                                                   f.P.drift.max_offset_per_scan, m.drift_offset, m.stats);
+      ++f.launches;
+    }
+    if (lists)
+      k_side_prep<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(
+          m.cur, f.ncell, drift ? static_cast<const double*>(m.drift_offset) : nullptr,
+          static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell, m.stats);
+    else
+      k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
+    ++f.launches;
     checkCuda(cudaEventRecord(m.ev_djoin, m.stream2), "event");
-    f.launches += 2;
     f.drift_join = true;
+    f.lists_built = lists;
     return;
   }
+  if (!drift) return;
   launchPdl(k_drift_finalize, 1, 1024, 0, f.s, m.drift_sum_part, m.drift_n_part,
             static_cast<int>(gridFor(N)), f.P.drift.min_points, f.P.drift.max_offset_per_scan,
             m.drift_offset, m.stats);
@@ -2761,9 +2815,9 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   fa.maha = U.mahalanobis_threshold;
   fa.maha2 = U.mahalanobis_threshold * U.mahalanobis_threshold;
   fa.wall = U.wall_count_threshold;
-  const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
-  f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
-  f.heavy = f.overlap ? kHeavyCell : INT_MAX;
+  setOverlap(f);
+  f.fa = fa;
+  if (f.lists_built) launchHeavy(f);  // lists built on stream2: start beside k_fuse
 // Drift offset and ray classification as their own sweeps (default) or inside
 // k_fuse: k_fuse runs at low occupancy (fold registers), so per-cell work for
 // every cell there costs more than a separate streaming sweep (C4 frame +11 /
@@ -2797,7 +2851,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound) ? 1 : 0;
   }
   launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv,
-            fa, m.stats, f.heavy, m.heavy, m.heavy + f.ncell, f.fuse_offset, classify, ca, m.cls,
+            fa, m.stats, f.heavy, f.lists_built ? nullptr : m.heavy, m.heavy + f.ncell, f.fuse_offset, classify, ca, m.cls,
             m.probe, m.kstar);
   ++f.launches;
   f.fuse_offset = nullptr;
@@ -2805,7 +2859,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   f.fa = fa;
   // (Launching it after k_classify instead, to keep that kernel boundary programmatic, made
   // the frame 15 % slower: the side-stream blocks then queue behind the ray pass.)
-  launchHeavy(f);
+  if (!f.lists_built) launchHeavy(f);
   RB_PHASE_EVENT(5, s);  // fusion done (short cells when overlapped)
 }
 
@@ -3110,6 +3164,7 @@ void preloadFrameKernels(int device) {
   const void* kernels[] = {
       reinterpret_cast<const void*>(k_shift), reinterpret_cast<const void*>(k_ingest),
       reinterpret_cast<const void*>(k_drift_finalize), reinterpret_cast<const void*>(k_apply_offset),
+      reinterpret_cast<const void*>(k_side_prep),
       reinterpret_cast<const void*>(k_sort_rowscan),
       reinterpret_cast<const void*>(k_sort_scatter<kSortItems>),
       reinterpret_cast<const void*>(k_sort_scatter<kSortItems, true>),
