@@ -950,7 +950,7 @@ constexpr int kFoldBatch = 8;
 
 // Cells with more points than this fold on the side stream (k_fuse_heavy).
 #ifndef RB_HEAVY_CELL
-#define RB_HEAVY_CELL 64
+#define RB_HEAVY_CELL 32  // (16 / 24 / 48 / 64 measured slower with the early long fold)
 #endif
 constexpr int kHeavyCell = RB_HEAVY_CELL;
 #ifndef RB_HEAVY_BLOCKS
@@ -1132,7 +1132,9 @@ __device__ __forceinline__ void appendHeavy(int cnt, int heavy, size_t i, uint32
 // then builds no lists).
 __global__ void __launch_bounds__(kThreads)
     k_side_prep(Layers L, size_t n, const double* off_p, const int32_t* __restrict__ count, int heavy,
-                uint32_t* heavy_list, uint32_t* vheavy_list, DevStats* st) {
+                uint32_t* heavy_list, uint32_t* vheavy_list, DevStats* st, int classify,
+                ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
+                int32_t* __restrict__ kstar) {
   const double off = off_p != nullptr ? *off_p : 0.0;
   const int lane = threadIdx.x & 31;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -1143,7 +1145,9 @@ __global__ void __launch_bounds__(kThreads)
       if (L.valid[i]) L.elev[i] += off;
       if (L.ubv[i]) L.ub[i] += off;
     }
-    if (heavy_list != nullptr) appendHeavy(in ? count[i] : 0, heavy, i, heavy_list, vheavy_list, st);
+    const int cnt = in ? count[i] : 0;
+    if (heavy_list != nullptr) appendHeavy(cnt, heavy, i, heavy_list, vheavy_list, st);
+    if (classify && in && cnt == 0) classifyCell(L, i, false, ca, cls, probe, kstar);
   }
 }
 
@@ -2492,6 +2496,7 @@ struct Frame {
   const double* fuse_offset = nullptr;
   bool classified = false;  // k_fuse wrote this frame's ray classes
   bool drift_join = false;  // phaseDrift(side) ran on stream2: join before the fold
+  bool prepped = false;     // k_side_prep classified the cells without points
   bool lists_built = false; // k_side_prep queued the long cells (the long fold starts after the sort)
   // Removal of k* < inf cells: in k_cells (fold_remove, set when the ray pass
   // ran with cleanup on), or by k_remove right after the ray pass
@@ -2702,6 +2707,9 @@ RayArgs rayArgs(const Frame& f) {
 #ifndef RB_EARLY_HEAVY
 #define RB_EARLY_HEAVY 1
 #endif
+#ifndef RB_SIDE_CLASSIFY
+#define RB_SIDE_CLASSIFY 0  // k_side_prep also classifies the cells without points (k_fuse the rest)
+#endif
 void setOverlap(Frame& f) {
   const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
   f.overlap = (cleanup || bound) && (!cleanup || f.P.cleanup.t_free >= 0.0);
@@ -2723,11 +2731,15 @@ void phaseDrift(Frame& f, uint32_t N, bool side = false) {
                                                    f.P.drift.max_offset_per_scan, m.drift_offset, m.stats);
       ++f.launches;
     }
-    if (lists)
+    if (lists) {
+      const RayArgs ra = rayArgs(f);
+      const ClassArgs ca{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W};
+      f.prepped = RB_SIDE_CLASSIFY != 0;  // (lists imply a ray pass: cleanup or bound)
       k_side_prep<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(
           m.cur, f.ncell, drift ? static_cast<const double*>(m.drift_offset) : nullptr,
-          static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell, m.stats);
-    else
+          static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell, m.stats,
+          f.prepped ? 1 : 0, ca, m.cls, m.probe, m.kstar);
+    } else
       k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
     ++f.launches;
     checkCuda(cudaEventRecord(m.ev_djoin, m.stream2), "event");
@@ -2835,7 +2847,9 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
   const RayArgs ra = rayArgs(f);
   const ClassArgs ca{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W};
   int classify = 0;
-  if (RB_SPLIT_CLASSIFY && (ra.cleanup || ra.bound)) {
+  if (f.prepped) {
+    classify = 2;
+  } else if (RB_SPLIT_CLASSIFY && (ra.cleanup || ra.bound)) {
     launchPdl(k_prep, streamGrid(f.ncell), kThreads, 0, s, m.cur, f.ncell,
               static_cast<const double*>(f.fuse_offset), static_cast<const int32_t*>(m.count), ca,
               m.cls, m.probe, m.kstar);
