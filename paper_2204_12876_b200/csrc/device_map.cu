@@ -163,7 +163,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     const std::size_t n = grid.cells();
     const std::size_t guard = static_cast<std::size_t>(DeviceMap::kProbeGuardRows) * (grid.width + 2);
     const std::size_t np = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2) + 2 * guard;
-    const std::size_t bytes = 2 * layerBytes(n) + 4 * alignUp(n * 4) + alignUp(np * 2) +
+    const std::size_t bytes = 2 * layerBytes(n) + 5 * alignUp(n * 4) + alignUp(np * 2) +
                               alignUp((n + 1) * 4) + alignUp(n) + alignUp(n * 8) + 8 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
     Carver c{static_cast<char*>(m->slab)};
@@ -171,7 +171,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     carveLayers(c, m->alt, n);
     m->count = c.take<int32_t>(n);
     m->kstar = c.take<int32_t>(n + 32) + 32;  // kstar[-1]: the frame's "any removal" flag
-    m->heavy = c.take<uint32_t>(2 * n);
+    m->heavy = c.take<uint32_t>(3 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
     m->probe = c.take<uint16_t>(np) + guard;

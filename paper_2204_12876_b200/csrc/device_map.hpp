@@ -49,6 +49,7 @@ struct DevStats {
   unsigned long long visits;          // DDA cells emitted by pass 1
   unsigned long long heavy_cells;     // cells folded by k_fuse_heavy, one per lane
   unsigned long long vheavy_cells;    // cells folded by k_fuse_heavy, one per warp
+  unsigned long long light_cells;     // cells folded by k_fuse_list (lists built by k_side_prep)
   double drift_offset;                // applied offset (0 when not applied)
   int drift_n;
   int drift_clamped;
@@ -133,7 +134,8 @@ struct DeviceMap {
   // pass-1 jump grid (pipeline.cu k_jump_grid): one word per 16 x 16 cells
   float* jgrid = nullptr;
   int jw = 0, jh = 0;
-  uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H)
+  uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H),
+                              // then the short-cell list of k_fuse_list (W*H)
   // information-form group frames (allocated on first use, W*H each): the
   // exchanged per-cell partials (sum p/v, sum 1/v, first point, points, first
   // rank) and this rank's first point per cell

@@ -1126,13 +1126,25 @@ __device__ __forceinline__ void appendHeavy(int cnt, int heavy, size_t i, uint32
   }
 }
 
+// Appends the lanes with `pred` to `list` (warp-aggregated; order within a
+// warp kept, across warps arbitrary). All 32 lanes call it.
+__device__ __forceinline__ void appendCell(bool pred, size_t i, uint32_t* list, unsigned long long* n) {
+  const int lane = threadIdx.x & 31;
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if (!b) return;
+  unsigned base = 0;
+  if (lane == __ffs(b) - 1) base = static_cast<unsigned>(atomicAdd(n, static_cast<unsigned long long>(__popc(b))));
+  base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+  if (pred) list[base + __popc(b & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
+}
+
 // Second-stream sweep after the ingest (RB_EARLY_HEAVY): the drift offset
 // (off_p null: none) and the long-cell lists from the per-cell counts, so the
 // long-cell fold can start as soon as the sort is done, beside k_fuse (which
 // then builds no lists).
 __global__ void __launch_bounds__(kThreads)
     k_side_prep(Layers L, size_t n, const double* off_p, const int32_t* __restrict__ count, int heavy,
-                uint32_t* heavy_list, uint32_t* vheavy_list, DevStats* st, int classify,
+                uint32_t* heavy_list, uint32_t* vheavy_list, uint32_t* light_list, DevStats* st, int classify,
                 ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
                 int32_t* __restrict__ kstar) {
   const double off = off_p != nullptr ? *off_p : 0.0;
@@ -1147,8 +1159,26 @@ __global__ void __launch_bounds__(kThreads)
     }
     const int cnt = in ? count[i] : 0;
     if (heavy_list != nullptr) appendHeavy(cnt, heavy, i, heavy_list, vheavy_list, st);
+    if (light_list != nullptr) appendCell(cnt > 0 && cnt <= heavy, i, light_list, &st->light_cells);
     if (classify && in && cnt == 0) classifyCell(L, i, false, ca, cls, probe, kstar);
   }
+}
+
+// The short cells listed by k_side_prep, one thread each (grid-stride): only
+// occupied cells take threads, instead of one thread per map cell (k_fuse).
+__global__ void __launch_bounds__(kThreads)
+    k_fuse_list(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
+                const uint32_t* __restrict__ start, const double* __restrict__ spz,
+                const double* __restrict__ spv, FuseArgs a, DevStats* st) {
+  pdlWait();
+  pdlTrigger();
+  const unsigned total = static_cast<unsigned>(st->light_cells);
+  FoldCounts k;
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+    const uint32_t i = list[q];
+    foldCell(L, i, count[i], start, spz, spv, a, st, k);
+  }
+  flushCounts(k, st);
 }
 
 // Cells with at most `heavy` points are folded here, one thread per cell;
@@ -2707,6 +2737,12 @@ RayArgs rayArgs(const Frame& f) {
 #ifndef RB_EARLY_HEAVY
 #define RB_EARLY_HEAVY 1
 #endif
+#ifndef RB_FUSE_LIST
+#define RB_FUSE_LIST 1  // short-cell fold over k_side_prep's list (k_fuse_list)
+#endif
+#ifndef RB_FUSE_LIST_BLOCKS
+#define RB_FUSE_LIST_BLOCKS 2  // k_fuse_list blocks per SM (fold registers: 2 resident)
+#endif
 #ifndef RB_SIDE_CLASSIFY
 #define RB_SIDE_CLASSIFY 0  // k_side_prep also classifies the cells without points (k_fuse the rest)
 #endif
@@ -2737,7 +2773,8 @@ void phaseDrift(Frame& f, uint32_t N, bool side = false) {
       f.prepped = RB_SIDE_CLASSIFY != 0;  // (lists imply a ray pass: cleanup or bound)
       k_side_prep<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(
           m.cur, f.ncell, drift ? static_cast<const double*>(m.drift_offset) : nullptr,
-          static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell, m.stats,
+          static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell,
+          RB_FUSE_LIST ? m.heavy + 2 * f.ncell : nullptr, m.stats,
           f.prepped ? 1 : 0, ca, m.cls, m.probe, m.kstar);
     } else
       k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
@@ -2864,9 +2901,15 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     }
     classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound) ? 1 : 0;
   }
-  launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv,
-            fa, m.stats, f.heavy, f.lists_built ? nullptr : m.heavy, m.heavy + f.ncell, f.fuse_offset, classify, ca, m.cls,
-            m.probe, m.kstar);
+  if (f.lists_built && RB_FUSE_LIST && classify == 0 && f.fuse_offset == nullptr)
+    launchPdl(k_fuse_list, 148u * RB_FUSE_LIST_BLOCKS, kThreads, 0, s, m.cur,
+              static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
+              static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
+              static_cast<const double*>(m.spv), fa, m.stats);
+  else
+    launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv,
+              fa, m.stats, f.heavy, f.lists_built ? nullptr : m.heavy, m.heavy + f.ncell, f.fuse_offset,
+              classify, ca, m.cls, m.probe, m.kstar);
   ++f.launches;
   f.fuse_offset = nullptr;
   f.classified = classify != 0;
@@ -3178,7 +3221,7 @@ void preloadFrameKernels(int device) {
   const void* kernels[] = {
       reinterpret_cast<const void*>(k_shift), reinterpret_cast<const void*>(k_ingest),
       reinterpret_cast<const void*>(k_drift_finalize), reinterpret_cast<const void*>(k_apply_offset),
-      reinterpret_cast<const void*>(k_side_prep),
+      reinterpret_cast<const void*>(k_side_prep), reinterpret_cast<const void*>(k_fuse_list),
       reinterpret_cast<const void*>(k_sort_rowscan),
       reinterpret_cast<const void*>(k_sort_scatter<kSortItems>),
       reinterpret_cast<const void*>(k_sort_scatter<kSortItems, true>),
