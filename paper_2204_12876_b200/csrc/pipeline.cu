@@ -1160,7 +1160,9 @@ __global__ void __launch_bounds__(kThreads)
     const int cnt = in ? count[i] : 0;
     if (heavy_list != nullptr) appendHeavy(cnt, heavy, i, heavy_list, vheavy_list, st);
     if (light_list != nullptr) appendCell(cnt > 0 && cnt <= heavy, i, light_list, &st->light_cells);
-    if (classify && in && cnt == 0) classifyCell(L, i, false, ca, cls, probe, kstar);
+    // (classify: the cells without points, and the long cells speculatively;
+    // the short-cell fold classifies the cells it folds)
+    if (classify && in && (cnt == 0 || cnt > heavy)) classifyCell(L, i, cnt > heavy, ca, cls, probe, kstar);
   }
 }
 
@@ -1169,7 +1171,8 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     k_fuse_list(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
                 const uint32_t* __restrict__ start, const double* __restrict__ spz,
-                const double* __restrict__ spv, FuseArgs a, DevStats* st) {
+                const double* __restrict__ spv, FuseArgs a, DevStats* st, int classify, ClassArgs ca,
+                uint8_t* __restrict__ cls, ProbeT* __restrict__ probe, int32_t* __restrict__ kstar) {
   pdlWait();
   pdlTrigger();
   const unsigned total = static_cast<unsigned>(st->light_cells);
@@ -1177,6 +1180,7 @@ __global__ void __launch_bounds__(kThreads)
   for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
     const uint32_t i = list[q];
     foldCell(L, i, count[i], start, spz, spv, a, st, k);
+    if (classify) classifyCell(L, i, false, ca, cls, probe, kstar);
   }
   flushCounts(k, st);
 }
@@ -2744,7 +2748,7 @@ RayArgs rayArgs(const Frame& f) {
 #define RB_FUSE_LIST_BLOCKS 2  // k_fuse_list blocks per SM (fold registers: 2 resident)
 #endif
 #ifndef RB_SIDE_CLASSIFY
-#define RB_SIDE_CLASSIFY 0  // k_side_prep also classifies the cells without points (k_fuse the rest)
+#define RB_SIDE_CLASSIFY 1  // k_side_prep also classifies the cells without points and the long ones (k_fuse_list its cells)
 #endif
 void setOverlap(Frame& f) {
   const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
@@ -2770,7 +2774,7 @@ void phaseDrift(Frame& f, uint32_t N, bool side = false) {
     if (lists) {
       const RayArgs ra = rayArgs(f);
       const ClassArgs ca{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W};
-      f.prepped = RB_SIDE_CLASSIFY != 0;  // (lists imply a ray pass: cleanup or bound)
+      f.prepped = RB_SIDE_CLASSIFY && RB_FUSE_LIST;  // (lists imply a ray pass: cleanup or bound)
       k_side_prep<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(
           m.cur, f.ncell, drift ? static_cast<const double*>(m.drift_offset) : nullptr,
           static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell,
@@ -2901,11 +2905,12 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     }
     classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound) ? 1 : 0;
   }
-  if (f.lists_built && RB_FUSE_LIST && classify == 0 && f.fuse_offset == nullptr)
+  if (f.lists_built && RB_FUSE_LIST && (classify == 0 || f.prepped) && f.fuse_offset == nullptr)
     launchPdl(k_fuse_list, 148u * RB_FUSE_LIST_BLOCKS, kThreads, 0, s, m.cur,
               static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
               static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
-              static_cast<const double*>(m.spv), fa, m.stats);
+              static_cast<const double*>(m.spv), fa, m.stats, f.prepped ? 1 : 0, ca, m.cls, m.probe,
+              m.kstar);
   else
     launchPdl(k_fuse, gridFor(f.ncell), kThreads, 0, s, m.cur, f.ncell, m.count, m.start, m.spz, m.spv,
               fa, m.stats, f.heavy, f.lists_built ? nullptr : m.heavy, m.heavy + f.ncell, f.fuse_offset,
