@@ -69,6 +69,44 @@ constexpr uint32_t kGraphHeadPoints = RB_GRAPH_HEAD_POINTS;
 
 constexpr double kInf = __builtin_huge_val();
 
+// RB_TIMELINE (diagnostic builds): per kernel slot, the first block's start
+// (sampled: every 16th block and the last) and the last block's end
+// (%globaltimer, ns) of the frame, printed to stderr after each synchronous
+// frame (scripts/timeline.py).
+#ifdef RB_TIMELINE
+constexpr int kTlSlots = 16;
+__device__ unsigned long long g_tl[kTlSlots][2];
+__device__ unsigned long long g_tl_end[kTlSlots][32];  // block ends spread over 32 words
+__device__ __forceinline__ unsigned long long tlNow() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct TlGuard {
+  int slot;
+  // (every 16th block and the last one record: fewer atomics on one address)
+  __device__ explicit TlGuard(int s) : slot(s) {
+    if (threadIdx.x == 0 && ((blockIdx.x & 15) == 0 || blockIdx.x == gridDim.x - 1))
+      atomicMin(&g_tl[s][0], tlNow());
+  }
+  __device__ ~TlGuard() {
+    if (threadIdx.x == 0) atomicMax(&g_tl_end[slot][blockIdx.x & 31], tlNow());
+  }
+};
+#define RB_TL(slot) TlGuard tl_guard_(slot)
+__global__ void k_tl_reset() {
+  if (threadIdx.x < kTlSlots) {
+    g_tl[threadIdx.x][0] = ~0ull;
+    g_tl[threadIdx.x][1] = 0ull;
+  }
+  for (int k = threadIdx.x; k < kTlSlots * 32; k += blockDim.x) g_tl_end[k / 32][k % 32] = 0ull;
+}
+#else
+#define RB_TL(slot) \
+  do {              \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double dnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
@@ -152,6 +190,7 @@ __device__ __forceinline__ void invalidateCell(const Layers& L, size_t i) {
 constexpr int kShiftThreads = 256;
 __global__ void __launch_bounds__(kShiftThreads) k_shift(Layers in, Layers out, int W, int H, int dc,
                                                          int dr) {
+  RB_TL(0);
   const int r = blockIdx.y;
   const int sr = r + dr;
   const bool row_in = sr >= 0 && sr < H;
@@ -418,6 +457,7 @@ __global__ void __launch_bounds__(kThreads)
              uint8_t* __restrict__ kept, double* __restrict__ drift_part,
              int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
              uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base, uint32_t in_base) {
+  RB_TL(1);
   pdlEnter();
   // k_base: first point of this launch (a chunk of a frame whose upload is
   // split); block partials are indexed by the frame-wide block k / kThreads.
@@ -480,6 +520,7 @@ __global__ void __launch_bounds__(kThreads)
                  int* __restrict__ drift_npart, uint32_t* __restrict__ tc0, uint32_t pitch,
                  uint32_t dmask, int count_cells, DevStats* st, uint32_t k_base, uint32_t in_base,
                  uint32_t ntl) {
+  RB_TL(1);
   pdlEnter();
   constexpr uint32_t kTileBytes = 3 * kThreads * sizeof(double);  // 6 KB
   __shared__ alignas(128) double s_buf[2][3 * kThreads];
@@ -537,12 +578,14 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(1024)
     k_drift_finalize(const double* part, const int* npart, int nblocks, int min_points,
                      double max_off, double* offset_out, DevStats* st) {
+  RB_TL(5);
   pdlEnter();
   driftFinalizeBlock(part, npart, nblocks, min_points, max_off, offset_out, st);
 }
 
 // Reference drift.cpp:44-55 as a separate sweep (RB_FUSE_OFFSET=0 builds).
 __global__ void __launch_bounds__(kThreads) k_apply_offset(Layers L, size_t n, const double* off_p) {
+  RB_TL(6);
   pdlEnter();
   const double off = *off_p;
   if (off == 0.0) return;
@@ -689,6 +732,7 @@ struct SortGeom {
 // Row d of tc -> exclusive offsets within the digit; rowsum[d] = row total.
 __global__ void __launch_bounds__(kThreads)
     k_sort_rowscan(uint32_t* __restrict__ tc, uint32_t pitch, uint32_t* __restrict__ rowsum) {
+  RB_TL(2);
   pdlEnter();
   uint4* row = reinterpret_cast<uint4*>(tc + static_cast<size_t>(blockIdx.x) * pitch);
   const uint32_t nq = pitch / 4;
@@ -721,6 +765,7 @@ __global__ void __launch_bounds__(kThreads)
                    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                    const double* __restrict__ pz, const double* __restrict__ pvar,
                    double* __restrict__ spz, double* __restrict__ spv, uint32_t* start) {
+  RB_TL(3 + pass);
   pdlEnter();
   extern __shared__ unsigned char smem[];
   const int dbits = sg.dbits, shift = pass * dbits;
@@ -954,7 +999,7 @@ constexpr int kFoldBatch = 8;
 #endif
 constexpr int kHeavyCell = RB_HEAVY_CELL;
 #ifndef RB_HEAVY_BLOCKS
-#define RB_HEAVY_BLOCKS 256
+#define RB_HEAVY_BLOCKS 512
 #endif
 constexpr int kHeavyBlocks = RB_HEAVY_BLOCKS;  // one warp each
 
@@ -1096,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 #ifndef RB_VHEAVY_CELL
-#define RB_VHEAVY_CELL 256  // (64 / 96 / 128 measured slower)
+#define RB_VHEAVY_CELL 160  // (128 / 192 / 224 / 256 measured)
 #endif
 constexpr int kVeryHeavyCell = RB_VHEAVY_CELL;
 
@@ -1147,6 +1192,7 @@ __global__ void __launch_bounds__(kThreads)
                 uint32_t* heavy_list, uint32_t* vheavy_list, uint32_t* light_list, DevStats* st, int classify,
                 ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
                 int32_t* __restrict__ kstar) {
+  RB_TL(6);
   const double off = off_p != nullptr ? *off_p : 0.0;
   const int lane = threadIdx.x & 31;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -1168,11 +1214,22 @@ __global__ void __launch_bounds__(kThreads)
 
 // The short cells listed by k_side_prep, one thread each (grid-stride): only
 // occupied cells take threads, instead of one thread per map cell (k_fuse).
-__global__ void __launch_bounds__(kThreads)
+// 3 blocks of 128 threads per SM at the fold's 128 registers leave a quarter
+// of the register file to the long-cell fold, which starts at the same time
+// on the second stream (a full register file would hold its warps back until
+// short-fold blocks retire).
+#ifndef RB_FUSE_LIST_THREADS
+#define RB_FUSE_LIST_THREADS 128
+#endif
+#ifndef RB_FUSE_LIST_BLOCKS
+#define RB_FUSE_LIST_BLOCKS 3  // k_fuse_list blocks per SM
+#endif
+__global__ void __launch_bounds__(RB_FUSE_LIST_THREADS)
     k_fuse_list(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
                 const uint32_t* __restrict__ start, const double* __restrict__ spz,
                 const double* __restrict__ spv, FuseArgs a, DevStats* st, int classify, ClassArgs ca,
                 uint8_t* __restrict__ cls, ProbeT* __restrict__ probe, int32_t* __restrict__ kstar) {
+  RB_TL(7);
   pdlWait();
   pdlTrigger();
   const unsigned total = static_cast<unsigned>(st->light_cells);
@@ -1201,6 +1258,7 @@ __global__ void __launch_bounds__(kThreads)
            uint32_t* heavy_list, uint32_t* vheavy_list, const double* __restrict__ off_p,
            int classify, ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
            int32_t* __restrict__ kstar) {
+  RB_TL(7);
   // wait first: the ray pass launched on our trigger may then read anything
   // older than this kernel before its own wait. When the ray pass follows
   // directly (classify 2), trigger only once the fold is done: resident
@@ -1252,6 +1310,7 @@ __global__ void __launch_bounds__(32)
                  const uint32_t* __restrict__ start, const double* __restrict__ spz,
                  const double* __restrict__ spv, FuseArgs a, DevStats* st, double t_free,
                  int cleanup, int bound) {
+  RB_TL(8);
   __shared__ double sz[kHeavyStage];
   __shared__ double sv[kHeavyStage];
   const int lane = threadIdx.x;
@@ -1331,6 +1390,7 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
                                                        const int32_t* __restrict__ count,
                                                        int heavy, int retry, DevStats* st,
                                                        ProbeT* probe) {
+  RB_TL(9 + retry);
   // wait first: the ray pass launched on our trigger may then read anything
   // older than this kernel before its own wait
   pdlWait();
@@ -1357,6 +1417,7 @@ __global__ void __launch_bounds__(kThreads) k_classify(Layers L, size_t n, RayAr
 // the border. One warp per block: lanes 0-17 take the 18 ring columns.
 __global__ void __launch_bounds__(kThreads) k_jump_grid(const ProbeT* __restrict__ probe, int W, int H,
                                                         float* __restrict__ jg, int jw, int jh) {
+  RB_TL(11);
   pdlWait();
   pdlTrigger();
   const int warp = static_cast<int>((blockIdx.x * static_cast<unsigned>(kThreads) + threadIdx.x) >> 5);
@@ -2081,6 +2142,7 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
                  Layers L, const uint8_t* __restrict__ cls, int32_t* kstar, uint32_t* raylist,
                  DevStats* st, int retry, uint32_t ray_base, const ProbeT* __restrict__ probe,
                  const uint32_t* __restrict__ pcell) {
+  RB_TL(12 + kStride);
   pdlTrigger();  // the per-ray setup runs before the wait (inputs from k_ingest)
   if (retry && !st->respeculate) return;
   for (uint32_t k0 = blockIdx.x * kP1Threads; k0 < n;
@@ -2126,6 +2188,7 @@ __global__ void __launch_bounds__(kP1Threads, RB_PASS1_MIN_BLOCKS)
                 const double* __restrict__ pz, RayArgs a, Layers L, uint8_t* cls,
                 int32_t* kstar, uint32_t* raylist, DevStats* st, ProbeT* probe,
                 const uint32_t* __restrict__ pcell, double* ub2) {
+  RB_TL(14);
   pdlWait();
   pdlTrigger();
   if (retry && st->respeculate) {
@@ -2425,6 +2488,7 @@ template <int RT>
 __global__ void __launch_bounds__(kTileX* kTileY)
     k_cells(Layers L, int32_t* __restrict__ count, uint32_t* __restrict__ seg_start, CellArgs a,
             DevStats* st) {
+  RB_TL(15);
   pdlEnter();
   extern __shared__ unsigned char smem[];
   const int halo = a.radius > 1 ? a.radius : 1;
@@ -2744,9 +2808,6 @@ RayArgs rayArgs(const Frame& f) {
 #ifndef RB_FUSE_LIST
 #define RB_FUSE_LIST 1  // short-cell fold over k_side_prep's list (k_fuse_list)
 #endif
-#ifndef RB_FUSE_LIST_BLOCKS
-#define RB_FUSE_LIST_BLOCKS 2  // k_fuse_list blocks per SM (fold registers: 2 resident)
-#endif
 #ifndef RB_SIDE_CLASSIFY
 #define RB_SIDE_CLASSIFY 1  // k_side_prep also classifies the cells without points and the long ones (k_fuse_list its cells)
 #endif
@@ -2906,7 +2967,7 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound) ? 1 : 0;
   }
   if (f.lists_built && RB_FUSE_LIST && (classify == 0 || f.prepped) && f.fuse_offset == nullptr)
-    launchPdl(k_fuse_list, 148u * RB_FUSE_LIST_BLOCKS, kThreads, 0, s, m.cur,
+    launchPdl(k_fuse_list, 148u * RB_FUSE_LIST_BLOCKS, RB_FUSE_LIST_THREADS, 0, s, m.cur,
               static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
               static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
               static_cast<const double*>(m.spv), fa, m.stats, f.prepped ? 1 : 0, ca, m.cls, m.probe,
@@ -3218,6 +3279,9 @@ ScanResult resultFrom(const DevStats& d, std::size_t n) {
 // Loads the frame kernels' code on this device now (map creation) rather than
 // at their first launch: with the runtime's lazy module loading the first
 // frame of a process otherwise pays ~10 ms on the device.
+#ifndef RB_CARVEOUT
+#define RB_CARVEOUT -1  // (-1: the driver's choice per kernel; 25 / 50 / 100 measured slower)
+#endif
 void preloadFrameKernels(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64 || done[device]) return;
@@ -3225,6 +3289,7 @@ void preloadFrameKernels(int device) {
   cudaFuncAttributes fa;
   const void* kernels[] = {
       reinterpret_cast<const void*>(k_shift), reinterpret_cast<const void*>(k_ingest),
+      reinterpret_cast<const void*>(k_ingest_tma),
       reinterpret_cast<const void*>(k_drift_finalize), reinterpret_cast<const void*>(k_apply_offset),
       reinterpret_cast<const void*>(k_side_prep), reinterpret_cast<const void*>(k_fuse_list),
       reinterpret_cast<const void*>(k_sort_rowscan),
@@ -3238,7 +3303,15 @@ void preloadFrameKernels(int device) {
       reinterpret_cast<const void*>(k_rays_tail), reinterpret_cast<const void*>(k_cells<0>),
       reinterpret_cast<const void*>(k_cells<1>), reinterpret_cast<const void*>(k_cells<2>),
       reinterpret_cast<const void*>(k_cells_global)};
-  for (const void* k : kernels) cudaFuncGetAttributes(&fa, k);
+  // One shared-memory carveout for every frame kernel (RB_CARVEOUT, percent
+  // of the unified L1 / shared memory): kernels of both streams share SMs, and
+  // an SM runs one carveout at a time -- with the driver's per-kernel choice,
+  // blocks of the long-cell fold (34 KB) could not join an SM running the
+  // short-cell fold (1 KB) until it drained.
+  for (const void* k : kernels) {
+    cudaFuncGetAttributes(&fa, k);
+    if (RB_CARVEOUT >= 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, RB_CARVEOUT);
+  }
   cudaGetLastError();
 }
 
@@ -3289,6 +3362,9 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
     if (!chunked) recordTiming(m.ev[13], f.s);  // copy done
   }
   phaseBegin(f, false);
+#ifdef RB_TIMELINE
+  k_tl_reset<<<1, 32, 0, f.s>>>();
+#endif
   // count[] is all zero here: k_cells clears it after its last use each scan.
   const SortGeom sg = phaseSortGeometry(f, N);
   RB_PHASE_EVENT(1, f.s);  // resets done
@@ -3316,6 +3392,20 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
   const auto t_sub = std::chrono::steady_clock::now();
 #endif
   const DevStats& d = phaseStatsWait(f);
+#ifdef RB_TIMELINE
+  {
+    checkCuda(cudaStreamSynchronize(f.s), "timeline");
+    unsigned long long tl[kTlSlots][2];
+    checkCuda(cudaMemcpyFromSymbol(tl, g_tl, sizeof(tl)), "timeline");
+    unsigned long long te[kTlSlots][32];
+    checkCuda(cudaMemcpyFromSymbol(te, g_tl_end, sizeof(te)), "timeline");
+    for (int k = 0; k < kTlSlots; ++k)
+      for (int j = 0; j < 32; ++j) tl[k][1] = std::max(tl[k][1], te[k][j]);
+    fprintf(stderr, "TL");
+    for (int k = 0; k < kTlSlots; ++k) fprintf(stderr, " %llu %llu", tl[k][0], tl[k][1]);
+    fprintf(stderr, "\n");
+  }
+#endif
   ScanResult out = resultFrom(d, n);
 #ifdef RB_HOST_DIAG
   {  // host-side split of the call: submission, wait (averages every 200 calls)
