@@ -1214,15 +1214,11 @@ __global__ void __launch_bounds__(kThreads)
 
 // The short cells listed by k_side_prep, one thread each (grid-stride): only
 // occupied cells take threads, instead of one thread per map cell (k_fuse).
-// 3 blocks of 128 threads per SM at the fold's 128 registers leave a quarter
-// of the register file to the long-cell fold, which starts at the same time
-// on the second stream (a full register file would hold its warps back until
-// short-fold blocks retire).
 #ifndef RB_FUSE_LIST_THREADS
-#define RB_FUSE_LIST_THREADS 128
+#define RB_FUSE_LIST_THREADS 256
 #endif
 #ifndef RB_FUSE_LIST_BLOCKS
-#define RB_FUSE_LIST_BLOCKS 3  // k_fuse_list blocks per SM
+#define RB_FUSE_LIST_BLOCKS 2  // k_fuse_list blocks per SM (3 x 128 threads: slower)
 #endif
 __global__ void __launch_bounds__(RB_FUSE_LIST_THREADS)
     k_fuse_list(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
