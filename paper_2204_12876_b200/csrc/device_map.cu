@@ -133,11 +133,16 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
   m->device = device;
   m->grid = grid;
   try {
-    checkCuda(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream create");
     // (RB_STREAM2_PRIO: the long-cell fold's stream at the highest priority, so
-    // its blocks take SM slots as the ray pass's retire)
+    // its blocks take SM slots as the ray pass's retire; RB_MAIN_PRIO: the
+    // frame stream at the highest priority)
     int prio_lo = 0, prio_hi = 0;
     checkCuda(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
+#ifndef RB_MAIN_PRIO
+#define RB_MAIN_PRIO 0
+#endif
+    checkCuda(cudaStreamCreateWithPriority(&m->stream, cudaStreamNonBlocking, RB_MAIN_PRIO ? prio_hi : prio_lo),
+              "stream create");
 #ifndef RB_STREAM2_PRIO
 #define RB_STREAM2_PRIO 0  // measured slower
 #endif
@@ -149,6 +154,9 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     checkCuda(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_dfork, cudaEventDisableTiming), "event create");
     checkCuda(cudaEventCreateWithFlags(&m->ev_djoin, cudaEventDisableTiming), "event create");
+    checkCuda(cudaEventCreateWithFlags(&m->ev_sfork, cudaEventDisableTiming), "event create");
+    checkCuda(cudaEventCreateWithFlags(&m->ev_sjoin, cudaEventDisableTiming), "event create");
+    checkCuda(cudaStreamCreateWithFlags(&m->stream3, cudaStreamNonBlocking), "stream create");
     checkCuda(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "stream create");
     for (auto& e : m->ev_chunk)
       checkCuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
@@ -163,7 +171,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     const std::size_t n = grid.cells();
     const std::size_t guard = static_cast<std::size_t>(DeviceMap::kProbeGuardRows) * (grid.width + 2);
     const std::size_t np = static_cast<std::size_t>(grid.width + 2) * (grid.height + 2) + 2 * guard;
-    const std::size_t bytes = 2 * layerBytes(n) + 5 * alignUp(n * 4) + alignUp(np * 2) +
+    const std::size_t bytes = 2 * layerBytes(n) + 6 * alignUp(n * 4) + alignUp(np * 2) +
                               alignUp((n + 1) * 4) + alignUp(n) + alignUp(n * 8) + 8 * kAlign;
     checkCuda(cudaMalloc(&m->slab, bytes), "map allocation");
     Carver c{static_cast<char*>(m->slab)};
@@ -171,7 +179,7 @@ DeviceMap* createDeviceMap(int device, const Grid& grid) {
     carveLayers(c, m->alt, n);
     m->count = c.take<int32_t>(n);
     m->kstar = c.take<int32_t>(n + 32) + 32;  // kstar[-1]: the frame's "any removal" flag
-    m->heavy = c.take<uint32_t>(3 * n);
+    m->heavy = c.take<uint32_t>(4 * n);
     m->start = c.take<uint32_t>(n + 1);
     m->cls = c.take<uint8_t>(n);
     m->probe = c.take<uint16_t>(np) + guard;
@@ -236,6 +244,9 @@ void destroyDeviceMap(DeviceMap* m) {
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_dfork) cudaEventDestroy(m->ev_dfork);
   if (m->ev_djoin) cudaEventDestroy(m->ev_djoin);
+  if (m->ev_sfork) cudaEventDestroy(m->ev_sfork);
+  if (m->ev_sjoin) cudaEventDestroy(m->ev_sjoin);
+  if (m->stream3) cudaStreamDestroy(m->stream3);
   for (int k = 0; k < m->graph_count; ++k) cudaGraphExecDestroy(m->graphs[k]);
   for (auto& e : m->ev_chunk)
     if (e) cudaEventDestroy(e);

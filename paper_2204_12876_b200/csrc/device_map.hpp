@@ -50,6 +50,7 @@ struct DevStats {
   unsigned long long heavy_cells;     // cells folded by k_fuse_heavy, one per lane
   unsigned long long vheavy_cells;    // cells folded by k_fuse_heavy, one per warp
   unsigned long long light_cells;     // cells folded by k_fuse_list (lists built by k_side_prep)
+  unsigned long long pre_cells;       // cells folded before the ray pass (RB_PRESPLIT)
   double drift_offset;                // applied offset (0 when not applied)
   int drift_n;
   int drift_clamped;
@@ -117,6 +118,7 @@ struct DeviceMap {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // long-cell fold, overlapped with the ray pass
+  cudaStream_t stream3 = nullptr;  // short-cell fold, overlapped with the ray pass (RB_PRESPLIT)
   Grid grid;
   Layers cur, alt;
   void* slab = nullptr;  // backing allocation of both layer sets + cell scratch
@@ -135,7 +137,8 @@ struct DeviceMap {
   float* jgrid = nullptr;
   int jw = 0, jh = 0;
   uint32_t* heavy = nullptr;  // ids of cells queued for the side-stream fold (2 lists of W*H),
-                              // then the short-cell list of k_fuse_list (W*H)
+                              // the short-cell list of k_fuse_list (W*H), the cells folded
+                              // before the ray pass (W*H)
   // information-form group frames (allocated on first use, W*H each): the
   // exchanged per-cell partials (sum p/v, sum 1/v, first point, points, first
   // rank) and this rank's first point per cell
@@ -209,6 +212,7 @@ struct DeviceMap {
   cudaEvent_t ev_after = nullptr;  // relief_gpu_map_after_stream
   cudaEvent_t ev_fork = nullptr;   // frame stream -> copy stream (chunked upload)
   cudaEvent_t ev_dfork = nullptr, ev_djoin = nullptr;  // drift on stream2 (phaseDrift side)
+  cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;  // short-cell fold on stream3
   // Executable graphs of recent synchronous-frame topologies, most recent
   // first (pipeline.cu FrameCapture); off: direct launches.
   static constexpr int kGraphs = 4;

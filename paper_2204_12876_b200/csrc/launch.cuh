@@ -58,6 +58,25 @@ void launchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem
 #endif
 }
 
+// Launch with a per-launch scheduling priority (cudaLaunchAttributePriority;
+// kept on the node of a captured graph instantiated with
+// cudaGraphInstantiateFlagUseNodePriority).
+template <typename... KArgs, typename... Args>
+void launchPrio(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+                int priority, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = priority;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  checkCuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+}
+
 // Cooperative launch (all blocks co-resident, for a grid barrier), chained
 // like launchPdl.
 template <typename... KArgs, typename... Args>

@@ -1189,7 +1189,8 @@ __device__ __forceinline__ void appendCell(bool pred, size_t i, uint32_t* list, 
 // then builds no lists).
 __global__ void __launch_bounds__(kThreads)
     k_side_prep(Layers L, size_t n, const double* off_p, const int32_t* __restrict__ count, int heavy,
-                uint32_t* heavy_list, uint32_t* vheavy_list, uint32_t* light_list, DevStats* st, int classify,
+                uint32_t* heavy_list, uint32_t* vheavy_list, uint32_t* light_list, uint32_t* pre_list,
+                DevStats* st, int classify,
                 ClassArgs ca, uint8_t* __restrict__ cls, ProbeT* __restrict__ probe,
                 int32_t* __restrict__ kstar) {
   RB_TL(6);
@@ -1204,12 +1205,40 @@ __global__ void __launch_bounds__(kThreads)
       if (L.ubv[i]) L.ub[i] += off;
     }
     const int cnt = in ? count[i] : 0;
-    if (heavy_list != nullptr) appendHeavy(cnt, heavy, i, heavy_list, vheavy_list, st);
-    if (light_list != nullptr) appendCell(cnt > 0 && cnt <= heavy, i, light_list, &st->light_cells);
+    // pre_list (RB_PRESPLIT): a cell with points whose class before the fold
+    // is "removal candidate" (valid, stale, with a normal) ends the fold as a
+    // candidate or, if it fuses, as "none" -- it is folded and classified
+    // before the ray pass. Every other cell with points ends the fold "none"
+    // (it fuses, so it is fresh; or it stays valid and fresh, or without a
+    // normal; only a variance error could leave it otherwise, which the folds'
+    // checkSpeculation turns into a retry): classified "none" here and folded
+    // beside the ray pass.
+    bool pre = false;
+    if (pre_list != nullptr && cnt > 0)
+      pre = L.valid[i] && ca.cleanup && !(ca.now - L.last[i] <= ca.t_free) &&
+            (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0);
+    const int lc = pre ? 0 : cnt;
+    if (heavy_list != nullptr) appendHeavy(lc, heavy, i, heavy_list, vheavy_list, st);
+    if (light_list != nullptr) appendCell(lc > 0 && lc <= heavy, i, light_list, &st->light_cells);
+    if (pre_list != nullptr) appendCell(pre, i, pre_list, &st->pre_cells);
     // (classify: the cells without points, and the long cells speculatively;
     // the short-cell fold classifies the cells it folds)
-    if (classify && in && (cnt == 0 || cnt > heavy)) classifyCell(L, i, cnt > heavy, ca, cls, probe, kstar);
+    if (pre_list != nullptr) {
+      if (in && !pre) classifyCell(L, i, cnt > 0, ca, cls, probe, kstar);
+    } else if (classify && in && (cnt == 0 || cnt > heavy)) {
+      classifyCell(L, i, cnt > heavy, ca, cls, probe, kstar);
+    }
   }
+}
+
+// Post-fusion ray class of a cell the concurrent ray pass treated as "none";
+// flags a wrong speculation (DESIGN.md §5.1).
+__device__ __forceinline__ void checkSpeculation(const Layers& L, size_t i, const FuseArgs& a,
+                                                 double t_free, int cleanup, int bound, DevStats* st) {
+  const bool none = L.valid[i] ? !(cleanup && !(a.now - L.last[i] <= t_free) &&
+                                   (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0))
+                               : !bound;
+  if (!none) atomicExch(&st->respeculate, 1);
 }
 
 // The short cells listed by k_side_prep, one thread each (grid-stride): only
@@ -1222,18 +1251,22 @@ __global__ void __launch_bounds__(kThreads)
 #endif
 __global__ void __launch_bounds__(RB_FUSE_LIST_THREADS)
     k_fuse_list(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
-                const uint32_t* __restrict__ start, const double* __restrict__ spz,
-                const double* __restrict__ spv, FuseArgs a, DevStats* st, int classify, ClassArgs ca,
-                uint8_t* __restrict__ cls, ProbeT* __restrict__ probe, int32_t* __restrict__ kstar) {
+                const unsigned long long* n_list, const uint32_t* __restrict__ start,
+                const double* __restrict__ spz, const double* __restrict__ spv, FuseArgs a,
+                DevStats* st, int classify, ClassArgs ca, uint8_t* __restrict__ cls,
+                ProbeT* __restrict__ probe, int32_t* __restrict__ kstar) {
   RB_TL(7);
   pdlWait();
   pdlTrigger();
-  const unsigned total = static_cast<unsigned>(st->light_cells);
+  // classify 1: classify each folded cell; 2: it was classified "none" before
+  // the fold (RB_PRESPLIT) -- check that (a wrong class retries the ray pass)
+  const unsigned total = static_cast<unsigned>(*n_list);
   FoldCounts k;
   for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
     const uint32_t i = list[q];
     foldCell(L, i, count[i], start, spz, spv, a, st, k);
-    if (classify) classifyCell(L, i, false, ca, cls, probe, kstar);
+    if (classify == 1) classifyCell(L, i, false, ca, cls, probe, kstar);
+    if (classify == 2) checkSpeculation(L, i, a, ca.t_free, ca.cleanup, ca.bound, st);
   }
   flushCounts(k, st);
 }
@@ -1280,16 +1313,6 @@ __global__ void __launch_bounds__(kThreads)
     classifyCell(L, i, is_heavy, ca, cls, probe, kstar);
   flushCounts(k, st);
   if (classify == 2) pdlTrigger();
-}
-
-// Post-fusion ray class of a cell the concurrent ray pass treated as "none";
-// flags a wrong speculation (DESIGN.md §5.1).
-__device__ __forceinline__ void checkSpeculation(const Layers& L, size_t i, const FuseArgs& a,
-                                                 double t_free, int cleanup, int bound, DevStats* st) {
-  const bool none = L.valid[i] ? !(cleanup && !(a.now - L.last[i] <= t_free) &&
-                                   (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0))
-                               : !bound;
-  if (!none) atomicExch(&st->respeculate, 1);
 }
 
 // Long cells (queued by k_fuse), concurrently with the ray pass. The very
@@ -2591,6 +2614,7 @@ struct Frame {
   bool classified = false;  // k_fuse wrote this frame's ray classes
   bool drift_join = false;  // phaseDrift(side) ran on stream2: join before the fold
   bool prepped = false;     // k_side_prep classified the cells without points
+  bool presplit = false;    // RB_PRESPLIT: candidates folded before the ray pass, the rest beside it
   bool lists_built = false; // k_side_prep queued the long cells (the long fold starts after the sort)
   // Removal of k* < inf cells: in k_cells (fold_remove, set when the ray pass
   // ran with cleanup on), or by k_remove right after the ray pass
@@ -2804,6 +2828,24 @@ RayArgs rayArgs(const Frame& f) {
 #ifndef RB_FUSE_LIST
 #define RB_FUSE_LIST 1  // short-cell fold over k_side_prep's list (k_fuse_list)
 #endif
+#ifndef RB_HEAVY_PRIO
+#define RB_HEAVY_PRIO 0
+#endif
+#ifndef RB_MAIN_PRIO
+#define RB_MAIN_PRIO 0
+#endif
+#ifndef RB_B_AFTER_A
+#define RB_B_AFTER_A 0  // the short-cell fold beside the ray pass starts after the candidates' fold
+#endif
+#ifndef RB_PRE_THREADS
+#define RB_PRE_THREADS 64  // block size of the fold of the removal candidates before the ray pass
+#endif
+#ifndef RB_SFOLD_BLOCKS
+#define RB_SFOLD_BLOCKS 2  // blocks per SM of the short-cell fold beside the ray pass
+#endif
+#ifndef RB_PRESPLIT
+#define RB_PRESPLIT 1  // fold only the removal candidates before the ray pass, the rest beside it
+#endif
 #ifndef RB_SIDE_CLASSIFY
 #define RB_SIDE_CLASSIFY 1  // k_side_prep also classifies the cells without points and the long ones (k_fuse_list its cells)
 #endif
@@ -2832,10 +2874,12 @@ void phaseDrift(Frame& f, uint32_t N, bool side = false) {
       const RayArgs ra = rayArgs(f);
       const ClassArgs ca{ra.now, ra.t_free, ra.cleanup, ra.bound, ra.g.W};
       f.prepped = RB_SIDE_CLASSIFY && RB_FUSE_LIST;  // (lists imply a ray pass: cleanup or bound)
+      f.presplit = f.prepped && RB_PRESPLIT;
       k_side_prep<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(
           m.cur, f.ncell, drift ? static_cast<const double*>(m.drift_offset) : nullptr,
           static_cast<const int32_t*>(m.count), f.heavy, m.heavy, m.heavy + f.ncell,
-          RB_FUSE_LIST ? m.heavy + 2 * f.ncell : nullptr, m.stats,
+          RB_FUSE_LIST ? m.heavy + 2 * f.ncell : nullptr, f.presplit ? m.heavy + 3 * f.ncell : nullptr,
+          m.stats,
           f.prepped ? 1 : 0, ca, m.cls, m.probe, m.kstar);
     } else
       k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
@@ -2870,9 +2914,16 @@ void launchHeavy(Frame& f) {
   const bool cleanup = f.P.cleanup.cleanup_enabled, bound = f.P.cleanup.upper_bound_enabled;
   checkCuda(cudaEventRecord(m.ev[10], f.s), "event");
   checkCuda(cudaStreamWaitEvent(m.stream2, m.ev[10], 0), "stream wait");
-  k_fuse_heavy<<<kHeavyBlocks, 32, 0, m.stream2>>>(m.cur, m.count, m.heavy, m.heavy + f.ncell, m.stats,
-                                                    m.start, m.spz, m.spv, f.fa, m.stats,
-                                                    f.P.cleanup.t_free, cleanup, bound);
+  // (RB_HEAVY_PRIO: the long-cell fold, the critical path from the end of the
+  // sort, at the highest scheduling priority)
+  int prio_lo = 0, prio_hi = 0;
+  if (RB_HEAVY_PRIO) checkCuda(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
+  launchPrio(k_fuse_heavy, kHeavyBlocks, 32, 0, m.stream2, RB_HEAVY_PRIO ? prio_hi : prio_lo, m.cur,
+             static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy),
+             static_cast<const uint32_t*>(m.heavy + f.ncell), static_cast<const DevStats*>(m.stats),
+             static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
+             static_cast<const double*>(m.spv), f.fa, m.stats, f.P.cleanup.t_free, cleanup ? 1 : 0,
+             bound ? 1 : 0);
   ++f.launches;
   checkCuda(cudaEventRecord(m.ev[11], m.stream2), "event");
 }
@@ -2962,9 +3013,30 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     }
     classify = RB_FUSE_CLASSIFY && (ra.cleanup || ra.bound) ? 1 : 0;
   }
-  if (f.lists_built && RB_FUSE_LIST && (classify == 0 || f.prepped) && f.fuse_offset == nullptr)
+  if (f.presplit) {
+    // The removal candidates with points folded and classified first (usually
+    // none: small blocks, enqueued first, so they find room beside the folds
+    // below), then the short cells on stream3 beside the ray pass (checked,
+    // not classified).
+    checkCuda(cudaEventRecord(m.ev_sfork, s), "event");
+    launchPdl(k_fuse_list, 148u, RB_PRE_THREADS, 0, s, m.cur, static_cast<const int32_t*>(m.count),
+              static_cast<const uint32_t*>(m.heavy + 3 * f.ncell),
+              static_cast<const unsigned long long*>(&m.stats->pre_cells),
+              static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
+              static_cast<const double*>(m.spv), fa, m.stats, 1, ca, m.cls, m.probe, m.kstar);
+    if (RB_B_AFTER_A) checkCuda(cudaEventRecord(m.ev_sfork, s), "event");
+    checkCuda(cudaStreamWaitEvent(m.stream3, m.ev_sfork, 0), "stream wait");
+    k_fuse_list<<<148u * RB_SFOLD_BLOCKS, RB_FUSE_LIST_THREADS, 0, m.stream3>>>(
+        m.cur, static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
+        static_cast<const unsigned long long*>(&m.stats->light_cells), static_cast<const uint32_t*>(m.start),
+        static_cast<const double*>(m.spz), static_cast<const double*>(m.spv), fa, m.stats, 2, ca, m.cls,
+        m.probe, m.kstar);
+    checkCuda(cudaEventRecord(m.ev_sjoin, m.stream3), "event");
+    ++f.launches;
+  } else if (f.lists_built && RB_FUSE_LIST && (classify == 0 || f.prepped) && f.fuse_offset == nullptr)
     launchPdl(k_fuse_list, 148u * RB_FUSE_LIST_BLOCKS, RB_FUSE_LIST_THREADS, 0, s, m.cur,
               static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
+              static_cast<const unsigned long long*>(&m.stats->light_cells),
               static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
               static_cast<const double*>(m.spv), fa, m.stats, f.prepped ? 1 : 0, ca, m.cls, m.probe,
               m.kstar);
@@ -3043,6 +3115,7 @@ void phaseRaysTail(Frame& f, uint32_t N) {
   const bool pass2 = ra.cleanup && ra.bound;
   if (ra.cleanup) f.fold_remove = true;
   if (f.overlap) checkCuda(cudaStreamWaitEvent(f.s, m.ev[11], 0), "stream wait");
+  if (f.presplit) checkCuda(cudaStreamWaitEvent(f.s, m.ev_sjoin, 0), "stream wait");
   if (!retry && !pass2) return;
   static int blocks_per_sm = 0, sms = 0;
   if (blocks_per_sm == 0) {
@@ -3227,7 +3300,9 @@ struct FrameCapture {
       }
     }
     if (exec == nullptr) {
-      const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+      // (RB_MAIN_PRIO: the captured streams' priorities kept on the graph's nodes)
+      const cudaError_t e =
+          cudaGraphInstantiate(&exec, g, (RB_MAIN_PRIO || RB_HEAVY_PRIO) ? cudaGraphInstantiateFlagUseNodePriority : 0);
       if (e != cudaSuccess) {
         cudaGraphDestroy(g);
         checkCuda(e, "graph instantiate");
@@ -3399,7 +3474,8 @@ ScanResult integrateScanDevice(DeviceMap& m, const PipelineParams& P, const doub
       for (int j = 0; j < 32; ++j) tl[k][1] = std::max(tl[k][1], te[k][j]);
     fprintf(stderr, "TL");
     for (int k = 0; k < kTlSlots; ++k) fprintf(stderr, " %llu %llu", tl[k][0], tl[k][1]);
-    fprintf(stderr, "\n");
+    fprintf(stderr, "\nTLC pre %llu light %llu heavy %llu vheavy %llu respec %d\n", d.pre_cells,
+            d.light_cells, d.heavy_cells, d.vheavy_cells, d.respeculate);
   }
 #endif
   ScanResult out = resultFrom(d, n);

@@ -58,6 +58,9 @@ def main():
         t0 = v[2]  # ingest start
         rows.append([(v[2 * k] - t0, v[2 * k + 1] - t0) if v[2 * k + 1] else None for k in range(len(SLOTS))])
     print(f"{name}: median over the last {len(rows)} frames (us from the ingest start)")
+    counts = [l for l in r.stderr.splitlines() if l.startswith("TLC ")]
+    if counts:
+        print("  last frame's lists:", counts[-1][4:])
     for k, label in enumerate(SLOTS):
         vals = [r[k] for r in rows if r[k] is not None]
         if not vals:
