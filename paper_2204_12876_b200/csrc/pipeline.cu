@@ -1390,6 +1390,9 @@ __global__ void __launch_bounds__(32)
   const unsigned busy = nv < gridDim.x ? nv : 0u;
   if (blockIdx.x < busy) {
     flushCounts(k, st);
+#ifdef RB_TIMELINE
+    if (lane == 0) atomicMax(&g_tl_end[9][blockIdx.x & 31], tlNow());  // warp-per-cell part's end
+#endif
     return;
   }
   for (unsigned q = (blockIdx.x - busy) * 32 + lane; q < total; q += (gridDim.x - busy) * 32) {
@@ -1398,6 +1401,9 @@ __global__ void __launch_bounds__(32)
     checkSpeculation(L, i, a, t_free, cleanup, bound, st);
   }
   flushCounts(k, st);
+#ifdef RB_TIMELINE
+  if (lane == 0) atomicMax(&g_tl_end[10][blockIdx.x & 31], tlNow());  // lane-per-cell part's end
+#endif
 }
 
 // ------------------------------------------------------------- K5/K6 rays

@@ -14,7 +14,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SLOTS = ["shift", "ingest", "sort rowscan (both)", "sort scatter 0", "sort scatter 1", "drift vote (s2)",
-         "side sweep / offset (s2)", "short fold", "long fold (s2)", "classify", "classify retry",
+         "side sweep / offset (s2)", "short fold", "long fold (s2)", "long fold: warp-per-cell end", "long fold: lane-per-cell end",
          "jump grid", "ray pass 1", "ray pass 1 retry", "ray tail", "cells"]
 
 CHILD = r'''
@@ -56,7 +56,9 @@ def main():
     for l in lines[-10:]:
         v = [int(x) for x in l]
         t0 = v[2]  # ingest start
-        rows.append([(v[2 * k] - t0, v[2 * k + 1] - t0) if v[2 * k + 1] else None for k in range(len(SLOTS))])
+        # (slots recorded at their end only have no start: shown as starting at their end)
+        rows.append([((v[2 * k] if v[2 * k] != 2**64 - 1 else v[2 * k + 1]) - t0, v[2 * k + 1] - t0)
+                     if v[2 * k + 1] else None for k in range(len(SLOTS))])
     print(f"{name}: median over the last {len(rows)} frames (us from the ingest start)")
     counts = [l for l in r.stderr.splitlines() if l.startswith("TLC ")]
     if counts:
