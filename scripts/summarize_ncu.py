@@ -18,7 +18,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 # kernel -> bench.py kernel group (the event-timed phases of integrateScanDevice)
-GROUP = {"k_ingest": "ingest", "k_drift_finalize": "drift", "k_apply_offset": "drift",
+GROUP = {"k_ingest": "ingest", "k_ingest_tma": "ingest", "k_drift_finalize": "drift", "k_apply_offset": "drift",
+         "k_side_prep": "drift", "k_fuse_list": "fusion", "k_jump_grid": "rays",
          "k_sort_rowscan": "sort", "k_sort_scatter": "sort", "k_fuse": "fusion", "k_fuse_heavy": "rays",
          "k_classify": "rays", "k_rays_pass1": "rays", "k_remove": "rays", "k_rays_pass2": "rays", "k_rays_tail": "rays",
          "k_cells": "cells", "k_shift": "shift"}
@@ -37,11 +38,17 @@ def main(rep, launches, tag):
     h, units, rows = raw_rows(rep)
     col = {n: i for i, n in enumerate(h)}
 
+    # byte counters in MB whatever unit ncu picked for the column (byte / Kbyte / Mbyte / Gbyte)
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+
     def val(r, n):
         try:
-            return float(r[col[n]].replace(",", ""))
+            v = float(r[col[n]].replace(",", ""))
         except (KeyError, ValueError):
             return None
+        if n.startswith("dram__bytes"):
+            v *= scale.get(units[col[n]], 1.0)
+        return v
 
     stall_cols = [n for n in h if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
     peaks = ROOT / "MEASURED_PEAKS.json"
