@@ -46,6 +46,9 @@ constexpr int kThreads = 256;
 // Graph frames of at least kGraphMinPoints points (graph_mode 2); from
 // kGraphHeadPoints on, the frame's head is launched directly and only the
 // rest captured (its ingest then covers the capture and graph update).
+#ifndef RB_CELLS_SKIP
+#define RB_CELLS_SKIP 1  // k_cells blocks whose tile has no valid cell and no points skip the staging
+#endif
 #ifndef RB_P1_JUMP
 #define RB_P1_JUMP 1  // pass-1 rays jump over the blocks their heights clear (pass1Jump)
 #endif
@@ -2523,6 +2526,21 @@ __global__ void __launch_bounds__(kTileX* kTileY)
   const int W = a.g.W, H = a.g.H;
   const int c0 = blockIdx.x * kTileX - halo, r0 = blockIdx.y * kTileY - halo;
   const int tid = threadIdx.y * kTileX + threadIdx.x;
+  if (RB_CELLS_SKIP && !a.scrub) {
+    // A tile with no valid cell and no cell with points this scan has nothing
+    // to do (no normals, no removal or clearance, no counters to reset): it
+    // skips the halo staging.
+    const int rr = blockIdx.y * kTileY + threadIdx.y, cc = blockIdx.x * kTileX + threadIdx.x;
+    bool busy = false;
+    if (rr < H && cc < W) {
+      const size_t j = static_cast<size_t>(rr) * W + cc;
+      busy = L.valid[j] != 0 || count[j] != 0;
+    }
+    if (!__syncthreads_or(busy)) {
+      handOverStats(a, st, static_cast<unsigned>(tid));
+      return;
+    }
+  }
   for (int q = tid; q < tw * th; q += kTileX * kTileY) {
     double e;
     sv[q] = stageCell(L, a, r0 + q / tw, c0 + q % tw, e);
