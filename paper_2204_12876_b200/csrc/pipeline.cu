@@ -9,10 +9,15 @@
 //                        (+ drift vote mean, fixed-order, in the last block)
 //   K2  radix sort       stable LSD sort of (cell, point) -> per-cell segments
 //                        in scan order; exclusive scan count -> segment start
-//   K3  k_fuse           drift offset (k_apply_offset) + gated Kalman fold, one
-//                        thread per cell (long cells: k_fuse_heavy, side stream)
-//   K5  k_classify       ray class + probe word per cell; k_jump_grid: the
-//                        16x16-block bounds the rays jump over
+//       (stream 2, under the sort) k_drift_finalize + k_side_prep: drift
+//                        offset, fold lists, ray class + probe word per cell
+//                        (cells with points "none", exact: DESIGN.md §5.1)
+//   K3  gated Kalman fold: the removal candidates with points first
+//                        (k_fuse_list, usually none); the short cells (stream 3,
+//                        k_fuse_list) and the long ones (stream 2, k_fuse_heavy)
+//                        beside the ray pass. (Frames without a ray pass:
+//                        k_fuse, one thread per cell.)
+//   K5  k_jump_grid      the 16x16-block bounds the rays jump over
 //       k_rays_pass1     exact 2-D DDA per kept point (jumping over cleared
 //                        blocks): bounds of invalid cells, k* = first removing
 //                        ray per candidate cell
