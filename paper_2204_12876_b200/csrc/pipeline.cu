@@ -51,6 +51,13 @@ constexpr int kThreads = 256;
 // Graph frames of at least kGraphMinPoints points (graph_mode 2); from
 // kGraphHeadPoints on, the frame's head is launched directly and only the
 // rest captured (its ingest then covers the capture and graph update).
+#ifndef RB_SIDE_JUMP
+#define RB_SIDE_JUMP 1  // the jump grid built on stream 2 right after the side sweep
+#endif
+#ifndef RB_SIDE_JUMP_CELLS
+#define RB_SIDE_JUMP_CELLS 524288  // ... on maps of at least this many cells
+#endif
+constexpr size_t kSideJumpCells = RB_SIDE_JUMP_CELLS;
 #ifndef RB_CELLS_SKIP
 #define RB_CELLS_SKIP 1  // k_cells blocks whose tile has no valid cell and no points skip the staging
 #endif
@@ -1232,7 +1239,15 @@ __global__ void __launch_bounds__(kThreads)
     // (classify: the cells without points, and the long cells speculatively;
     // the short-cell fold classifies the cells it folds)
     if (pre_list != nullptr) {
-      if (in && !pre) classifyCell(L, i, cnt > 0, ca, cls, probe, kstar);
+      if (in && !pre) {
+        classifyCell(L, i, cnt > 0, ca, cls, probe, kstar);
+      } else if (pre && RB_SIDE_JUMP && n >= kSideJumpCells) {
+        // provisional probe word "candidate" (the jump grid built on this
+        // stream then never jumps the cell's block); the candidates' fold
+        // writes the real class before the ray pass reads it
+        const size_t r = i / static_cast<unsigned>(ca.W);
+        probe[i + static_cast<size_t>(ca.W) + 3 + 2 * r] = probeWord(kClsCandidate, 0.0);
+      }
     } else if (classify && in && (cnt == 0 || cnt > heavy)) {
       classifyCell(L, i, cnt > heavy, ca, cls, probe, kstar);
     }
@@ -2643,7 +2658,8 @@ struct Frame {
   bool classified = false;  // k_fuse wrote this frame's ray classes
   bool drift_join = false;  // phaseDrift(side) ran on stream2: join before the fold
   bool prepped = false;     // k_side_prep classified the cells without points
-  bool presplit = false;    // RB_PRESPLIT: candidates folded before the ray pass, the rest beside it
+  bool presplit = false;
+  bool jump_done = false;   // k_jump_grid ran on stream 2 after the side sweep (RB_SIDE_JUMP)    // RB_PRESPLIT: candidates folded before the ray pass, the rest beside it
   bool lists_built = false; // k_side_prep queued the long cells (the long fold starts after the sort)
   // Removal of k* < inf cells: in k_cells (fold_remove, set when the ray pass
   // ran with cleanup on), or by k_remove right after the ray pass
@@ -2913,6 +2929,15 @@ void phaseDrift(Frame& f, uint32_t N, bool side = false) {
     } else
       k_apply_offset<<<streamGrid(f.ncell), kThreads, 0, m.stream2>>>(m.cur, f.ncell, m.drift_offset);
     ++f.launches;
+    // the jump grid under the sort as well, on large maps (on 400^2 / 500^2
+    // maps the sort is too short to hide it: C2 / C3 +8 %)
+    if (RB_SIDE_JUMP && RB_P1_JUMP && f.presplit && f.ncell >= kSideJumpCells) {
+      const int jw = (f.g.W + kJumpBlk - 1) / kJumpBlk, jh = (f.g.H + kJumpBlk - 1) / kJumpBlk;
+      k_jump_grid<<<static_cast<unsigned>((static_cast<std::size_t>(jw) * jh * 32 + kThreads - 1) / kThreads),
+                    kThreads, 0, m.stream2>>>(static_cast<const ProbeT*>(m.probe), f.g.W, f.g.H, m.jgrid, jw, jh);
+      ++f.launches;
+      f.jump_done = true;
+    }
     checkCuda(cudaEventRecord(m.ev_djoin, m.stream2), "event");
     f.drift_join = true;
     f.lists_built = lists;
@@ -3100,9 +3125,11 @@ void phaseRaysPass1(Frame& f, uint32_t N, uint32_t ray_base, bool tail = false) 
       RayArgs rj = ra;
       if (RB_P1_JUMP) {  // the jump grid of this frame's probe words (pass1Jump)
         const int jw = (f.g.W + kJumpBlk - 1) / kJumpBlk, jh = (f.g.H + kJumpBlk - 1) / kJumpBlk;
-        launchPdl(k_jump_grid, static_cast<unsigned>((static_cast<std::size_t>(jw) * jh * 32 + kThreads - 1) / kThreads),
-                  kThreads, 0, s, static_cast<const ProbeT*>(m.probe), f.g.W, f.g.H, m.jgrid, jw, jh);
-        ++f.launches;
+        if (!f.jump_done) {
+          launchPdl(k_jump_grid, static_cast<unsigned>((static_cast<std::size_t>(jw) * jh * 32 + kThreads - 1) / kThreads),
+                    kThreads, 0, s, static_cast<const ProbeT*>(m.probe), f.g.W, f.g.H, m.jgrid, jw, jh);
+          ++f.launches;
+        }
         rj.jgrid = m.jgrid;
         rj.jw = jw;
         rj.jh = jh;
