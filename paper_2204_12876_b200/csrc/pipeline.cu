@@ -348,6 +348,10 @@ struct IngestArgs {
 // drift vote against the pre-fusion map, per-cell point count.
 // One 256-point tile of the ingest: the points k = k_base + tile * 256 + thread,
 // read from the staged copy `sx` in shared memory (null: from xyz directly).
+struct IngestCounts {  // a block's out-of-range / excluded / out-of-map points (thread 0)
+  unsigned oor = 0, exc = 0, oom = 0;
+};
+
 __device__ __forceinline__ void ingestTile(const double* __restrict__ xyz, uint32_t n, const IngestArgs& a,
                                            const Layers& L, int32_t* __restrict__ count,
                                            double* __restrict__ px, double* __restrict__ py,
@@ -356,7 +360,8 @@ __device__ __forceinline__ void ingestTile(const double* __restrict__ xyz, uint3
                                            double* __restrict__ drift_part, int* __restrict__ drift_npart,
                                            uint32_t* __restrict__ tc0, uint32_t pitch, uint32_t dmask,
                                            int count_cells, DevStats* st, uint32_t k_base,
-                                           uint32_t in_base, uint32_t tile, const double* sx) {
+                                           uint32_t in_base, uint32_t tile, const double* sx,
+                                           IngestCounts& stat_acc) {
   const uint32_t WH = static_cast<uint32_t>(a.g.W) * static_cast<uint32_t>(a.g.H);
   const uint32_t k = k_base + tile * kThreads + threadIdx.x;
   int oor = 0, exc = 0, oom = 0, dn = 0;
@@ -432,37 +437,41 @@ __device__ __forceinline__ void ingestTile(const double* __restrict__ xyz, uint3
   // Fixed-shape block reduction: deterministic drift partial per block.
   __shared__ double s_sum[kThreads / 32];
   __shared__ int s_cnt[4][kThreads / 32];
+  // (the three rejection counters packed in 10-bit fields: at most 256 per tile)
   ds = warpSum(ds);
   dn = warpSum(dn);
-  oor = warpSum(oor);
-  exc = warpSum(exc);
-  oom = warpSum(oom);
+  const int packed = warpSum(oor | (exc << 10) | (oom << 20));
   const int warp = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     s_sum[warp] = ds;
     s_cnt[0][warp] = dn;
-    s_cnt[1][warp] = oor;
-    s_cnt[2][warp] = exc;
-    s_cnt[3][warp] = oom;
+    s_cnt[1][warp] = packed;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double bs = s_sum[0];
-    int c0 = s_cnt[0][0], c1 = s_cnt[1][0], c2 = s_cnt[2][0], c3 = s_cnt[3][0];
+    int c0 = s_cnt[0][0], c1 = s_cnt[1][0];
     for (int w = 1; w < kThreads / 32; ++w) {
       bs += s_sum[w];
       c0 += s_cnt[0][w];
       c1 += s_cnt[1][w];
-      c2 += s_cnt[2][w];
-      c3 += s_cnt[3][w];
     }
     drift_part[k_base / kThreads + tile] = bs;
     drift_npart[k_base / kThreads + tile] = c0;
-    if (c1) atomicAdd(&st->out_of_range, static_cast<unsigned long long>(c1));
-    if (c2) atomicAdd(&st->excluded, static_cast<unsigned long long>(c2));
-    if (c3) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c3));
+    // the block's running counters (flushed once per block: flushIngestStats)
+    stat_acc.oor += c1 & 1023;
+    stat_acc.exc += (c1 >> 10) & 1023;
+    stat_acc.oom += (c1 >> 20) & 1023;
   }
   __syncthreads();  // (the block's reduction arrays are reused by its next tile)
+}
+
+// Thread 0: the block's rejection counters to the frame stats, once per block.
+__device__ __forceinline__ void flushIngestStats(const IngestCounts& c, DevStats* st) {
+  if (threadIdx.x != 0) return;
+  if (c.oor) atomicAdd(&st->out_of_range, static_cast<unsigned long long>(c.oor));
+  if (c.exc) atomicAdd(&st->excluded, static_cast<unsigned long long>(c.exc));
+  if (c.oom) atomicAdd(&st->out_of_map, static_cast<unsigned long long>(c.oom));
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -497,9 +506,11 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
   }
+  IngestCounts stat_acc;
   ingestTile(xyz, n, a, L, count, px, py, pz, pvar, key, kept, drift_part, drift_npart, tc0, pitch,
              dmask, count_cells, st, k_base, in_base, blockIdx.x,
-             staged ? reinterpret_cast<const double*>(s_xyz) : nullptr);
+             staged ? reinterpret_cast<const double*>(s_xyz) : nullptr, stat_acc);
+  flushIngestStats(stat_acc, st);
 #if RB_INGEST_FINALIZE
   if (a.drift_blocks == 0) return;
   // The last block of the frame's ingest (over all chunk launches) reduces the
@@ -563,6 +574,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   uint32_t it = 0;
+  IngestCounts stat_acc;
   for (uint32_t t = blockIdx.x; t < ntl; t += gridDim.x, ++it) {
     const int b = static_cast<int>(it & 1u);
     // the other buffer is free: every thread finished the previous tile (the
@@ -581,8 +593,9 @@ __global__ void __launch_bounds__(kThreads)
       sx = s_buf[b];
     }
     ingestTile(xyz, n, a, L, count, px, py, pz, pvar, key, kept, drift_part, drift_npart, tc0, pitch,
-               dmask, count_cells, st, k_base, in_base, t, sx);
+               dmask, count_cells, st, k_base, in_base, t, sx, stat_acc);
   }
+  flushIngestStats(stat_acc, st);
 }
 
 // ------------------------------------------------------ drift (one block)
