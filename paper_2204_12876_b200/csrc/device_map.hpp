@@ -50,6 +50,7 @@ struct DevStats {
   unsigned long long heavy_cells;     // cells folded by k_fuse_heavy, one per lane
   unsigned long long vheavy_cells;    // cells folded by k_fuse_heavy, one per warp
   unsigned long long light_cells;     // cells folded by k_fuse_list (lists built by k_side_prep)
+  unsigned long long light2_cells;    // ... of them, from the far end of the list (RB_LIGHT_SPLIT)
   unsigned long long pre_cells;       // cells folded before the ray pass (RB_PRESPLIT)
   double drift_offset;                // applied offset (0 when not applied)
   int drift_n;

@@ -61,6 +61,9 @@ constexpr size_t kSideJumpCells = RB_SIDE_JUMP_CELLS;
 #ifndef RB_CELLS_SKIP
 #define RB_CELLS_SKIP 1  // k_cells blocks whose tile has no valid cell and no points skip the staging
 #endif
+#ifndef RB_LIGHT_SPLIT
+#define RB_LIGHT_SPLIT 12  // short-fold list: cells of <= this many points first, the rest from the far end
+#endif
 #ifndef RB_P1_JUMP
 #define RB_P1_JUMP 1  // pass-1 rays jump over the blocks their heights clear (pass1Jump)
 #endif
@@ -1211,6 +1214,17 @@ __device__ __forceinline__ void appendCell(bool pred, size_t i, uint32_t* list, 
   if (pred) list[base + __popc(b & ((1u << lane) - 1u))] = static_cast<uint32_t>(i);
 }
 
+// appendCell filling the list downwards from `last`.
+__device__ __forceinline__ void appendCellBack(bool pred, size_t i, uint32_t* last, unsigned long long* n) {
+  const int lane = threadIdx.x & 31;
+  const unsigned b = __ballot_sync(0xffffffffu, pred);
+  if (!b) return;
+  unsigned base = 0;
+  if (lane == __ffs(b) - 1) base = static_cast<unsigned>(atomicAdd(n, static_cast<unsigned long long>(__popc(b))));
+  base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+  if (pred) *(last - (base + __popc(b & ((1u << lane) - 1u)))) = static_cast<uint32_t>(i);
+}
+
 // Second-stream sweep after the ingest (RB_EARLY_HEAVY): the drift offset
 // (off_p null: none) and the long-cell lists from the per-cell counts, so the
 // long-cell fold can start as soon as the sort is done, beside k_fuse (which
@@ -1247,7 +1261,14 @@ __global__ void __launch_bounds__(kThreads)
             (L.nx[i] != 0.0 || L.ny[i] != 0.0 || L.nz[i] != 0.0);
     const int lc = pre ? 0 : cnt;
     if (heavy_list != nullptr) appendHeavy(lc, heavy, i, heavy_list, vheavy_list, st);
-    if (light_list != nullptr) appendCell(lc > 0 && lc <= heavy, i, light_list, &st->light_cells);
+    if (light_list != nullptr) {
+      // RB_LIGHT_SPLIT: cells of up to that many points from the front of the
+      // list, longer ones from its far end, so a fold warp's lanes get folds of
+      // similar length
+      const int split = RB_LIGHT_SPLIT > 0 ? RB_LIGHT_SPLIT : heavy;
+      appendCell(lc > 0 && lc <= split, i, light_list, &st->light_cells);
+      if (RB_LIGHT_SPLIT > 0) appendCellBack(lc > split && lc <= heavy, i, light_list + n - 1, &st->light2_cells);
+    }
     if (pre_list != nullptr) appendCell(pre, i, pre_list, &st->pre_cells);
     // (classify: the cells without points, and the long cells speculatively;
     // the short-cell fold classifies the cells it folds)
@@ -1287,7 +1308,8 @@ __device__ __forceinline__ void checkSpeculation(const Layers& L, size_t i, cons
 #endif
 __global__ void __launch_bounds__(RB_FUSE_LIST_THREADS)
     k_fuse_list(Layers L, const int32_t* __restrict__ count, const uint32_t* __restrict__ list,
-                const unsigned long long* n_list, const uint32_t* __restrict__ start,
+                const unsigned long long* n_list, const unsigned long long* n_back, size_t list_len,
+                const uint32_t* __restrict__ start,
                 const double* __restrict__ spz, const double* __restrict__ spv, FuseArgs a,
                 DevStats* st, int classify, ClassArgs ca, uint8_t* __restrict__ cls,
                 ProbeT* __restrict__ probe, int32_t* __restrict__ kstar) {
@@ -1296,10 +1318,12 @@ __global__ void __launch_bounds__(RB_FUSE_LIST_THREADS)
   pdlTrigger();
   // classify 1: classify each folded cell; 2: it was classified "none" before
   // the fold (RB_PRESPLIT) -- check that (a wrong class retries the ray pass)
-  const unsigned total = static_cast<unsigned>(*n_list);
+  // n_back (not null): n_back entries more at the far end of the list
+  const unsigned front = static_cast<unsigned>(*n_list);
+  const unsigned total = front + (n_back != nullptr ? static_cast<unsigned>(*n_back) : 0u);
   FoldCounts k;
   for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
-    const uint32_t i = list[q];
+    const uint32_t i = q < front ? list[q] : list[list_len - 1 - (q - front)];
     foldCell(L, i, count[i], start, spz, spv, a, st, k);
     if (classify == 1) classifyCell(L, i, false, ca, cls, probe, kstar);
     if (classify == 2) checkSpeculation(L, i, a, ca.t_free, ca.cleanup, ca.bound, st);
@@ -3089,13 +3113,15 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     launchPdl(k_fuse_list, 148u, RB_PRE_THREADS, 0, s, m.cur, static_cast<const int32_t*>(m.count),
               static_cast<const uint32_t*>(m.heavy + 3 * f.ncell),
               static_cast<const unsigned long long*>(&m.stats->pre_cells),
-              static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
+              static_cast<const unsigned long long*>(nullptr), f.ncell, static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
               static_cast<const double*>(m.spv), fa, m.stats, 1, ca, m.cls, m.probe, m.kstar);
     if (RB_B_AFTER_A) checkCuda(cudaEventRecord(m.ev_sfork, s), "event");
     checkCuda(cudaStreamWaitEvent(m.stream3, m.ev_sfork, 0), "stream wait");
     k_fuse_list<<<148u * RB_SFOLD_BLOCKS, RB_FUSE_LIST_THREADS, 0, m.stream3>>>(
         m.cur, static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
-        static_cast<const unsigned long long*>(&m.stats->light_cells), static_cast<const uint32_t*>(m.start),
+        static_cast<const unsigned long long*>(&m.stats->light_cells),
+        RB_LIGHT_SPLIT > 0 ? static_cast<const unsigned long long*>(&m.stats->light2_cells) : nullptr, f.ncell,
+        static_cast<const uint32_t*>(m.start),
         static_cast<const double*>(m.spz), static_cast<const double*>(m.spv), fa, m.stats, 2, ca, m.cls,
         m.probe, m.kstar);
     checkCuda(cudaEventRecord(m.ev_sjoin, m.stream3), "event");
@@ -3104,7 +3130,8 @@ void phaseSortFuse(Frame& f, const uint32_t* keys, uint32_t N, const double* z, 
     launchPdl(k_fuse_list, 148u * RB_FUSE_LIST_BLOCKS, RB_FUSE_LIST_THREADS, 0, s, m.cur,
               static_cast<const int32_t*>(m.count), static_cast<const uint32_t*>(m.heavy + 2 * f.ncell),
               static_cast<const unsigned long long*>(&m.stats->light_cells),
-              static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
+              RB_LIGHT_SPLIT > 0 ? static_cast<const unsigned long long*>(&m.stats->light2_cells) : nullptr,
+              f.ncell, static_cast<const uint32_t*>(m.start), static_cast<const double*>(m.spz),
               static_cast<const double*>(m.spv), fa, m.stats, f.prepped ? 1 : 0, ca, m.cls, m.probe,
               m.kstar);
   else
