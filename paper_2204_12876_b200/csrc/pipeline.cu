@@ -62,7 +62,7 @@ constexpr size_t kSideJumpCells = RB_SIDE_JUMP_CELLS;
 #define RB_CELLS_SKIP 1  // k_cells blocks whose tile has no valid cell and no points skip the staging
 #endif
 #ifndef RB_LIGHT_SPLIT
-#define RB_LIGHT_SPLIT 12  // short-fold list: cells of <= this many points first, the rest from the far end
+#define RB_LIGHT_SPLIT 32  // short-fold list: cells of <= this many points first, the rest from the far end
 #endif
 #ifndef RB_P1_JUMP
 #define RB_P1_JUMP 1  // pass-1 rays jump over the blocks their heights clear (pass1Jump)
@@ -1026,7 +1026,7 @@ constexpr int kFoldBatch = 8;
 
 // Cells with more points than this fold on the side stream (k_fuse_heavy).
 #ifndef RB_HEAVY_CELL
-#define RB_HEAVY_CELL 32  // (16 / 24 / 48 / 64 measured slower with the early long fold)
+#define RB_HEAVY_CELL 160  // = RB_VHEAVY_CELL: no lane-per-cell long fold
 #endif
 constexpr int kHeavyCell = RB_HEAVY_CELL;
 #ifndef RB_HEAVY_BLOCKS
