@@ -1030,7 +1030,7 @@ constexpr int kFoldBatch = 8;
 #endif
 constexpr int kHeavyCell = RB_HEAVY_CELL;
 #ifndef RB_HEAVY_BLOCKS
-#define RB_HEAVY_BLOCKS 512
+#define RB_HEAVY_BLOCKS 256
 #endif
 constexpr int kHeavyBlocks = RB_HEAVY_BLOCKS;  // one warp each
 
